@@ -1,0 +1,143 @@
+/*
+ * forestcoll.h — C ABI of the B200-native ForestColl schedule executor.
+ *
+ * The reference (`collsched` 0.1.0, /root/reference/pkg) ships a schedule
+ * *generator* and no executor: runtime execution is a stated non-goal
+ * (the hardware criterion is a bare pytest.skip at
+ * pkg/tests/test_acceptance.py:159-163).  Its public boundary for this path is
+ * the `Schedule` forest (pkg/src/collsched/schedule.py:31-81) and its JSON wire
+ * format (schedule.py:348-448), produced by `generate()` (pipeline.py:43-78).
+ * This library is the additive executor behind that boundary.  Entry points
+ * are NCCL-shaped so a binding (ctypes / cffi) can call
+ * them exactly where the reference's users would call a collective.
+ *
+ * Each entry point below names the reference interface it consumes/replaces:
+ *
+ *  fc_comm_init / fc_comm_export / fc_comm_connect
+ *      one communicator per rank process; the reference has no runtime
+ *      (SPEC.md:8).  Peer workspaces (flags + reduction scratch) are mapped
+ *      over NVLink with CUDA IPC handles exchanged by the caller.
+ *  fc_comm_init_virtual
+ *      all N ranks of one forest on a single device (one cooperative grid),
+ *      the single-GPU test mode of SURVEY.md §4.
+ *  fc_plan_load
+ *      consumes the lowered `Schedule` forest (schedule.py:31-81; lowering by
+ *      paper_2402_06787_b200/compiler.py): one table per collective —
+ *      allgather (schedule.py:88-129), reduce_scatter
+ *      (reverse_for_reduce_scatter, schedule.py:166-174), allreduce
+ *      (combine_allreduce, schedule.py:177-211).
+ *  fc_allgather / fc_reduce_scatter / fc_allreduce (+ _multi variants)
+ *      execute the forest: "a 1/k shard of data is broadcast along each
+ *      out-tree"; RS/AR per PAPER.md:1036.
+ *  fc_buffer_export / fc_buffer_register
+ *      zero-copy peer mapping of caller-owned output buffers.
+ *  fc_last_error / fc_comm_check
+ *      error reporting; the Python wrapper maps codes onto the reference's
+ *      CollschedError hierarchy (errors.py:10-140).
+ *
+ * Conventions: every function returns 0 (FC_SUCCESS) or an FC_ERR_* code;
+ * pointers are plain device pointers; `stream` is a cudaStream_t passed as
+ * void*; calls are stream-ordered and asynchronous; a communicator is not
+ * re-entrant across host threads and all calls on one communicator must be
+ * issued in the same order on every rank (NCCL semantics).
+ */
+#ifndef FORESTCOLL_H_
+#define FORESTCOLL_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FC_MAX_RANKS 16
+
+/* status codes */
+#define FC_SUCCESS 0
+#define FC_ERR_INVALID_ARG 1
+#define FC_ERR_CUDA 2
+#define FC_ERR_UNSUPPORTED 3
+#define FC_ERR_NOT_REGISTERED 4
+#define FC_ERR_PLAN 5
+#define FC_ERR_DEVICE 6 /* device-side failure (flag wait timed out) */
+
+/* collectives (plan slots) */
+#define FC_ALLGATHER 0
+#define FC_REDUCE_SCATTER 1
+#define FC_ALLREDUCE 2
+
+/* dtypes: numbering follows ncclDataType_t */
+#define FC_INT8 0
+#define FC_UINT8 1
+#define FC_INT32 2
+#define FC_UINT32 3
+#define FC_INT64 4
+#define FC_UINT64 5
+#define FC_FLOAT16 6
+#define FC_FLOAT32 7
+#define FC_FLOAT64 8
+#define FC_BFLOAT16 9
+
+/* reduction ops: numbering follows ncclRedOp_t (only SUM is implemented) */
+#define FC_SUM 0
+
+/* options for fc_comm_set_option */
+#define FC_OPT_CTAS_PER_RANK 1 /* CTAs per rank (default 32 real, 16 virtual) */
+#define FC_OPT_CHUNK_MAX 2     /* max bytes per pipeline chunk (default 512 KiB) */
+#define FC_OPT_CHUNK_MIN 3     /* min bytes per pipeline chunk (default 8 KiB) */
+#define FC_OPT_ITEMS_PER_WORKER 4 /* target work items per worker (default 4) */
+#define FC_OPT_TIMEOUT_MS 5    /* device flag-wait timeout (default 10000 ms) */
+
+typedef struct fc_comm fc_comm_t;
+
+const char* fc_version(void);
+size_t fc_handle_bytes(void);
+
+int fc_comm_init(int rank, int nranks, int device, size_t scratch_bytes,
+                 fc_comm_t** out);
+int fc_comm_init_virtual(int nranks, int device, size_t scratch_bytes,
+                         fc_comm_t** out);
+int fc_comm_export(fc_comm_t* comm, void* handle);
+int fc_comm_connect(fc_comm_t* comm, const void* handles);
+int fc_comm_set_option(fc_comm_t* comm, int option, long long value);
+int fc_comm_get_option(fc_comm_t* comm, int option, long long* value);
+int fc_comm_check(fc_comm_t* comm, int* device_error);
+int fc_comm_destroy(fc_comm_t* comm);
+const char* fc_last_error(const fc_comm_t* comm);
+
+int fc_buffer_export(fc_comm_t* comm, const void* ptr, size_t bytes,
+                     void* handle);
+int fc_buffer_register(fc_comm_t* comm, const void* ptr, size_t bytes,
+                       const void* handles);
+int fc_buffer_deregister(fc_comm_t* comm, const void* ptr);
+
+int fc_plan_load(fc_comm_t* comm, int collective, const int32_t* table,
+                 size_t nwords);
+
+int fc_allgather(fc_comm_t* comm, const void* send, void* recv,
+                 size_t sendcount, int dtype, void* stream);
+int fc_reduce_scatter(fc_comm_t* comm, const void* send, void* recv,
+                      size_t recvcount, int dtype, int op, void* stream);
+int fc_allreduce(fc_comm_t* comm, const void* send, void* recv, size_t count,
+                 int dtype, int op, void* stream);
+
+/* one send/recv pointer per local rank (nranks entries for a virtual comm) */
+int fc_allgather_multi(fc_comm_t* comm, const void* const* sends,
+                       void* const* recvs, size_t sendcount, int dtype,
+                       void* stream);
+int fc_reduce_scatter_multi(fc_comm_t* comm, const void* const* sends,
+                            void* const* recvs, size_t recvcount, int dtype,
+                            int op, void* stream);
+int fc_allreduce_multi(fc_comm_t* comm, const void* const* sends,
+                       void* const* recvs, size_t count, int dtype, int op,
+                       void* stream);
+
+/* statistics of the last collective call (launches, chunks, bytes) */
+int fc_last_call_info(const fc_comm_t* comm, long long* info, int ninfo);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FORESTCOLL_H_ */

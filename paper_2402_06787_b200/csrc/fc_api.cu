@@ -1,0 +1,664 @@
+// Host side of the C ABI (include/forestcoll.h): communicators, NVLink peer
+// mapping through CUDA IPC, plan tables, chunk planning and launches.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "fc_internal.h"
+
+namespace {
+
+constexpr uint32_t kCommMagic = 0x4d4d4346;  // 'FCMM'
+constexpr uint32_t kBufMagic = 0x46554246;   // 'FBUF'
+constexpr int kMaxC = 512;                   // flag slots per tree / slot (chunks per launch)
+constexpr int kTreeCap = 256;
+constexpr int kSlotCap = 512;
+constexpr size_t kCtlBytes = 256;
+
+struct CommBlob {
+  uint32_t magic;
+  int32_t rank, nranks, pad;
+  uint64_t ws_bytes, flags_off, flags_words, scratch_off, scratch_bytes;
+  cudaIpcMemHandle_t handle;
+};
+struct BufBlob {
+  uint32_t magic;
+  int32_t rank;
+  uint64_t offset, bytes;
+  cudaIpcMemHandle_t handle;
+};
+constexpr size_t kHandleBytes = 192;
+static_assert(sizeof(CommBlob) <= kHandleBytes, "blob size");
+static_assert(sizeof(BufBlob) <= kHandleBytes, "blob size");
+
+struct Mapping {
+  cudaIpcMemHandle_t handle;
+  char* base;
+};
+struct Reg {
+  uintptr_t lo, hi;
+  char* peer[FC_MAXR];
+};
+struct Plan {
+  bool loaded = false;
+  int nranks = 0, k = 0, ntrees = 0, max_slot_units = 0, max_slots = 0, max_mult = 0;
+  long long active_total = 0;
+  int* d_tasks[FC_MAXR] = {};
+  int nact[FC_MAXR] = {}, nwait[FC_MAXR] = {};
+};
+
+typedef CUresult (*PFN_getRange)(CUdeviceptr*, size_t*, CUdeviceptr);
+
+}  // namespace
+
+struct fc_comm {
+  int rank = 0, nranks = 0, device = 0, virt = 0, nlocal = 0, connected = 0;
+  size_t ws_bytes = 0, flags_off = 0, flags_words = 0, scratch_off = 0, scratch_bytes = 0;
+  char* ws[FC_MAXR] = {};
+  bool own[FC_MAXR] = {};
+  std::vector<Mapping> maps;
+  std::vector<Reg> regs;
+  Plan plans[3];
+  int ctas_per_rank = 32;
+  long long chunk_max = 512 << 10, chunk_min = 8 << 10, items_per_worker = 4;
+  long long timeout_ms = 10000;
+  std::string err;
+  long long info[8] = {};
+};
+
+namespace {
+
+int fail(fc_comm* c, int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  if (c) c->err = buf;
+  return code;
+}
+
+#define FC_CUDA(c, call)                                                                 \
+  do {                                                                                   \
+    cudaError_t e_ = (call);                                                             \
+    if (e_ != cudaSuccess)                                                               \
+      return fail((c), FC_ERR_CUDA, "%s failed: %s", #call, cudaGetErrorString(e_));    \
+  } while (0)
+
+int esize_of(int dtype) {
+  switch (dtype) {
+    case FC_INT8: case FC_UINT8: return 1;
+    case FC_FLOAT16: case FC_BFLOAT16: return 2;
+    case FC_INT32: case FC_UINT32: case FC_FLOAT32: return 4;
+    case FC_INT64: case FC_UINT64: case FC_FLOAT64: return 8;
+    default: return 0;
+  }
+}
+
+int reduce_kind(int dtype) {
+  switch (dtype) {
+    case FC_FLOAT32: return FC_FLOAT32;
+    case FC_BFLOAT16: return FC_BFLOAT16;
+    case FC_FLOAT16: return FC_FLOAT16;
+    case FC_INT32: case FC_UINT32: return FC_INT32;
+    default: return -1;
+  }
+}
+
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+int alloc_workspace(fc_comm* c, char** out) {
+  FC_CUDA(c, cudaMalloc((void**)out, c->ws_bytes));
+  FC_CUDA(c, cudaMemset(*out, 0, c->scratch_off));
+  return FC_SUCCESS;
+}
+
+int setup_layout(fc_comm* c, size_t scratch_bytes) {
+  c->flags_off = kCtlBytes;
+  c->flags_words = FC_READY_WORDS + (size_t)(kTreeCap + kSlotCap) * kMaxC;
+  c->scratch_off = align_up(c->flags_off + c->flags_words * 4, 4096);
+  c->scratch_bytes = align_up(scratch_bytes, 4096);
+  c->ws_bytes = c->scratch_off + c->scratch_bytes;
+  return FC_SUCCESS;
+}
+
+PFN_getRange get_range_fn() {
+  static PFN_getRange fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (PFN_getRange)p;
+  }
+  return fn;
+}
+
+int open_mapping(fc_comm* c, const cudaIpcMemHandle_t& h, char** base) {
+  for (auto& m : c->maps)
+    if (memcmp(&m.handle, &h, sizeof(h)) == 0) {
+      *base = m.base;
+      return FC_SUCCESS;
+    }
+  void* p = nullptr;
+  FC_CUDA(c, cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+  c->maps.push_back(Mapping{h, (char*)p});
+  *base = (char*)p;
+  return FC_SUCCESS;
+}
+
+const Reg* find_reg(const fc_comm* c, const void* p, size_t bytes) {
+  const uintptr_t a = (uintptr_t)p;
+  for (const auto& r : c->regs)
+    if (a >= r.lo && a + bytes <= r.hi) return &r;
+  return nullptr;
+}
+
+// Run one collective over this comm's local ranks.
+int run(fc_comm* c, int coll, const void* const* sends, void* const* recvs, size_t count,
+        int dtype, int op, void* stream) {
+  if (!c) return FC_ERR_INVALID_ARG;
+  if (!c->virt && !c->connected)
+    return fail(c, FC_ERR_INVALID_ARG, "communicator is not connected (fc_comm_connect)");
+  Plan& pl = c->plans[coll];
+  if (!pl.loaded) return fail(c, FC_ERR_PLAN, "no plan loaded for collective %d", coll);
+  const int es = esize_of(dtype);
+  if (!es) return fail(c, FC_ERR_INVALID_ARG, "unknown dtype %d", dtype);
+  int rd = FC_FLOAT32;
+  if (coll != FC_ALLGATHER) {
+    rd = reduce_kind(dtype);
+    if (rd < 0) return fail(c, FC_ERR_UNSUPPORTED, "dtype %d cannot be reduced", dtype);
+    if (op != FC_SUM) return fail(c, FC_ERR_UNSUPPORTED, "reduction op %d unsupported", op);
+  }
+  const int N = c->nranks;
+  long long S, stride, total;
+  if (coll == FC_ALLREDUCE) {
+    const long long a = FC_ALIGN / es;
+    S = ((long long)count + N - 1) / N;
+    S = (S + a - 1) / a * a;
+    stride = S;
+    total = (long long)count;
+  } else {
+    S = (long long)count;
+    stride = S;
+    total = S * N;
+  }
+  c->info[0] = c->info[1] = c->info[2] = c->info[3] = 0;
+  if (total == 0) return FC_SUCCESS;
+  for (int i = 0; i < c->nlocal; ++i)
+    if (!sends[i] || !recvs[i]) return fail(c, FC_ERR_INVALID_ARG, "null buffer");
+
+  FcParams P;
+  memset(&P, 0, sizeof(P));
+  P.nranks = N;
+  P.nlocal = c->nlocal;
+  P.k = pl.k;
+  for (int r = 0; r < N; ++r) {
+    P.scratch[r] = c->ws[r] + c->scratch_off;
+    P.flags[r] = (unsigned*)(c->ws[r] + c->flags_off);
+  }
+  for (int i = 0; i < c->nlocal; ++i) {
+    const int r = c->virt ? i : c->rank;
+    P.local_rank[i] = r;
+    P.tasks[i] = pl.d_tasks[i];
+    P.nactive[i] = pl.nact[i];
+    P.nwait[i] = pl.nwait[i];
+    P.ctl[i] = (FcCtl*)c->ws[r];
+    P.send[r] = (const char*)sends[i];
+    P.recv[r] = (char*)recvs[i];
+  }
+  if (!c->virt && coll != FC_REDUCE_SCATTER) {
+    const size_t need = (size_t)total * es;
+    const Reg* reg = find_reg(c, recvs[0], need);
+    if (!reg)
+      return fail(c, FC_ERR_NOT_REGISTERED,
+                  "output buffer %p (%zu bytes) is not registered (fc_buffer_register)",
+                  recvs[0], need);
+    const size_t delta = (uintptr_t)recvs[0] - reg->lo;
+    for (int r = 0; r < N; ++r) P.recv[r] = reg->peer[r] + delta;
+  }
+  P.shard_elems = S;
+  P.stride_elems = stride;
+  P.total_elems = total;
+  P.esize = es;
+  P.dtype = dtype;
+  P.op = op;
+  P.maxc = kMaxC;
+  P.ag_flag_off = FC_READY_WORDS;
+  P.rs_flag_off = FC_READY_WORDS + kTreeCap * kMaxC;
+  P.timeout_ns = c->timeout_ms * 1000000LL;
+  P.ctas_per_rank = c->ctas_per_rank;
+
+  // chunk plan: identical on every rank (depends on S, dtype, plan, options)
+  const long long slice_unit = (S + pl.k - 1) / pl.k * es;  // bytes per unit of multiplicity
+  const long long max_slice = slice_unit * pl.max_mult;
+  const long long workers = (long long)c->ctas_per_rank * 4;
+  const long long avg_active = std::max(1LL, pl.active_total / N);
+  long long n = (max_slice + c->chunk_max - 1) / c->chunk_max;
+  n = std::max(n, (c->items_per_worker * workers + avg_active - 1) / avg_active);
+  n = std::min(n, std::max(1LL, max_slice / std::max(1LL, c->chunk_min)));
+  n = std::max(n, 1LL);
+  if (n > (1LL << 30)) n = 1LL << 30;
+  long long W = std::min<long long>(n, kMaxC);
+  auto unit_for = [&](long long w) {
+    return (long long)align_up((size_t)((slice_unit * w + n - 1) / n), FC_ALIGN);
+  };
+  if (coll != FC_ALLGATHER) {
+    auto need = [&](long long w) {
+      return (long long)pl.max_slot_units * unit_for(w) + 2LL * FC_ALIGN * pl.max_slots;
+    };
+    while (W > 1 && need(W) > (long long)c->scratch_bytes) W = std::max(1LL, W / 2);
+    if (need(W) > (long long)c->scratch_bytes)
+      return fail(c, FC_ERR_INVALID_ARG,
+                  "scratch too small: %lld bytes needed per window, %zu available",
+                  need(W), c->scratch_bytes);
+    P.unit_bytes = unit_for(W);
+  }
+  P.nchunks = (int)n;
+  const int coop = c->virt ? 1 : 0;
+  int launches = 0, grid = 0;
+  for (long long c0 = 0; c0 < n; c0 += W) {
+    P.c0 = (int)c0;
+    P.c1 = (int)std::min(n, c0 + W);
+    const int e = fc_launch(P, rd, coop, stream, &grid);
+    if (e != 0)
+      return fail(c, FC_ERR_CUDA, "kernel launch failed: %s", cudaGetErrorString((cudaError_t)e));
+    ++launches;
+  }
+  c->info[0] = launches;
+  c->info[1] = n;
+  c->info[2] = W;
+  c->info[3] = grid;
+  c->info[4] = P.unit_bytes;
+  return FC_SUCCESS;
+}
+
+int free_plan(fc_comm* c, Plan& p) {
+  for (int i = 0; i < FC_MAXR; ++i)
+    if (p.d_tasks[i]) {
+      cudaFree(p.d_tasks[i]);
+      p.d_tasks[i] = nullptr;
+    }
+  p.loaded = false;
+  (void)c;
+  return FC_SUCCESS;
+}
+
+int default_ctas(fc_comm* c) {
+  int per_sm = 0, sms = 0;
+  FC_CUDA(c, (cudaError_t)fc_max_ctas_per_sm(FC_FLOAT32, &per_sm));
+  int v = 0;
+  for (int rd : {FC_BFLOAT16, FC_FLOAT16, FC_INT32}) {
+    FC_CUDA(c, (cudaError_t)fc_max_ctas_per_sm(rd, &v));
+    per_sm = std::min(per_sm, v);
+  }
+  FC_CUDA(c, cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));
+  const int cap = per_sm * sms / c->nlocal;
+  if (cap < 1) return fail(c, FC_ERR_UNSUPPORTED, "device cannot co-schedule %d ranks", c->nlocal);
+  c->ctas_per_rank = std::min(c->virt ? 16 : 32, cap);
+  return FC_SUCCESS;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* fc_version(void) { return "forestcoll-b200 0.1.0 (sm_100a)"; }
+
+size_t fc_handle_bytes(void) { return kHandleBytes; }
+
+int fc_comm_init(int rank, int nranks, int device, size_t scratch_bytes, fc_comm_t** out) {
+  if (!out || nranks < 1 || nranks > FC_MAXR || rank < 0 || rank >= nranks)
+    return FC_ERR_INVALID_ARG;
+  *out = nullptr;
+  fc_comm* c = new fc_comm();
+  c->rank = rank;
+  c->nranks = nranks;
+  c->device = device;
+  c->nlocal = 1;
+  setup_layout(c, scratch_bytes);
+  int st;
+  if (cudaSetDevice(device) != cudaSuccess || (st = alloc_workspace(c, &c->ws[rank])) != 0 ||
+      (st = default_ctas(c)) != 0) {
+    if (c->ws[rank]) cudaFree(c->ws[rank]);
+    fprintf(stderr, "fc_comm_init: %s\n", c->err.c_str());
+    delete c;
+    return FC_ERR_CUDA;
+  }
+  c->own[rank] = true;
+  c->connected = (nranks == 1);
+  *out = c;
+  return FC_SUCCESS;
+}
+
+int fc_comm_init_virtual(int nranks, int device, size_t scratch_bytes, fc_comm_t** out) {
+  if (!out || nranks < 1 || nranks > FC_MAXR) return FC_ERR_INVALID_ARG;
+  *out = nullptr;
+  fc_comm* c = new fc_comm();
+  c->nranks = nranks;
+  c->device = device;
+  c->virt = 1;
+  c->nlocal = nranks;
+  c->connected = 1;
+  setup_layout(c, scratch_bytes);
+  int st = cudaSetDevice(device) == cudaSuccess ? 0 : FC_ERR_CUDA;
+  for (int r = 0; r < nranks && st == 0; ++r) {
+    st = alloc_workspace(c, &c->ws[r]);
+    if (st == 0) c->own[r] = true;
+  }
+  if (st == 0) st = default_ctas(c);
+  if (st != 0) {
+    fprintf(stderr, "fc_comm_init_virtual: %s\n", c->err.c_str());
+    for (int r = 0; r < nranks; ++r)
+      if (c->own[r]) cudaFree(c->ws[r]);
+    delete c;
+    return st;
+  }
+  *out = c;
+  return FC_SUCCESS;
+}
+
+int fc_comm_export(fc_comm_t* c, void* handle) {
+  if (!c || !handle || c->virt) return FC_ERR_INVALID_ARG;
+  CommBlob b;
+  memset(&b, 0, sizeof(b));
+  b.magic = kCommMagic;
+  b.rank = c->rank;
+  b.nranks = c->nranks;
+  b.ws_bytes = c->ws_bytes;
+  b.flags_off = c->flags_off;
+  b.flags_words = c->flags_words;
+  b.scratch_off = c->scratch_off;
+  b.scratch_bytes = c->scratch_bytes;
+  FC_CUDA(c, cudaSetDevice(c->device));
+  FC_CUDA(c, cudaIpcGetMemHandle(&b.handle, c->ws[c->rank]));
+  memset(handle, 0, kHandleBytes);
+  memcpy(handle, &b, sizeof(b));
+  return FC_SUCCESS;
+}
+
+int fc_comm_connect(fc_comm_t* c, const void* handles) {
+  if (!c || !handles || c->virt) return FC_ERR_INVALID_ARG;
+  FC_CUDA(c, cudaSetDevice(c->device));
+  for (int r = 0; r < c->nranks; ++r) {
+    CommBlob b;
+    memcpy(&b, (const char*)handles + (size_t)r * kHandleBytes, sizeof(b));
+    if (b.magic != kCommMagic || b.rank != r || b.nranks != c->nranks)
+      return fail(c, FC_ERR_INVALID_ARG, "bad communicator handle for rank %d", r);
+    if (b.ws_bytes != c->ws_bytes || b.flags_off != c->flags_off ||
+        b.scratch_off != c->scratch_off || b.scratch_bytes != c->scratch_bytes)
+      return fail(c, FC_ERR_INVALID_ARG,
+                  "rank %d workspace layout differs (scratch_bytes must match on all ranks)", r);
+    if (r == c->rank) continue;
+    char* base = nullptr;
+    int st = open_mapping(c, b.handle, &base);
+    if (st) return st;
+    c->ws[r] = base;
+  }
+  c->connected = 1;
+  return FC_SUCCESS;
+}
+
+int fc_comm_set_option(fc_comm_t* c, int option, long long v) {
+  if (!c) return FC_ERR_INVALID_ARG;
+  switch (option) {
+    case FC_OPT_CTAS_PER_RANK: {
+      int per_sm = 0, sms = 0;
+      FC_CUDA(c, (cudaError_t)fc_max_ctas_per_sm(FC_FLOAT32, &per_sm));
+      FC_CUDA(c, cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));
+      if (v < 1 || v * c->nlocal > (long long)per_sm * sms)
+        return fail(c, FC_ERR_INVALID_ARG, "ctas_per_rank %lld out of range", v);
+      c->ctas_per_rank = (int)v;
+      return FC_SUCCESS;
+    }
+    case FC_OPT_CHUNK_MAX:
+      if (v < 256) return fail(c, FC_ERR_INVALID_ARG, "chunk_max too small");
+      c->chunk_max = v;
+      return FC_SUCCESS;
+    case FC_OPT_CHUNK_MIN:
+      if (v < 16) return fail(c, FC_ERR_INVALID_ARG, "chunk_min too small");
+      c->chunk_min = v;
+      return FC_SUCCESS;
+    case FC_OPT_ITEMS_PER_WORKER:
+      if (v < 0) return fail(c, FC_ERR_INVALID_ARG, "items_per_worker < 0");
+      c->items_per_worker = v;
+      return FC_SUCCESS;
+    case FC_OPT_TIMEOUT_MS:
+      if (v < 1) return fail(c, FC_ERR_INVALID_ARG, "timeout must be positive");
+      c->timeout_ms = v;
+      return FC_SUCCESS;
+    default:
+      return fail(c, FC_ERR_INVALID_ARG, "unknown option %d", option);
+  }
+}
+
+int fc_comm_get_option(fc_comm_t* c, int option, long long* v) {
+  if (!c || !v) return FC_ERR_INVALID_ARG;
+  switch (option) {
+    case FC_OPT_CTAS_PER_RANK: *v = c->ctas_per_rank; return FC_SUCCESS;
+    case FC_OPT_CHUNK_MAX: *v = c->chunk_max; return FC_SUCCESS;
+    case FC_OPT_CHUNK_MIN: *v = c->chunk_min; return FC_SUCCESS;
+    case FC_OPT_ITEMS_PER_WORKER: *v = c->items_per_worker; return FC_SUCCESS;
+    case FC_OPT_TIMEOUT_MS: *v = c->timeout_ms; return FC_SUCCESS;
+    default: return fail(c, FC_ERR_INVALID_ARG, "unknown option %d", option);
+  }
+}
+
+int fc_comm_check(fc_comm_t* c, int* device_error) {
+  if (!c) return FC_ERR_INVALID_ARG;
+  FC_CUDA(c, cudaSetDevice(c->device));
+  FC_CUDA(c, cudaDeviceSynchronize());
+  int worst = 0;
+  for (int i = 0; i < c->nlocal; ++i) {
+    const int r = c->virt ? i : c->rank;
+    FcCtl ctl;
+    FC_CUDA(c, cudaMemcpy(&ctl, c->ws[r], sizeof(ctl), cudaMemcpyDeviceToHost));
+    if (ctl.error && !worst) {
+      worst = (int)ctl.error;
+      fail(c, FC_ERR_DEVICE, "rank %d: device error %u (flag wait timed out; epoch %u, value %u)",
+           r, ctl.error, ctl.info[1], ctl.info[2]);
+    }
+  }
+  if (device_error) *device_error = worst;
+  return worst ? FC_ERR_DEVICE : FC_SUCCESS;
+}
+
+int fc_comm_destroy(fc_comm_t* c) {
+  if (!c) return FC_SUCCESS;
+  cudaSetDevice(c->device);
+  cudaDeviceSynchronize();
+  for (auto& p : c->plans) free_plan(c, p);
+  for (auto& m : c->maps) cudaIpcCloseMemHandle(m.base);
+  for (int r = 0; r < FC_MAXR; ++r)
+    if (c->own[r]) cudaFree(c->ws[r]);
+  delete c;
+  return FC_SUCCESS;
+}
+
+const char* fc_last_error(const fc_comm_t* c) { return c ? c->err.c_str() : "null communicator"; }
+
+int fc_buffer_export(fc_comm_t* c, const void* ptr, size_t bytes, void* handle) {
+  if (!c || !ptr || !handle) return FC_ERR_INVALID_ARG;
+  BufBlob b;
+  memset(&b, 0, sizeof(b));
+  b.magic = kBufMagic;
+  b.rank = c->rank;
+  b.bytes = bytes;
+  if (!c->virt) {
+    FC_CUDA(c, cudaSetDevice(c->device));
+    PFN_getRange fn = get_range_fn();
+    if (!fn) return fail(c, FC_ERR_CUDA, "cuMemGetAddressRange entry point unavailable");
+    CUdeviceptr base = 0;
+    size_t size = 0;
+    if (fn(&base, &size, (CUdeviceptr)ptr) != CUDA_SUCCESS)
+      return fail(c, FC_ERR_INVALID_ARG, "pointer %p is not device memory", ptr);
+    if ((uintptr_t)ptr + bytes > (uintptr_t)base + size)
+      return fail(c, FC_ERR_INVALID_ARG, "buffer exceeds its allocation");
+    b.offset = (uintptr_t)ptr - (uintptr_t)base;
+    FC_CUDA(c, cudaIpcGetMemHandle(&b.handle, (void*)base));
+  }
+  memset(handle, 0, kHandleBytes);
+  memcpy(handle, &b, sizeof(b));
+  return FC_SUCCESS;
+}
+
+int fc_buffer_register(fc_comm_t* c, const void* ptr, size_t bytes, const void* handles) {
+  if (!c || !ptr) return FC_ERR_INVALID_ARG;
+  if (c->virt) return FC_SUCCESS;  // all ranks' buffers are local pointers
+  if (!handles) return FC_ERR_INVALID_ARG;
+  FC_CUDA(c, cudaSetDevice(c->device));
+  Reg reg;
+  memset(&reg, 0, sizeof(reg));
+  reg.lo = (uintptr_t)ptr;
+  reg.hi = reg.lo + bytes;
+  for (int r = 0; r < c->nranks; ++r) {
+    BufBlob b;
+    memcpy(&b, (const char*)handles + (size_t)r * kHandleBytes, sizeof(b));
+    if (b.magic != kBufMagic || b.rank != r)
+      return fail(c, FC_ERR_INVALID_ARG, "bad buffer handle for rank %d", r);
+    if (b.bytes != bytes)
+      return fail(c, FC_ERR_INVALID_ARG, "rank %d registered %llu bytes, this rank %zu", r,
+                  (unsigned long long)b.bytes, bytes);
+    if (r == c->rank) {
+      reg.peer[r] = (char*)ptr;
+      continue;
+    }
+    char* base = nullptr;
+    int st = open_mapping(c, b.handle, &base);
+    if (st) return st;
+    reg.peer[r] = base + b.offset;
+  }
+  for (auto& r : c->regs)
+    if (r.lo == reg.lo) {
+      r = reg;
+      return FC_SUCCESS;
+    }
+  c->regs.push_back(reg);
+  return FC_SUCCESS;
+}
+
+int fc_buffer_deregister(fc_comm_t* c, const void* ptr) {
+  if (!c) return FC_ERR_INVALID_ARG;
+  for (size_t i = 0; i < c->regs.size(); ++i)
+    if (c->regs[i].lo == (uintptr_t)ptr) {
+      c->regs.erase(c->regs.begin() + i);
+      return FC_SUCCESS;
+    }
+  return fail(c, FC_ERR_NOT_REGISTERED, "buffer %p was not registered", ptr);
+}
+
+int fc_plan_load(fc_comm_t* c, int coll, const int32_t* t, size_t nwords) {
+  if (!c || !t) return FC_ERR_INVALID_ARG;
+  if (coll < 0 || coll > 2) return fail(c, FC_ERR_INVALID_ARG, "bad collective %d", coll);
+  if (nwords < FC_HEADER_WORDS || t[TH_MAGIC] != FC_TABLE_MAGIC ||
+      t[TH_VERSION] != FC_TABLE_VERSION)
+    return fail(c, FC_ERR_PLAN, "not a forest plan table (magic/version)");
+  const int N = t[TH_NRANKS], k = t[TH_K], ntrees = t[TH_NTREES], ntasks = t[TH_NTASKS];
+  if (t[TH_COLLECTIVE] != coll) return fail(c, FC_ERR_PLAN, "table is for collective %d", t[TH_COLLECTIVE]);
+  if (N != c->nranks) return fail(c, FC_ERR_PLAN, "table has %d ranks, comm %d", N, c->nranks);
+  if (k < 1 || ntrees < 1 || ntrees > kTreeCap || t[TH_TASK_WORDS] != FC_TASK_WORDS)
+    return fail(c, FC_ERR_PLAN, "bad table header (k=%d ntrees=%d)", k, ntrees);
+  if (t[TH_MAX_SLOTS] > kSlotCap) return fail(c, FC_ERR_PLAN, "too many slots per rank");
+  const size_t task0 = FC_HEADER_WORDS + (size_t)N * FC_RANKDESC_WORDS;
+  if (nwords != task0 + (size_t)ntasks * FC_TASK_WORDS)
+    return fail(c, FC_ERR_PLAN, "table length %zu does not match header", nwords);
+  Plan p;
+  p.nranks = N;
+  p.k = k;
+  p.ntrees = ntrees;
+  p.max_slot_units = t[TH_MAX_SLOT_UNITS];
+  p.max_slots = t[TH_MAX_SLOTS];
+  // validate every row
+  for (int i = 0; i < ntasks; ++i) {
+    const int32_t* T = t + task0 + (size_t)i * FC_TASK_WORDS;
+    const int kind = T[TW_KIND];
+    if (kind < FC_K_AG_ROOT || kind > FC_K_WAIT_AG || T[TW_TREE] < 0 || T[TW_TREE] >= ntrees ||
+        T[TW_ROOT] < 0 || T[TW_ROOT] >= N || T[TW_MLO] < 0 || T[TW_MLO] >= T[TW_MHI] ||
+        T[TW_MHI] > k || T[TW_N_AG_CHILD] < 0 || T[TW_N_AG_CHILD] >= FC_MAXR ||
+        T[TW_N_RS_CHILD] < 0 || T[TW_N_RS_CHILD] >= FC_MAXR)
+      return fail(c, FC_ERR_PLAN, "task row %d is malformed", i);
+    for (int j = 0; j < T[TW_N_AG_CHILD]; ++j)
+      if (T[TW_AG_CHILD + j] < 0 || T[TW_AG_CHILD + j] >= N)
+        return fail(c, FC_ERR_PLAN, "task row %d: bad child rank", i);
+    for (int j = 0; j < T[TW_N_RS_CHILD]; ++j)
+      if (T[TW_RS_CSLOT + j] < 0 || T[TW_RS_CSLOT + j] >= kSlotCap ||
+          T[TW_RS_CPREFIX + j] < 0 || T[TW_RS_CPREFIX + j] > p.max_slot_units)
+        return fail(c, FC_ERR_PLAN, "task row %d: bad slot", i);
+    if (kind == FC_K_RS_FWD &&
+        (T[TW_RS_PARENT] < 0 || T[TW_RS_PARENT] >= N || T[TW_RS_PSLOT] < 0 ||
+         T[TW_RS_PSLOT] >= kSlotCap))
+      return fail(c, FC_ERR_PLAN, "task row %d: bad reduce parent", i);
+    p.max_mult = std::max(p.max_mult, T[TW_MHI] - T[TW_MLO]);
+  }
+  for (int r = 0; r < N; ++r) {
+    const int32_t* D = t + FC_HEADER_WORDS + (size_t)r * FC_RANKDESC_WORDS;
+    if (D[RD_FIRST] < 0 || D[RD_NACTIVE] < 0 || D[RD_NWAIT] < 0 ||
+        D[RD_FIRST] + D[RD_NACTIVE] + D[RD_NWAIT] > ntasks)
+      return fail(c, FC_ERR_PLAN, "rank descriptor %d out of range", r);
+    p.active_total += D[RD_NACTIVE];
+  }
+  FC_CUDA(c, cudaSetDevice(c->device));
+  for (int i = 0; i < c->nlocal; ++i) {
+    const int r = c->virt ? i : c->rank;
+    const int32_t* D = t + FC_HEADER_WORDS + (size_t)r * FC_RANKDESC_WORDS;
+    const int rows = std::max(1, D[RD_NACTIVE] + D[RD_NWAIT]);
+    p.nact[i] = D[RD_NACTIVE];
+    p.nwait[i] = D[RD_NWAIT];
+    cudaError_t e = cudaMalloc((void**)&p.d_tasks[i], (size_t)rows * FC_TASK_WORDS * 4);
+    if (e == cudaSuccess && D[RD_NACTIVE] + D[RD_NWAIT] > 0)
+      e = cudaMemcpy(p.d_tasks[i], t + task0 + (size_t)D[RD_FIRST] * FC_TASK_WORDS,
+                     (size_t)(D[RD_NACTIVE] + D[RD_NWAIT]) * FC_TASK_WORDS * 4,
+                     cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+      free_plan(c, p);
+      return fail(c, FC_ERR_CUDA, "plan upload failed: %s", cudaGetErrorString(e));
+    }
+  }
+  free_plan(c, c->plans[coll]);
+  p.loaded = true;
+  c->plans[coll] = p;
+  return FC_SUCCESS;
+}
+
+int fc_allgather_multi(fc_comm_t* c, const void* const* sends, void* const* recvs,
+                       size_t sendcount, int dtype, void* stream) {
+  return run(c, FC_ALLGATHER, sends, recvs, sendcount, dtype, FC_SUM, stream);
+}
+int fc_reduce_scatter_multi(fc_comm_t* c, const void* const* sends, void* const* recvs,
+                            size_t recvcount, int dtype, int op, void* stream) {
+  return run(c, FC_REDUCE_SCATTER, sends, recvs, recvcount, dtype, op, stream);
+}
+int fc_allreduce_multi(fc_comm_t* c, const void* const* sends, void* const* recvs,
+                       size_t count, int dtype, int op, void* stream) {
+  return run(c, FC_ALLREDUCE, sends, recvs, count, dtype, op, stream);
+}
+int fc_allgather(fc_comm_t* c, const void* send, void* recv, size_t sendcount, int dtype,
+                 void* stream) {
+  if (c && c->virt) return fail(c, FC_ERR_INVALID_ARG, "virtual comm: use fc_allgather_multi");
+  return run(c, FC_ALLGATHER, &send, &recv, sendcount, dtype, FC_SUM, stream);
+}
+int fc_reduce_scatter(fc_comm_t* c, const void* send, void* recv, size_t recvcount, int dtype,
+                      int op, void* stream) {
+  if (c && c->virt) return fail(c, FC_ERR_INVALID_ARG, "virtual comm: use the _multi variant");
+  return run(c, FC_REDUCE_SCATTER, &send, &recv, recvcount, dtype, op, stream);
+}
+int fc_allreduce(fc_comm_t* c, const void* send, void* recv, size_t count, int dtype, int op,
+                 void* stream) {
+  if (c && c->virt) return fail(c, FC_ERR_INVALID_ARG, "virtual comm: use the _multi variant");
+  return run(c, FC_ALLREDUCE, &send, &recv, count, dtype, op, stream);
+}
+
+int fc_last_call_info(const fc_comm_t* c, long long* info, int ninfo) {
+  if (!c || !info) return FC_ERR_INVALID_ARG;
+  for (int i = 0; i < ninfo && i < 8; ++i) info[i] = c->info[i];
+  return FC_SUCCESS;
+}
+
+}  // extern "C"

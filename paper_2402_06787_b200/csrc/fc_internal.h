@@ -1,0 +1,110 @@
+// Internal layout shared by the host API (fc_api.cu) and the kernel
+// (fc_kernel.cu).  Not part of the C ABI.
+#pragma once
+#include <stdint.h>
+
+#include "../../include/forestcoll.h"
+
+#define FC_MAXR FC_MAX_RANKS
+#define FC_ALIGN 128          // chunk boundaries / scratch phase alignment (bytes)
+#define FC_READY_WORDS 64     // flags[0..nranks): entry (ready) epochs per peer
+#define FC_TABLE_MAGIC 0x50434c46  // 'FLCP'
+#define FC_TABLE_VERSION 1
+#define FC_HEADER_WORDS 16
+#define FC_RANKDESC_WORDS 8
+#define FC_TASK_WORDS 80
+
+// Task kinds (one task = one tree as seen from one rank).  See DESIGN.md §3.
+enum {
+  FC_K_AG_ROOT = 1,  // allgather root: send -> own recv + AG children
+  FC_K_AG_FWD = 2,   // allgather interior: wait parent, recv -> AG children
+  FC_K_RS_FWD = 3,   // reduce-scatter non-root: own + children partials -> parent scratch
+  FC_K_RS_ROOT = 4,  // reduce-scatter root: own + children partials -> out
+  FC_K_AR_ROOT = 5,  // allreduce root: reduce, write own buf, push to AG children
+  FC_K_WAIT_AG = 6,  // allgather leaf: wait for the chunk (completion only)
+};
+
+// Task word offsets.
+enum {
+  TW_KIND = 0,
+  TW_TREE = 1,
+  TW_STAGE = 2,
+  TW_ROOT = 3,
+  TW_MLO = 4,
+  TW_MHI = 5,
+  TW_AG_PARENT = 6,
+  TW_N_AG_CHILD = 7,
+  TW_AG_CHILD = 8,     // [FC_MAXR]
+  TW_RS_PARENT = 24,
+  TW_RS_PSLOT = 25,
+  TW_RS_PPREFIX = 26,
+  TW_N_RS_CHILD = 27,
+  TW_RS_CHILD = 28,    // [FC_MAXR]
+  TW_RS_CSLOT = 44,    // [FC_MAXR]
+  TW_RS_CPREFIX = 60,  // [FC_MAXR]
+  TW_END = 76,
+};
+
+// Header word offsets of a plan table (see compiler.py for the writer).
+enum {
+  TH_MAGIC = 0,
+  TH_VERSION = 1,
+  TH_COLLECTIVE = 2,
+  TH_NRANKS = 3,
+  TH_K = 4,
+  TH_NTREES = 5,
+  TH_NTASKS = 6,
+  TH_TASK_WORDS = 7,
+  TH_MAX_SLOT_UNITS = 8,
+  TH_MAX_SLOTS = 9,
+};
+// Rank descriptor words: first task, n active, n wait, slot units, n slots.
+enum { RD_FIRST = 0, RD_NACTIVE = 1, RD_NWAIT = 2, RD_SLOT_UNITS = 3, RD_NSLOTS = 4 };
+
+// Per-rank control block at the head of each rank's workspace.
+struct FcCtl {
+  unsigned int epoch;  // number of completed launches
+  unsigned int claim;  // dynamic work-claim counter (reset by the last CTA)
+  unsigned int done;   // CTAs finished in the current launch
+  unsigned int error;  // sticky device error code (0 = ok)
+  unsigned int info[12];
+};
+
+#define FC_DEVERR_TIMEOUT_AG 1
+#define FC_DEVERR_TIMEOUT_RS 2
+#define FC_DEVERR_TIMEOUT_READY 3
+
+struct FcParams {
+  int nranks;
+  int nlocal;
+  int ctas_per_rank;
+  int k;
+  int local_rank[FC_MAXR];
+  const int* tasks[FC_MAXR];  // by local index: this rank's task rows
+  int nactive[FC_MAXR];
+  int nwait[FC_MAXR];
+  FcCtl* ctl[FC_MAXR];        // by local index
+  // by rank: this process's view (peer-mapped for remote ranks)
+  const char* send[FC_MAXR];  // only local ranks are dereferenced
+  char* recv[FC_MAXR];        // AG/AR: peer-mapped; RS: local only
+  char* scratch[FC_MAXR];
+  unsigned int* flags[FC_MAXR];
+  long long shard_elems;   // S: elements per root shard
+  long long stride_elems;  // distance between root shards in the N-shard buffer
+  long long total_elems;   // elements in the N-shard buffer (AR: count)
+  long long unit_bytes;    // scratch bytes per unit of tree multiplicity per window
+  long long timeout_ns;
+  int esize;
+  int dtype;
+  int op;
+  int nchunks;  // chunks per tree slice for the whole call
+  int c0, c1;   // chunk window of this launch
+  int maxc;     // flag stride per tree / slot
+  int ag_flag_off;  // word offset of AG flags in the flags region
+  int rs_flag_off;  // word offset of RS flags in the flags region
+};
+
+// Kernel entry (fc_kernel.cu).  Returns a cudaError_t value.
+int fc_launch(const FcParams& p, int reduce_dtype, int cooperative,
+              void* stream, int* grid_out);
+int fc_max_ctas_per_sm(int reduce_dtype, int* out);

@@ -1,0 +1,420 @@
+"""PyTorch-facing executor for ForestColl schedules.
+
+``ForestCollComm`` is one communicator per rank process (torchrun, one GPU
+per rank): NCCL-shaped ``all_gather`` / ``reduce_scatter`` / ``all_reduce``
+on CUDA tensors, executed by the persistent sm_100a kernel through the C ABI.
+``VirtualComm`` runs all N ranks of a forest inside one grid on one GPU (the
+single-device test mode).  ``Executor`` is the §8b surface:
+one schedule (object, JSON text or path) plus its topology.
+
+Schedules come from the reference generator (``collsched.generate``,
+pipeline.py:43-78) through generator.get_schedule; pre-flight follows the
+reference CLI (validate before use, cli.py:186-195); errors derive from
+``CollschedError`` (errors.py:10-11).  torch is plumbing here — device
+memory, streams and the host-side handle exchange — not the data path.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+import torch
+
+from . import _lib
+from .compiler import lower
+from .errors import InvalidArgument, Unsupported
+from .generator import get_schedule, preflight
+from .schedule_io import ALLGATHER, ALLREDUCE, COLLECTIVES, REDUCE_SCATTER, load_schedule, \
+    parse_schedule_json, t_star_seconds
+from .topology import compute_ids, discover_for_torch, nvswitch_doc
+
+COLL_CODE = {ALLGATHER: 0, REDUCE_SCATTER: 1, ALLREDUCE: 2}
+DTYPE_CODE = {
+    torch.int8: 0, torch.uint8: 1, torch.int32: 2, torch.int64: 4, torch.float16: 6,
+    torch.float32: 7, torch.float64: 8, torch.bfloat16: 9,
+}
+for _name, _code in (("uint32", 3), ("uint64", 5)):
+    if hasattr(torch, _name):
+        DTYPE_CODE[getattr(torch, _name)] = _code
+REDUCIBLE = {torch.int32, torch.float16, torch.float32, torch.bfloat16}
+if hasattr(torch, "uint32"):
+    REDUCIBLE.add(torch.uint32)
+OPS = {"sum": 0}
+DEFAULT_SCRATCH = 1 << 30
+
+
+def _dtype_args(t: torch.Tensor, count: int):
+    code = DTYPE_CODE.get(t.dtype)
+    if code is None:  # opaque dtype: move bytes (allgather only)
+        return count * t.element_size(), 1
+    return count, code
+
+
+def _pci_bus_id(device: int):
+    p = torch.cuda.get_device_properties(device)
+    try:
+        return f"{p.pci_domain_id:04x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x}.0"
+    except AttributeError:
+        return None
+
+
+def _op_code(op) -> int:
+    if op not in OPS:
+        raise Unsupported(f"reduction op {op!r} is not supported (only 'sum')")
+    return OPS[op]
+
+
+def _as_doc(topology):
+    if topology is None:
+        return None
+    if isinstance(topology, dict):
+        return topology
+    if isinstance(topology, str):
+        import json
+
+        return json.loads(topology)
+    # reference Topology object: serialize through the reference
+    from ._refpath import import_collsched
+    import json
+
+    cs = import_collsched()
+    return json.loads(cs.serialize_topology(topology))
+
+
+class _CommBase:
+    """Shared plan management for real and virtual communicators."""
+
+    def __init__(self, topology_doc, nranks, schedules=None, validate=True, prune=True):
+        self.topology = topology_doc
+        self.nranks = nranks
+        self._validate = validate
+        self._prune = prune
+        self._schedules = dict(schedules or {})
+        self._plans = {}
+        self._comm = None
+        self._lib = _lib.load()
+        if topology_doc is not None and len(compute_ids(topology_doc)) != nranks:
+            raise InvalidArgument(
+                f"topology has {len(compute_ids(topology_doc))} compute nodes, comm {nranks} ranks")
+
+    # -- schedules and plans ------------------------------------------------
+    def schedule(self, collective: str):
+        if collective not in COLLECTIVES:
+            raise InvalidArgument(f"unknown collective {collective!r}")
+        s = self._schedules.get(collective)
+        if s is None:
+            if self.topology is None:
+                raise InvalidArgument(f"no schedule for {collective} and no topology to generate one")
+            s = get_schedule(self.topology, collective, prune=self._prune, validate=self._validate)
+            self._schedules[collective] = s
+        return s
+
+    def plan(self, collective: str):
+        p = self._plans.get(collective)
+        if p is None:
+            s = self.schedule(collective)
+            ranks = compute_ids(self.topology) if self.topology is not None else None
+            p = lower(s, ranks=ranks, collective=collective)
+            if p.nranks != self.nranks:
+                raise InvalidArgument(f"schedule has {p.nranks} ranks, comm {self.nranks}")
+            tbl = np.ascontiguousarray(p.table, dtype=np.int32)
+            _lib.check(
+                self._lib.fc_plan_load(self._comm, COLL_CODE[collective],
+                                       tbl.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
+                                       tbl.size),
+                self._comm, f"plan_load({collective})")
+            self._plans[collective] = p
+        return p
+
+    def t_star(self, collective: str, message_bytes: int) -> float:
+        """ForestColl optimal time (seconds) for M bytes."""
+        return t_star_seconds(self.schedule(collective), message_bytes, collective)
+
+    # -- options / status ---------------------------------------------------
+    def set_option(self, name: str, value: int) -> None:
+        _lib.check(self._lib.fc_comm_set_option(self._comm, _lib.OPTIONS[name], int(value)),
+                   self._comm, f"set_option({name})")
+
+    def get_option(self, name: str) -> int:
+        v = ctypes.c_longlong()
+        _lib.check(self._lib.fc_comm_get_option(self._comm, _lib.OPTIONS[name], ctypes.byref(v)),
+                   self._comm, f"get_option({name})")
+        return v.value
+
+    def check(self) -> None:
+        """Synchronize and raise DeviceError if a device-side wait failed."""
+        err = ctypes.c_int()
+        _lib.check(self._lib.fc_comm_check(self._comm, ctypes.byref(err)), self._comm, "check")
+
+    def last_call_info(self) -> dict:
+        buf = (ctypes.c_longlong * 8)()
+        self._lib.fc_last_call_info(self._comm, buf, 8)
+        return {"launches": buf[0], "nchunks": buf[1], "window": buf[2], "grid": buf[3],
+                "unit_bytes": buf[4]}
+
+    def close(self) -> None:
+        if self._comm is not None:
+            self._lib.fc_comm_destroy(self._comm)
+            self._comm = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @staticmethod
+    def _check_tensor(t, device, name):
+        if not isinstance(t, torch.Tensor) or not t.is_cuda:
+            raise InvalidArgument(f"{name} must be a CUDA tensor")
+        if t.device.index != device:
+            raise InvalidArgument(f"{name} is on {t.device}, communicator on cuda:{device}")
+        if not t.is_contiguous():
+            raise InvalidArgument(f"{name} must be contiguous")
+
+
+class ForestCollComm(_CommBase):
+    """One rank of a ForestColl communicator (one process per GPU)."""
+
+    def __init__(self, topology=None, *, rank=None, world_size=None, device=None, group=None,
+                 scratch_bytes=DEFAULT_SCRATCH, schedules=None, validate=True, prune=True,
+                 options=None):
+        import torch.distributed as dist
+
+        if rank is None or world_size is None:
+            if not dist.is_initialized():
+                raise InvalidArgument("rank/world_size not given and torch.distributed is not initialized")
+            rank = dist.get_rank() if rank is None else rank
+            world_size = dist.get_world_size() if world_size is None else world_size
+        if device is None:
+            device = int(os.environ.get("LOCAL_RANK", torch.cuda.current_device()))
+        self.rank, self.device = rank, device
+        self._group = None
+        if world_size > 1:
+            self._group = group if group is not None else dist.new_group(backend="gloo")
+        self.nranks = world_size
+        doc = _as_doc(topology)
+        if doc is None and not schedules:
+            buses = self._allgather_obj(_pci_bus_id(device))
+            doc = discover_for_torch(world_size, None if None in buses else buses)
+        super().__init__(doc, world_size, schedules, validate, prune)
+        comm = ctypes.c_void_p()
+        _lib.check(self._lib.fc_comm_init(rank, world_size, device, int(scratch_bytes),
+                                          ctypes.byref(comm)), None, "fc_comm_init")
+        self._comm = comm
+        for name, value in (options or {}).items():
+            self.set_option(name, value)
+        if world_size > 1:
+            hb = self._lib.fc_handle_bytes()
+            mine = ctypes.create_string_buffer(hb)
+            _lib.check(self._lib.fc_comm_export(self._comm, mine), self._comm, "comm_export")
+            allh = self._allgather_obj(mine.raw)
+            blob = ctypes.create_string_buffer(b"".join(allh), hb * world_size)
+            _lib.check(self._lib.fc_comm_connect(self._comm, blob), self._comm, "comm_connect")
+        self._registered = {}
+
+    def _allgather_obj(self, obj):
+        import torch.distributed as dist
+
+        if self._group is None:
+            return [obj]
+        out = [None] * self.nranks
+        dist.all_gather_object(out, obj, group=self._group)
+        return out
+
+    # -- buffers ------------------------------------------------------------
+    def register(self, t: torch.Tensor) -> None:
+        """Map `t` into every peer (collective: all ranks call together with
+        same-sized tensors).  Outputs of all_gather / all_reduce must be
+        registered; first use registers automatically."""
+        key = (t.data_ptr(), t.numel() * t.element_size())
+        if key in self._registered or self.nranks == 1:
+            return
+        hb = self._lib.fc_handle_bytes()
+        mine = ctypes.create_string_buffer(hb)
+        _lib.check(self._lib.fc_buffer_export(self._comm, key[0], key[1], mine), self._comm,
+                   "buffer_export")
+        allh = self._allgather_obj(mine.raw)
+        blob = ctypes.create_string_buffer(b"".join(allh), hb * self.nranks)
+        _lib.check(self._lib.fc_buffer_register(self._comm, key[0], key[1], blob), self._comm,
+                   "buffer_register")
+        self._registered[key] = t  # keep the allocation alive while mapped
+
+    def deregister(self, t: torch.Tensor) -> None:
+        key = (t.data_ptr(), t.numel() * t.element_size())
+        if self._registered.pop(key, None) is not None:
+            self._lib.fc_buffer_deregister(self._comm, key[0])
+
+    def empty(self, *shape, dtype=torch.float32) -> torch.Tensor:
+        t = torch.empty(*shape, dtype=dtype, device=f"cuda:{self.device}")
+        self.register(t)
+        return t
+
+    def _stream(self):
+        return torch.cuda.current_stream(self.device).cuda_stream
+
+    # -- collectives --------------------------------------------------------
+    def all_gather(self, out: torch.Tensor, inp: torch.Tensor) -> torch.Tensor:
+        """out[r*S:(r+1)*S] = inp of rank r (NCCL all_gather_into_tensor)."""
+        self._check_tensor(inp, self.device, "input")
+        self._check_tensor(out, self.device, "output")
+        if out.dtype != inp.dtype or out.numel() != inp.numel() * self.nranks:
+            raise InvalidArgument("output must hold world_size x input elements of the same dtype")
+        self.plan(ALLGATHER)
+        self.register(out)
+        count, code = _dtype_args(inp, inp.numel())
+        _lib.check(self._lib.fc_allgather(self._comm, inp.data_ptr(), out.data_ptr(), count, code,
+                                          self._stream()), self._comm, "allgather")
+        return out
+
+    all_gather_into_tensor = all_gather
+
+    def reduce_scatter(self, out: torch.Tensor, inp: torch.Tensor, op="sum") -> torch.Tensor:
+        """out = sum over ranks of inp[rank*S:(rank+1)*S] (reduce_scatter_tensor)."""
+        self._check_tensor(inp, self.device, "input")
+        self._check_tensor(out, self.device, "output")
+        if out.dtype != inp.dtype or inp.numel() != out.numel() * self.nranks:
+            raise InvalidArgument("input must hold world_size x output elements of the same dtype")
+        if inp.dtype not in REDUCIBLE:
+            raise Unsupported(f"dtype {inp.dtype} cannot be reduced")
+        self.plan(REDUCE_SCATTER)
+        _lib.check(self._lib.fc_reduce_scatter(self._comm, inp.data_ptr(), out.data_ptr(),
+                                               out.numel(), DTYPE_CODE[inp.dtype], _op_code(op),
+                                               self._stream()), self._comm, "reduce_scatter")
+        return out
+
+    reduce_scatter_tensor = reduce_scatter
+
+    def all_reduce(self, buf: torch.Tensor, op="sum", out: torch.Tensor | None = None) -> torch.Tensor:
+        """In-place (or into `out`) sum over ranks."""
+        out = buf if out is None else out
+        self._check_tensor(buf, self.device, "buffer")
+        self._check_tensor(out, self.device, "output")
+        if out.dtype != buf.dtype or out.numel() != buf.numel():
+            raise InvalidArgument("output must match the buffer")
+        if buf.dtype not in REDUCIBLE:
+            raise Unsupported(f"dtype {buf.dtype} cannot be reduced")
+        self.plan(ALLREDUCE)
+        self.register(out)
+        _lib.check(self._lib.fc_allreduce(self._comm, buf.data_ptr(), out.data_ptr(), buf.numel(),
+                                          DTYPE_CODE[buf.dtype], _op_code(op), self._stream()),
+                   self._comm, "allreduce")
+        return out
+
+
+class VirtualComm(_CommBase):
+    """All N ranks of a forest executed by one cooperative grid on one GPU.
+
+    Rank r's buffers are ordinary tensors on the same device; "peer" stores
+    land in local HBM.  Same kernel, tables, flags and chunking as the
+    multi-GPU path (SURVEY.md §4 "virtual ranks" mode).
+    """
+
+    def __init__(self, topology=None, *, nranks=None, device=0, scratch_bytes=DEFAULT_SCRATCH,
+                 schedules=None, validate=True, prune=True, options=None):
+        doc = _as_doc(topology)
+        if doc is None:
+            if schedules:
+                any_s = next(iter(schedules.values()))
+                nranks = any_s.num_compute
+            elif nranks is not None:
+                doc = nvswitch_doc(nranks)
+            else:
+                raise InvalidArgument("need a topology, schedules or nranks")
+        if doc is not None:
+            nranks = len(compute_ids(doc))
+        self.device = device
+        super().__init__(doc, nranks, schedules, validate, prune)
+        comm = ctypes.c_void_p()
+        _lib.check(self._lib.fc_comm_init_virtual(nranks, device, int(scratch_bytes),
+                                                  ctypes.byref(comm)), None, "fc_comm_init_virtual")
+        self._comm = comm
+        for name, value in (options or {}).items():
+            self.set_option(name, value)
+
+    def _ptrs(self, ts, name):
+        if len(ts) != self.nranks:
+            raise InvalidArgument(f"need {self.nranks} {name} tensors, got {len(ts)}")
+        for t in ts:
+            self._check_tensor(t, self.device, name)
+        arr = (ctypes.c_void_p * self.nranks)(*[t.data_ptr() for t in ts])
+        return arr
+
+    def _stream(self):
+        return torch.cuda.current_stream(self.device).cuda_stream
+
+    def all_gather(self, outs, inps):
+        for o, i in zip(outs, inps):
+            if o.dtype != i.dtype or o.numel() != i.numel() * self.nranks or i.numel() != inps[0].numel():
+                raise InvalidArgument("each output must hold nranks x input elements")
+        self.plan(ALLGATHER)
+        count, code = _dtype_args(inps[0], inps[0].numel())
+        _lib.check(self._lib.fc_allgather_multi(self._comm, self._ptrs(inps, "input"),
+                                                self._ptrs(outs, "output"), count, code,
+                                                self._stream()), self._comm, "allgather")
+        return outs
+
+    def reduce_scatter(self, outs, inps, op="sum"):
+        for o, i in zip(outs, inps):
+            if o.dtype != i.dtype or i.numel() != o.numel() * self.nranks or o.numel() != outs[0].numel():
+                raise InvalidArgument("each input must hold nranks x output elements")
+        if inps[0].dtype not in REDUCIBLE:
+            raise Unsupported(f"dtype {inps[0].dtype} cannot be reduced")
+        self.plan(REDUCE_SCATTER)
+        _lib.check(self._lib.fc_reduce_scatter_multi(
+            self._comm, self._ptrs(inps, "input"), self._ptrs(outs, "output"), outs[0].numel(),
+            DTYPE_CODE[inps[0].dtype], _op_code(op), self._stream()), self._comm, "reduce_scatter")
+        return outs
+
+    def all_reduce(self, bufs, op="sum", outs=None):
+        outs = bufs if outs is None else outs
+        for o, b in zip(outs, bufs):
+            if o.dtype != b.dtype or o.numel() != b.numel() or b.numel() != bufs[0].numel():
+                raise InvalidArgument("buffers must all have the same size and dtype")
+        if bufs[0].dtype not in REDUCIBLE:
+            raise Unsupported(f"dtype {bufs[0].dtype} cannot be reduced")
+        self.plan(ALLREDUCE)
+        _lib.check(self._lib.fc_allreduce_multi(
+            self._comm, self._ptrs(bufs, "buffer"), self._ptrs(outs, "output"), bufs[0].numel(),
+            DTYPE_CODE[bufs[0].dtype], _op_code(op), self._stream()), self._comm, "allreduce")
+        return outs
+
+
+class Executor:
+    """§8b surface: ``Executor(schedule_or_path, topology, rank, world, device)``.
+
+    Accepts a reference ``Schedule``, its JSON text, or a path to the JSON
+    (``parse_schedule``, schedule.py:439-448); validates it against the
+    topology when the reference is importable (verify.py:478-534) before
+    lowering.  ``virtual=True`` executes all ranks on one device.
+    """
+
+    def __init__(self, schedule_or_path, topology=None, rank=None, world=None, device=None,
+                 virtual=False, **kw):
+        s = schedule_or_path
+        if isinstance(s, str):
+            s = load_schedule(s) if os.path.exists(s) else parse_schedule_json(s)
+        doc = _as_doc(topology)
+        if doc is not None and kw.get("validate", True):
+            preflight(s, doc)
+        scheds = {s.collective: s}
+        self.collective = s.collective
+        if virtual:
+            self.comm = VirtualComm(doc, device=device or 0, schedules=scheds, **kw)
+        else:
+            self.comm = ForestCollComm(doc, rank=rank, world_size=world, device=device,
+                                       schedules=scheds, **kw)
+
+    def all_gather(self, out, inp):
+        return self.comm.all_gather(out, inp)
+
+    def reduce_scatter(self, out, inp, op="sum"):
+        return self.comm.reduce_scatter(out, inp, op)
+
+    def all_reduce(self, buf, op="sum"):
+        return self.comm.all_reduce(buf, op)
+
+    def close(self):
+        self.comm.close()

@@ -1,0 +1,100 @@
+"""GPU parity: the sm_100a forest kernel (virtual ranks, one device) against
+the CPU oracle, bit-exact, on reference-generated forests."""
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import golden_names, load_golden
+
+pytestmark = pytest.mark.gpu
+
+TORCH_DT = {"float32": torch.float32, "bfloat16": torch.bfloat16, "float16": torch.float16,
+            "int32": torch.int32}
+
+
+def _np(t):
+    if t.dtype == torch.bfloat16:
+        return t.view(torch.int16).cpu().numpy().view(np.uint16)
+    return t.cpu().numpy()
+
+
+def _rand(n, dtype, gen, dev):
+    if dtype == "int32":
+        return torch.randint(-2**20, 2**20, (n,), generator=gen, dtype=torch.int32).to(dev)
+    return torch.empty(n).uniform_(-1, 1, generator=gen).to(TORCH_DT[dtype]).to(dev)
+
+
+def _bits(a):
+    a = np.ascontiguousarray(a)
+    return a.view(np.uint8)
+
+
+@pytest.fixture(scope="module")
+def dev():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return torch.device("cuda:0")
+
+
+def _comm(s, **kw):
+    from paper_2402_06787_b200 import VirtualComm
+
+    return VirtualComm(schedules={s.collective: s}, **kw)
+
+
+@pytest.mark.parametrize("name", golden_names("allgather"))
+@pytest.mark.parametrize("S", [1, 37, 4096, 262144 + 3])
+def test_allgather_virtual(dev, name, S):
+    from oracle import forest_oracle as fo
+
+    s = load_golden(name)
+    comm = _comm(s)
+    n = comm.nranks
+    gen = torch.Generator().manual_seed(1234)
+    sends = [torch.randint(0, 2**31 - 1, (S,), generator=gen, dtype=torch.int32).view(torch.float32).to(dev)
+             for _ in range(n)]
+    outs = [torch.full((n * S,), float("nan"), device=dev) for _ in range(n)]
+    comm.all_gather(outs, sends)
+    comm.check()
+    ref = fo.allgather(s, [_np(x) for x in sends])
+    for r in range(n):
+        assert np.array_equal(_bits(_np(outs[r])), _bits(ref[r])), f"rank {r}"
+
+
+@pytest.mark.parametrize("name", golden_names("reduce_scatter"))
+@pytest.mark.parametrize("dtype", ["float32", "bfloat16", "int32", "float16"])
+@pytest.mark.parametrize("S", [5, 1000, 65536 + 7])
+def test_reduce_scatter_virtual(dev, name, dtype, S):
+    from oracle import forest_oracle as fo
+
+    s = load_golden(name)
+    comm = _comm(s)
+    n = comm.nranks
+    gen = torch.Generator().manual_seed(99)
+    ins = [_rand(n * S, dtype, gen, dev) for _ in range(n)]
+    outs = [torch.zeros(S, dtype=TORCH_DT[dtype], device=dev) for _ in range(n)]
+    comm.reduce_scatter(outs, ins)
+    comm.check()
+    ref = fo.reduce_scatter(s, [_np(x) for x in ins], dtype)
+    for r in range(n):
+        assert np.array_equal(_bits(_np(outs[r])), _bits(ref[r])), f"rank {r}"
+
+
+@pytest.mark.parametrize("name", golden_names("allreduce"))
+@pytest.mark.parametrize("dtype", ["bfloat16", "float32", "int32"])
+@pytest.mark.parametrize("count", [3, 1001, 1 << 18])
+def test_allreduce_virtual(dev, name, dtype, count):
+    from oracle import forest_oracle as fo
+
+    s = load_golden(name)
+    comm = _comm(s)
+    n = comm.nranks
+    gen = torch.Generator().manual_seed(7)
+    ins = [_rand(count, dtype, gen, dev) for _ in range(n)]
+    outs = [torch.zeros(count, dtype=TORCH_DT[dtype], device=dev) for _ in range(n)]
+    comm.all_reduce(ins, outs=outs)
+    comm.check()
+    ref = fo.allreduce(s, [_np(x) for x in ins], dtype)
+    for r in range(n):
+        assert np.array_equal(_bits(_np(outs[r])), _bits(ref[r])), f"rank {r}"
