@@ -1,0 +1,495 @@
+"""Benchmark: ForestColl collectives executed by the B200-native forest kernel.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...
+
+Metric (BASELINE.json): collective algbw (GB/s, 1 GB = 1e9 B, M/T as in
+nccl-tests) and the fraction of ForestColl's optimal time T* (SURVEY.md §8d).
+
+* N >= 2 (one process per GPU, torchrun): allgather of M = 1 GiB total output
+  on the nvswitch(N) forest (NVML-discovered topology, nominal fallback),
+  inputs resident in HBM; NCCL all_gather_into_tensor on the same buffers
+  and reduce-scatter / allreduce points are reported beside it.
+* N = 1: the same kernel executes the 8-GPU NVSwitch forest (configs[0]'s
+  topology) with all 8 ranks as virtual ranks on one B200 (HBM-bound; the
+  per-rank "peer" stores land in local HBM), at M = 512 MiB per rank; the
+  1-GPU local-copy sanity point and configs[0]'s 8 x 1 MiB case are attached.
+* --impl reference: the CPU executor (oracle/, a restatement: the reference
+  ships no executor) timed on the host on a bounded sample.
+
+Timing: W warm-up steps, then K steps between a barrier + synchronize on both
+sides, CUDA events on the launching stream, max over ranks.  Inputs are
+larger than L2 (126 MB), so no flush is needed.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+GIB = 1 << 30
+MIB = 1 << 20
+NVLINK_PEAK_GBS = 770.0  # B200_PROFILING.md: measured peer copy per direction (nominal 900)
+NVLINK_NOMINAL_GBS = 900.0
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except OSError:
+        return {}
+
+
+def hbm_peak():
+    pk = measured_peaks()
+    if "hbm_gbs" in pk:
+        return float(pk["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+def ncu_traffic(workload):
+    try:
+        with open(os.path.join(REPO, "profiles", "ncu_traffic.json")) as f:
+            return json.load(f).get(workload)
+    except (OSError, ValueError):
+        return None
+
+
+# ---------------------------------------------------------------------------
+# clocks sampling (B200_PROFILING.md recipe)
+# ---------------------------------------------------------------------------
+class Clocks:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 9:
+                continue
+            try:
+                sm.append(float(p[1]))
+                mx = max(mx, float(p[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, p[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# timing helpers
+# ---------------------------------------------------------------------------
+def timed(fn, steps, warmup, dist=None):
+    import torch
+
+    for _ in range(warmup):
+        fn()
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    s = torch.cuda.current_stream()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(s)
+    for _ in range(steps):
+        fn()
+    t1.record(s)
+    torch.cuda.synchronize()
+    ms = t0.elapsed_time(t1) / steps
+    if dist is not None:
+        x = torch.tensor([ms], device="cuda")
+        dist.all_reduce(x, op=dist.ReduceOp.MAX)
+        ms = float(x.item())
+    return ms
+
+
+def gbs(nbytes, ms):
+    return nbytes / (ms * 1e-3) / 1e9
+
+
+def cpu_baseline_allgather(schedule, shard_bytes, budget_s=15.0):
+    """Oracle (numpy port) allgather over N host buffers; bounded sample."""
+    import numpy as np
+
+    from oracle import forest_oracle as fo
+
+    n = schedule.num_compute
+    S = shard_bytes // 4
+    sends = [np.random.default_rng(r).standard_normal(S).astype(np.float32) for r in range(n)]
+    fo.allgather(schedule, sends)  # warm
+    reps, t0 = 0, time.perf_counter()
+    while True:
+        fo.allgather(schedule, sends)
+        reps += 1
+        el = time.perf_counter() - t0
+        if el > budget_s or reps >= 50:
+            break
+    per = el / reps
+    M = n * S * 4
+    return {"value": round(gbs(M, per * 1e3), 3), "unit": "GB/s", "cores": 1, "kind": "port",
+            "sample": f"oracle.forest_oracle.allgather, {n} ranks x {shard_bytes // MIB} MiB shards, "
+                      f"{reps} reps in {el:.1f}s (numpy, single thread; host os.cpu_count()={os.cpu_count()})"}
+
+
+# ---------------------------------------------------------------------------
+# N = 1: virtual ranks on one device
+# ---------------------------------------------------------------------------
+def plan_bytes_ag(plan, S_bytes):
+    """HBM bytes one virtual-rank allgather must move (writes + reads)."""
+    n = plan.nranks
+    fwd_units = sum(t.mhi - t.mlo for v in range(n) for t in plan.tasks[v] if t.kind == 2)
+    writes = n * n * S_bytes  # every rank's output, once
+    reads = n * S_bytes + fwd_units * S_bytes // plan.k  # root inputs + forwarded slices
+    return writes + reads
+
+
+def run_single(args):
+    import torch
+
+    from paper_2402_06787_b200 import VirtualComm
+    from paper_2402_06787_b200.topology import nvswitch_doc
+
+    dev = torch.device("cuda:0")
+    torch.cuda.set_device(dev)
+    n = 8
+    comm = VirtualComm(nvswitch_doc(n), device=0)
+    S_bytes = args.shard_mib * MIB
+    S = S_bytes // 4
+    M = n * S_bytes
+    sends = [torch.randn(S, device=dev) for _ in range(n)]
+    outs = [torch.empty(n * S, device=dev) for _ in range(n)]
+    plan = comm.plan("allgather")
+    fn = lambda: comm.all_gather(outs, sends)  # noqa: E731
+    with Clocks(0) as clk:
+        ms = timed(fn, args.steps, args.warmup)
+    comm.check()
+    info = comm.last_call_info()
+    tstar = comm.t_star("allgather", M)
+    alg = gbs(M, ms)
+    hbm_bytes = plan_bytes_ag(plan, S_bytes)
+    peak, peak_kind = hbm_peak()
+    achieved = gbs(hbm_bytes, ms)
+    workload = f"nvs8-forest-allgather-virtual8-{args.shard_mib}MiBx8"
+
+    # e2e through the public API: pinned host inputs -> device, collective, outputs -> host
+    host_in = [torch.empty(S, dtype=torch.float32, pin_memory=True).copy_(x.cpu()) for x in sends]
+    host_out = [torch.empty(n * S, dtype=torch.float32, pin_memory=True) for _ in range(n)]
+
+    def e2e_step():
+        for h, d in zip(host_in, sends):
+            d.copy_(h, non_blocking=True)
+        comm.all_gather(outs, sends)
+        for h, d in zip(host_out, outs):
+            h.copy_(d, non_blocking=True)
+
+    e2e_steps = max(1, min(args.steps, 3))
+    e2e_ms = timed(e2e_step, e2e_steps, 1)
+
+    # configs[0] case (8 x 1 MiB fp32 shards) and the 1-GPU local-copy sanity point
+    small_s = [torch.randn(MIB // 4, device=dev) for _ in range(n)]
+    small_o = [torch.empty(n * MIB // 4, device=dev) for _ in range(n)]
+    small_ms = timed(lambda: comm.all_gather(small_o, small_s), 50, 10)
+    lc_src = torch.randn(S, device=dev)
+    lc_dst = torch.empty(S, device=dev)
+    from paper_2402_06787_b200 import executor as ex
+
+    single = _local_copy_comm(ex, dev)
+    lc_ms = timed(lambda: single.all_gather([lc_dst], [lc_src]), args.steps, args.warmup)
+
+    line = {
+        "metric": "collective algbw GB/s (ForestColl allgather, M = total output bytes per rank)",
+        "value": round(alg, 2),
+        "unit": "GB/s",
+        "n_gpus": 1,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(ms, 4),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "u8 (fp32 payload, byte copy)",
+        "data": "synthetic torch.randn fp32 shards",
+        "config": {"workload": workload, "topology": "nvswitch(8) forest from collsched.generate",
+                   "ranks": "8 virtual ranks on cuda:0", "M_bytes": M, "shard_bytes": S_bytes,
+                   "l2": "inputs+outputs (4.5 GiB) larger than L2; no flush",
+                   "chunks_per_tree": info["nchunks"], "ctas_per_rank": comm.get_option("ctas_per_rank")},
+        "t_star_ms_nvlink_model": round(tstar * 1e3, 4),
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                     "frac": round(achieved / peak, 4), "peak_kind": peak_kind,
+                     "algorithmic_bytes_per_launch": hbm_bytes,
+                     "traffic": ncu_traffic(workload)},
+        "e2e": {"value": round(gbs(M, e2e_ms), 3), "unit": "GB/s",
+                "h2d_bytes_per_step": n * S_bytes, "d2h_bytes_per_step": n * M,
+                "ms_per_step": round(e2e_ms, 3)},
+        "gpu_launches": args.steps * info["launches"],
+        "clocks": clk.summary(),
+        "configs0_8x1MiB": {"ms": round(small_ms, 4), "algbw_GBps": round(gbs(8 * MIB, small_ms), 2)},
+        "local_copy_sanity": {"bytes": S_bytes, "ms": round(lc_ms, 4),
+                              "hbm_GBps_rw": round(gbs(2 * S_bytes, lc_ms), 1)},
+    }
+    if not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline_allgather(comm.schedule("allgather"), 4 * MIB)
+    comm.close()
+    print(json.dumps(line), flush=True)
+
+
+def _local_copy_comm(ex, dev):
+    """1-rank forest (N=1 is outside the reference's API, topology.py:263-266):
+    the root task copies send -> recv; the HBM sanity point."""
+    from paper_2402_06787_b200.schedule_io import RootTrees, Schedule, ScheduleBatch
+    from fractions import Fraction
+
+    s = Schedule(collective="allgather", num_compute=1, k=1, U=Fraction(1), y=Fraction(1),
+                 inv_x_star=Fraction(0), roots=(RootTrees("g0", (ScheduleBatch(1, ()),)),))
+    return ex.VirtualComm(schedules={"allgather": s}, device=dev.index)
+
+
+# ---------------------------------------------------------------------------
+# N >= 2: one process per GPU
+# ---------------------------------------------------------------------------
+def run_multi(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2402_06787_b200 import ForestCollComm
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    torch.cuda.set_device(local)
+    dev = torch.device(f"cuda:{local}")
+    dist.init_process_group("nccl", device_id=dev)
+    rank, n = dist.get_rank(), dist.get_world_size()
+    comm = ForestCollComm(None, rank=rank, world_size=n, device=local)
+    topo_kind = comm.topology_source
+    M = args.msg_mib * MIB
+    S = M // n // 4
+    M = S * 4 * n
+    inp = torch.randn(S, device=dev)
+    out = comm.empty(n * S, dtype=torch.float32)
+    fn = lambda: comm.all_gather(out, inp)  # noqa: E731
+    with Clocks(local) as clk:
+        ms = timed(fn, args.steps, args.warmup, dist)
+    comm.check()
+    info = comm.last_call_info()
+    tstar = comm.t_star("allgather", M)
+    alg = gbs(M, ms)
+    ingress = (n - 1) * M // n
+    achieved = gbs(ingress, ms)
+    # NCCL on the same buffers
+    nccl_out = torch.empty_like(out)
+    nccl_ms = timed(lambda: dist.all_gather_into_tensor(nccl_out, inp), args.steps, args.warmup, dist)
+    ok = bool(torch.equal(out, nccl_out))
+
+    # e2e: pinned host input -> device, collective, output -> host
+    h_in = torch.empty(S, pin_memory=True).copy_(inp.cpu())
+    h_out = torch.empty(n * S, pin_memory=True)
+
+    def e2e_step():
+        inp.copy_(h_in, non_blocking=True)
+        comm.all_gather(out, inp)
+        h_out.copy_(out, non_blocking=True)
+
+    e2e_ms = timed(e2e_step, max(1, min(args.steps, 5)), 1, dist)
+
+    extra = {}
+    if not args.quick:
+        extra = sweep_multi(comm, dist, n, dev, args)
+    if rank == 0:
+        line = {
+            "metric": "collective algbw GB/s (ForestColl allgather, M = total output bytes per rank)",
+            "value": round(alg, 2),
+            "unit": "GB/s",
+            "n_gpus": n,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": round(ms, 4),
+            "higher_is_better": True,
+            "scaling": "strong",
+            "vs_baseline": None,
+            "dtype": "u8 (fp32 payload, byte copy)",
+            "data": "synthetic torch.randn fp32 shards",
+            "config": {"workload": f"nvs{n}-forest-allgather-{args.msg_mib}MiB",
+                       "topology": f"nvswitch({n}) from {topo_kind} ingestion, collsched forest",
+                       "M_bytes": M, "shard_bytes": S * 4, "parallelism": f"{n} ranks, 1 per GPU",
+                       "l2": "M larger than L2; no flush", "chunks_per_tree": info["nchunks"],
+                       "ctas_per_rank": comm.get_option("ctas_per_rank")},
+            "frac_of_t_star": round(tstar * 1e3 / ms, 4),
+            "t_star_ms": round(tstar * 1e3, 4),
+            "busbw_GBps": round(alg * (n - 1) / n, 2),
+            "roofline": {"bound": "nvlink", "achieved": round(achieved, 1), "peak": NVLINK_PEAK_GBS,
+                         "unit": "GB/s", "frac": round(achieved / NVLINK_PEAK_GBS, 4),
+                         "peak_kind": "fallback: B200_PROFILING.md measured peer copy per direction",
+                         "nominal": NVLINK_NOMINAL_GBS,
+                         "algorithmic_bytes_per_launch": ingress,
+                         "traffic": None},
+            "e2e": {"value": round(gbs(M, e2e_ms), 3), "unit": "GB/s",
+                    "h2d_bytes_per_step": S * 4, "d2h_bytes_per_step": M,
+                    "ms_per_step": round(e2e_ms, 3)},
+            "gpu_launches": args.steps * info["launches"],
+            "clocks": clk.summary(),
+            "nccl": {"ms": round(nccl_ms, 4), "algbw_GBps": round(gbs(M, nccl_ms), 2),
+                     "bitexact_vs_forestcoll": ok},
+        }
+        line.update(extra)
+        print(json.dumps(line), flush=True)
+    comm.close()
+    dist.destroy_process_group()
+
+
+def sweep_multi(comm, dist, n, dev, args):
+    import torch
+
+    res = {"sweep": []}
+    steps, warm = max(5, args.steps), 3
+
+    def rec(coll, M, ms, nccl_ms, dtype):
+        t = comm.t_star(coll, M)
+        res["sweep"].append({"collective": coll, "M_bytes": M, "dtype": dtype, "ms": round(ms, 4),
+                             "algbw_GBps": round(gbs(M, ms), 2), "frac_of_t_star": round(t * 1e3 / ms, 4),
+                             "nccl_ms": round(nccl_ms, 4), "nccl_algbw_GBps": round(gbs(M, nccl_ms), 2)})
+
+    for mib in (1, 64, 1024):
+        M = mib * MIB
+        S = M // n // 4
+        inp = torch.randn(S, device=dev)
+        out = comm.empty(n * S, dtype=torch.float32)
+        o2 = torch.empty_like(out)
+        ms = timed(lambda: comm.all_gather(out, inp), steps, warm, dist)
+        nm = timed(lambda: dist.all_gather_into_tensor(o2, inp), steps, warm, dist)
+        rec("allgather", S * 4 * n, ms, nm, "float32")
+        comm.deregister(out)
+    for mib, dt in ((256, torch.float32), (256, torch.bfloat16)):
+        M = mib * MIB
+        R = M // n // torch.tensor([], dtype=dt).element_size()
+        inp = torch.randn(R * n, device=dev).to(dt)
+        out = torch.empty(R, device=dev, dtype=dt)
+        ms = timed(lambda: comm.reduce_scatter(out, inp), steps, warm, dist)
+        nm = timed(lambda: dist.reduce_scatter_tensor(out, inp), steps, warm, dist)
+        rec("reduce_scatter", M, ms, nm, str(dt).split(".")[-1])
+    for mib in (25, 1024):
+        M = mib * MIB
+        cnt = M // 2
+        buf = comm.empty(cnt, dtype=torch.bfloat16)
+        buf.normal_()
+        ms = timed(lambda: comm.all_reduce(buf), steps, warm, dist)
+        nm = timed(lambda: dist.all_reduce(buf), steps, warm, dist)
+        rec("allreduce", M, ms, nm, "bfloat16")
+        comm.deregister(buf)
+    comm.check()
+    return res
+
+
+# ---------------------------------------------------------------------------
+# reference arm: CPU executor on the host
+# ---------------------------------------------------------------------------
+def run_reference(args):
+    rank = int(os.environ.get("RANK", 0))
+    if rank != 0:
+        return
+    from paper_2402_06787_b200.generator import get_schedule
+    from paper_2402_06787_b200.topology import nvswitch_doc
+
+    n = 8 if args.gpus <= 1 else args.gpus
+    s = get_schedule(nvswitch_doc(n), "allgather", validate=False)
+    shard_bytes = 16 * MIB
+    import numpy as np
+
+    from oracle import forest_oracle as fo
+
+    S = shard_bytes // 4
+    sends = [np.random.default_rng(r).standard_normal(S).astype(np.float32) for r in range(n)]
+    for _ in range(args.warmup):
+        fo.allgather(s, sends)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        fo.allgather(s, sends)
+    el = (time.perf_counter() - t0) / args.steps
+    M = n * shard_bytes
+    v = round(gbs(M, el * 1e3), 3)
+    wl = (f"nvs8-forest-allgather-virtual8-{args.shard_mib}MiBx8" if args.gpus <= 1
+          else f"nvs{n}-forest-allgather-{args.msg_mib}MiB")
+    line = {
+        "impl": "reference",
+        "metric": "collective algbw GB/s (ForestColl allgather, M = total output bytes per rank)",
+        "value": v, "unit": "GB/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(el * 1e3, 3), "higher_is_better": True,
+        "scaling": "weak" if args.gpus <= 1 else "strong", "vs_baseline": None,
+        "dtype": "u8 (fp32 payload, byte copy)", "data": "synthetic numpy fp32 shards",
+        "config": {"workload": wl, "sample_shard_bytes": shard_bytes},
+        "cpu_baseline": {"value": v, "unit": "GB/s", "cores": 1, "kind": "port",
+                         "sample": f"oracle.forest_oracle.allgather on nvswitch({n}) forest, "
+                                   f"{n} x {shard_bytes // MIB} MiB shards per step (the reference "
+                                   f"ships no executor; this is its CPU restatement)"},
+        "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--msg-mib", type=int, default=1024, help="N>=2: allgather total output")
+    ap.add_argument("--shard-mib", type=int, default=64, help="N=1: per virtual rank shard")
+    ap.add_argument("--quick", action="store_true", help="skip the RS/AR/size sweep")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+    if args.impl == "reference":
+        return run_reference(args)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world > 1:
+        run_multi(args)
+    else:
+        run_single(args)
+
+
+if __name__ == "__main__":
+    main()

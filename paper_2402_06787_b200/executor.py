@@ -195,10 +195,12 @@ class ForestCollComm(_CommBase):
         if world_size > 1:
             self._group = group if group is not None else dist.new_group(backend="gloo")
         self.nranks = world_size
+        self.topology_source = "given"
         doc = _as_doc(topology)
         if doc is None and not schedules:
             buses = self._allgather_obj(_pci_bus_id(device))
-            doc = discover_for_torch(world_size, None if None in buses else buses)
+            doc, self.topology_source = discover_for_torch(world_size,
+                                                           None if None in buses else buses)
         super().__init__(doc, world_size, schedules, validate, prune)
         comm = ctypes.c_void_p()
         _lib.check(self._lib.fc_comm_init(rank, world_size, device, int(scratch_bytes),

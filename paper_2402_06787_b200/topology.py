@@ -179,14 +179,15 @@ def _bus(b) -> str:
     return ":".join(parts)
 
 
-def discover_for_torch(world_size: int, pci_bus_ids: Sequence[str] | None = None) -> dict:
-    """Topology for `world_size` ranks: NVML when it works, else the
-    nominal B200 NVSwitch model (900 GB/s per GPU per direction)."""
+def discover_for_torch(world_size: int, pci_bus_ids: Sequence[str] | None = None):
+    """(topology, source) for `world_size` ranks: NVML when it works
+    ("nvml"), else the nominal B200 NVSwitch model, 900 GB/s per GPU per
+    direction ("nominal")."""
     if world_size >= 2:
         try:
             doc = discover_nvml(pci_bus_ids)
             if len(compute_ids(doc)) == world_size:
-                return doc
+                return doc, "nvml"
         except Exception:
             pass
-    return nvswitch_doc(world_size)
+    return nvswitch_doc(world_size), "nominal"

@@ -1,0 +1,100 @@
+"""torchrun worker: multi-GPU parity of ForestCollComm against the oracle.
+
+Every rank regenerates all ranks' seeded inputs on the host, so it can run
+the CPU oracle itself and compare its own device output bit-for-bit.
+Launched by tests/test_gpu_multiproc.py (one process per GPU).
+"""
+
+import os
+import sys
+
+REPO = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, REPO)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+from oracle import forest_oracle as fo  # noqa: E402
+from paper_2402_06787_b200 import ForestCollComm  # noqa: E402
+from paper_2402_06787_b200.topology import nvswitch_doc  # noqa: E402
+
+
+def host(t):
+    if t.dtype == torch.bfloat16:
+        return t.view(torch.int16).cpu().numpy().view(np.uint16)
+    return t.cpu().numpy()
+
+
+def seeded(n_el, dtype, seed, bits=False):
+    g = torch.Generator().manual_seed(seed)
+    if dtype == torch.int32:
+        return torch.randint(-2**20, 2**20, (n_el,), generator=g, dtype=torch.int32)
+    if bits:
+        # raw bit patterns (NaN / denormal / inf included) for byte-exact checks
+        return torch.randint(0, 2**31 - 1, (n_el,), generator=g, dtype=torch.int32).view(torch.float32)
+    return torch.empty(n_el).uniform_(-1, 1, generator=g).to(dtype)
+
+
+def main():
+    local = int(os.environ["LOCAL_RANK"])
+    torch.cuda.set_device(local)
+    dev = torch.device(f"cuda:{local}")
+    dist.init_process_group("nccl", device_id=dev)
+    rank, n = dist.get_rank(), dist.get_world_size()
+    topo = nvswitch_doc(n)
+    comm = ForestCollComm(topo, rank=rank, world_size=n, device=local,
+                          options={"timeout_ms": 20000})
+    fails = []
+    # allgather: odd and aligned sizes, bit patterns
+    for S in (1, 333, 4096, 1 << 20, (1 << 22) + 5):
+        for seed in (10, 11):
+            sends = [seeded(S, torch.float32, seed * 100 + r, bits=seed % 2 == 1) for r in range(n)]
+            out = comm.empty(n * S, dtype=torch.float32)
+            out.fill_(-7.0)
+            comm.all_gather(out, sends[rank].to(dev))
+            torch.cuda.synchronize()
+            ref = fo.allgather(comm.schedule("allgather"), [host(x) for x in sends])[rank]
+            if not np.array_equal(host(out).view(np.uint8), ref.view(np.uint8)):
+                fails.append(f"allgather S={S} seed={seed}")
+    # reduce-scatter
+    for dtype, name in ((torch.float32, "float32"), (torch.bfloat16, "bfloat16"), (torch.int32, "int32")):
+        for S in (7, 1000, (1 << 20) + 3):
+            ins = [seeded(n * S, dtype, 500 + r + 2 * S) for r in range(n)]
+            out = torch.zeros(S, dtype=dtype, device=dev)
+            comm.reduce_scatter(out, ins[rank].to(dev))
+            torch.cuda.synchronize()
+            ref = fo.reduce_scatter(comm.schedule("reduce_scatter"), [host(x) for x in ins], name)[rank]
+            if not np.array_equal(host(out).view(np.uint8), ref.view(np.uint8)):
+                fails.append(f"reduce_scatter {name} S={S}")
+    # allreduce (in place)
+    for dtype, name in ((torch.bfloat16, "bfloat16"), (torch.float32, "float32"), (torch.int32, "int32")):
+        for count in (5, 12345, 1 << 22):
+            ins = [seeded(count, dtype, 900 + r + count) for r in range(n)]
+            buf = comm.empty(count, dtype=dtype)
+            buf.copy_(ins[rank].to(dev))
+            comm.all_reduce(buf)
+            torch.cuda.synchronize()
+            ref = fo.allreduce(comm.schedule("allreduce"), [host(x) for x in ins], name)[rank]
+            if not np.array_equal(host(buf).view(np.uint8), ref.view(np.uint8)):
+                fails.append(f"allreduce {name} count={count}")
+    # back-to-back calls reusing buffers (entry barrier / epoch reuse)
+    S = 1 << 18
+    out = comm.empty(n * S, dtype=torch.float32)
+    for it in range(20):
+        sends = [seeded(S, torch.float32, 7000 + it * 16 + r) for r in range(n)]
+        comm.all_gather(out, sends[rank].to(dev))
+        got = host(out).copy()
+        ref = fo.allgather(comm.schedule("allgather"), [host(x) for x in sends])[rank]
+        if not np.array_equal(got.view(np.uint8), ref.view(np.uint8)):
+            fails.append(f"allgather repeat {it}")
+            break
+    comm.check()
+    print(f"RANK {rank} {'OK' if not fails else 'FAIL ' + '; '.join(fails)}", flush=True)
+    comm.close()
+    dist.destroy_process_group()
+    sys.exit(1 if fails else 0)
+
+
+if __name__ == "__main__":
+    main()
