@@ -1,0 +1,63 @@
+"""Golden schedule fixtures are the reference generator's own output."""
+
+import json
+import os
+import subprocess
+import sys
+from fractions import Fraction
+
+import pytest
+
+from conftest import GOLDEN, REPO, golden_names, load_golden, load_golden_topology, reference_collsched
+
+
+def test_fixtures_match_reference_generator():
+    cs = reference_collsched()
+    if cs is None:
+        pytest.skip("reference collsched not importable")
+    r = subprocess.run([sys.executable, os.path.join(GOLDEN, "make_golden.py"), "--check"],
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("name", golden_names())
+def test_fixture_validates_and_attains_bound(name):
+    cs = reference_collsched()
+    if cs is None:
+        pytest.skip("reference collsched not importable")
+    topo = name.rsplit("_", 1)[0] if not name.endswith("reduce_scatter") else name[: -len("_reduce_scatter")]
+    t = cs.parse_topology(json.dumps(load_golden_topology(topo)))
+    with open(os.path.join(GOLDEN, "schedules", name + ".json")) as f:
+        s = cs.parse_schedule(f.read())
+    from paper_2402_06787_b200.generator import meta_of
+
+    rep = cs.validate_schedule(s, t, meta_of(s))
+    assert rep.ok, rep.violations
+    phases = 2 if s.collective == "allreduce" else 1
+    assert cs.congestion_time(s, t) == phases * Fraction(s.inv_x_star) / s.num_compute
+
+
+def test_package_cache_serves_reference_schedules_without_reference(monkeypatch):
+    """The GPU box has no reference: the shipped cache must yield the same
+    forests as the fixtures, through the package's own JSON reader."""
+    from paper_2402_06787_b200 import _refpath, generator
+    from paper_2402_06787_b200.topology import groups_switch_doc, nvswitch_doc
+
+    monkeypatch.setattr(_refpath, "_CACHED", [None])
+    monkeypatch.setenv("FORESTCOLL_CACHE", "/nonexistent-cache-dir")
+    cases = {f"nvs{n}": nvswitch_doc(n) for n in (2, 4, 8)}
+    cases.update({f"groups{b}": groups_switch_doc(b) for b in (450, 300, 100)})
+    for name, doc in cases.items():
+        assert doc == load_golden_topology(name)
+        for coll in ("allgather", "reduce_scatter", "allreduce"):
+            s = generator.get_schedule(doc, coll, validate=False, write_cache=False)
+            with open(os.path.join(GOLDEN, "schedules", f"{name}_{coll}.json")) as f:
+                assert generator.export_json(s) == f.read()
+
+
+def test_appendix_a_forest_shape():
+    """nvswitch(8) allgather forest as listed in SURVEY.md Appendix A."""
+    s = load_golden("nvs8_allgather")
+    rows = {rt.root: " ".join(f"{e.src[1:]}>{e.dst[1:]}" for e in rt.batches[0].edges) for rt in s.roots}
+    assert rows["g0"] == "0>1 0>2 0>3 0>4 4>7 7>6 6>5"
+    assert rows["g7"] == "7>6 6>5 5>4 4>3 3>2 2>1 1>0"
