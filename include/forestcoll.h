@@ -83,11 +83,14 @@ extern "C" {
 #define FC_SUM 0
 
 /* options for fc_comm_set_option */
-#define FC_OPT_CTAS_PER_RANK 1 /* CTAs per rank (default 32 real, 16 virtual) */
-#define FC_OPT_CHUNK_MAX 2     /* max bytes per pipeline chunk (default 512 KiB) */
-#define FC_OPT_CHUNK_MIN 3     /* min bytes per pipeline chunk (default 8 KiB) */
-#define FC_OPT_ITEMS_PER_WORKER 4 /* target work items per worker (default 4) */
+#define FC_OPT_CTAS_PER_RANK 1 /* CTAs per rank (default 96 real, 16 virtual) */
+#define FC_OPT_CHUNK_MAX 2     /* max bytes per pipeline chunk (default 256 KiB) */
+#define FC_OPT_CHUNK_MIN 3     /* min bytes per pipeline chunk (default 16 KiB) */
+#define FC_OPT_ITEMS_PER_WORKER 4 /* target work items per CTA (default 4) */
 #define FC_OPT_TIMEOUT_MS 5    /* device flag-wait timeout (default 10000 ms) */
+#define FC_OPT_LAG 6           /* claim-order skew, chunks per tree stage (default 16) */
+#define FC_OPT_COPY_MODE 7     /* 0: TMA bulk stores, 1: TMA loads + vector stores (default 0) */
+#define FC_OPT_DMA_ROOT_COPY 8 /* allgather: copy engine places the own shard (default 0) */
 
 typedef struct fc_comm fc_comm_t;
 
@@ -135,6 +138,13 @@ int fc_allreduce_multi(fc_comm_t* comm, const void* const* sends,
 
 /* statistics of the last collective call (launches, chunks, bytes) */
 int fc_last_call_info(const fc_comm_t* comm, long long* info, int ninfo);
+
+/* item tracing: 32-byte records {u64 t_start, u64 t_end (ns, %globaltimer),
+ * u32 t_wait (ns waiting on flags), i32 chunk, i16 rank, i16 task,
+ * i16 worker, u16 launch} appended at atomicAdd(*count) while
+ * *count < capacity; pass records == NULL to disable. */
+int fc_comm_set_trace(fc_comm_t* comm, void* records, unsigned int* count,
+                      unsigned int capacity);
 
 #ifdef __cplusplus
 }

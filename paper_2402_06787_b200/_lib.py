@@ -18,12 +18,16 @@ LIB_PATH = os.path.join(LIB_DIR, "libforestcoll.so")
 FC_ALLGATHER, FC_REDUCE_SCATTER, FC_ALLREDUCE = 0, 1, 2
 FC_SUM = 0
 OPT_CTAS_PER_RANK, OPT_CHUNK_MAX, OPT_CHUNK_MIN, OPT_ITEMS_PER_WORKER, OPT_TIMEOUT_MS = 1, 2, 3, 4, 5
+OPT_LAG, OPT_COPY_MODE, OPT_DMA_ROOT_COPY = 6, 7, 8
 OPTIONS = {
     "ctas_per_rank": OPT_CTAS_PER_RANK,
     "chunk_max": OPT_CHUNK_MAX,
     "chunk_min": OPT_CHUNK_MIN,
     "items_per_worker": OPT_ITEMS_PER_WORKER,
     "timeout_ms": OPT_TIMEOUT_MS,
+    "lag": OPT_LAG,
+    "copy_mode": OPT_COPY_MODE,
+    "dma_root_copy": OPT_DMA_ROOT_COPY,
 }
 
 # symbol -> (restype, argtypes)
@@ -54,6 +58,7 @@ SIGNATURES = {
     "fc_reduce_scatter_multi": (_I, [_P, _P, _P, _SZ, _I, _I, _P]),
     "fc_allreduce_multi": (_I, [_P, _P, _P, _SZ, _I, _I, _P]),
     "fc_last_call_info": (_I, [_P, ctypes.POINTER(_LL), _I]),
+    "fc_comm_set_trace": (_I, [_P, _P, _P, ctypes.c_uint]),
 }
 
 _LIB = []

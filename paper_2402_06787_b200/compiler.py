@@ -52,6 +52,7 @@ TW_KIND, TW_TREE, TW_STAGE, TW_ROOT, TW_MLO, TW_MHI = 0, 1, 2, 3, 4, 5
 TW_AG_PARENT, TW_N_AG_CHILD, TW_AG_CHILD = 6, 7, 8
 TW_RS_PARENT, TW_RS_PSLOT, TW_RS_PPREFIX, TW_N_RS_CHILD = 24, 25, 26, 27
 TW_RS_CHILD, TW_RS_CSLOT, TW_RS_CPREFIX = 28, 44, 60
+TW_LAG, TW_AG_LEAFMASK = 76, 77
 
 
 @dataclass
@@ -88,6 +89,8 @@ class Task:
     rs_children: tuple = ()
     rs_cslots: tuple = ()
     rs_cprefix: tuple = ()
+    lag: int = 0  # dense stage index (claim-order skew), set by lower()
+    leafmask: int = 0  # bit j: ag_children[j] is a leaf of this tree
 
 
 @dataclass
@@ -285,6 +288,14 @@ def lower(schedule, ranks=None, collective: str | None = None) -> Plan:
                     else:
                         tasks[v].append(Task(K_WAIT_AG, **kw))
 
+    # dense stage index, global over ranks: the kernel claims item (c, task)
+    # at diagonal c + lag * index, so dependencies stay at smaller diagonals
+    dense = {st: i for i, st in enumerate(sorted({x.stage for ts in tasks for x in ts}))}
+    for ts in tasks:
+        for x in ts:
+            x.lag = dense[x.stage]
+            tr = trees[x.tree]
+            x.leafmask = sum(1 << j for j, ch in enumerate(x.ag_children) if not tr.children[ch])
     nactive, nwait = [], []
     for v in range(n):
         act = sorted((x for x in tasks[v] if x.kind != K_WAIT_AG), key=lambda x: (x.stage, x.tree))
@@ -324,6 +335,8 @@ def encode(coll, n, k, trees, tasks, nactive, nwait, slot_units, nslots) -> np.n
             row[TW_RS_CHILD:TW_RS_CHILD + m] = t.rs_children
             row[TW_RS_CSLOT:TW_RS_CSLOT + m] = t.rs_cslots
             row[TW_RS_CPREFIX:TW_RS_CPREFIX + m] = t.rs_cprefix
+            row[TW_LAG] = t.lag
+            row[TW_AG_LEAFMASK] = t.leafmask
             pos += TASK_WORDS
     return a
 

@@ -16,7 +16,7 @@ namespace {
 
 constexpr uint32_t kCommMagic = 0x4d4d4346;  // 'FCMM'
 constexpr uint32_t kBufMagic = 0x46554246;   // 'FBUF'
-constexpr int kMaxC = 512;                   // flag slots per tree / slot (chunks per launch)
+constexpr int kMaxC = 2048;                  // flag slots per tree / slot (chunks per launch)
 constexpr int kTreeCap = 256;
 constexpr int kSlotCap = 512;
 constexpr size_t kCtlBytes = 256;
@@ -50,7 +50,7 @@ struct Plan {
   int nranks = 0, k = 0, ntrees = 0, max_slot_units = 0, max_slots = 0, max_mult = 0;
   long long active_total = 0;
   int* d_tasks[FC_MAXR] = {};
-  int nact[FC_MAXR] = {}, nwait[FC_MAXR] = {};
+  int nact[FC_MAXR] = {}, nwait[FC_MAXR] = {}, lag_max[FC_MAXR] = {};
 };
 
 typedef CUresult (*PFN_getRange)(CUdeviceptr*, size_t*, CUdeviceptr);
@@ -65,9 +65,17 @@ struct fc_comm {
   std::vector<Mapping> maps;
   std::vector<Reg> regs;
   Plan plans[3];
-  int ctas_per_rank = 32;
-  long long chunk_max = 512 << 10, chunk_min = 8 << 10, items_per_worker = 4;
+  int ctas_per_rank = 64;
+  long long chunk_max = 256 << 10, chunk_min = 16 << 10, items_per_worker = 4;
   long long timeout_ms = 10000;
+  int lag = 16;
+  int copy_mode = 1;
+  int dma_root_copy = 0;
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  FcTraceRec* trace = nullptr;
+  unsigned* trace_count = nullptr;
+  unsigned trace_cap = 0;
   std::string err;
   long long info[8] = {};
 };
@@ -121,7 +129,7 @@ int alloc_workspace(fc_comm* c, char** out) {
 
 int setup_layout(fc_comm* c, size_t scratch_bytes) {
   c->flags_off = kCtlBytes;
-  c->flags_words = FC_READY_WORDS + (size_t)(kTreeCap + kSlotCap) * kMaxC;
+  c->flags_words = FC_READY_WORDS + kTreeCap + (size_t)(kTreeCap + kSlotCap) * kMaxC;
   c->scratch_off = align_up(c->flags_off + c->flags_words * 4, 4096);
   c->scratch_bytes = align_up(scratch_bytes, 4096);
   c->ws_bytes = c->scratch_off + c->scratch_bytes;
@@ -210,6 +218,7 @@ int run(fc_comm* c, int coll, const void* const* sends, void* const* recvs, size
     P.tasks[i] = pl.d_tasks[i];
     P.nactive[i] = pl.nact[i];
     P.nwait[i] = pl.nwait[i];
+    P.lag_max[i] = pl.lag_max[i];
     P.ctl[i] = (FcCtl*)c->ws[r];
     P.send[r] = (const char*)sends[i];
     P.recv[r] = (char*)recvs[i];
@@ -231,15 +240,21 @@ int run(fc_comm* c, int coll, const void* const* sends, void* const* recvs, size
   P.dtype = dtype;
   P.op = op;
   P.maxc = kMaxC;
-  P.ag_flag_off = FC_READY_WORDS;
-  P.rs_flag_off = FC_READY_WORDS + kTreeCap * kMaxC;
+  P.cnt_off = FC_READY_WORDS;
+  P.ag_flag_off = FC_READY_WORDS + kTreeCap;
+  P.rs_flag_off = P.ag_flag_off + kTreeCap * kMaxC;
   P.timeout_ns = c->timeout_ms * 1000000LL;
   P.ctas_per_rank = c->ctas_per_rank;
+  P.lag = c->lag;
+  P.copy_mode = c->copy_mode;
+  P.trace = c->trace;
+  P.trace_count = c->trace_count;
+  P.trace_cap = c->trace_cap;
 
   // chunk plan: identical on every rank (depends on S, dtype, plan, options)
   const long long slice_unit = (S + pl.k - 1) / pl.k * es;  // bytes per unit of multiplicity
   const long long max_slice = slice_unit * pl.max_mult;
-  const long long workers = (long long)c->ctas_per_rank * 4;
+  const long long workers = (long long)c->ctas_per_rank;  // one item in flight per CTA
   const long long avg_active = std::max(1LL, pl.active_total / N);
   long long n = (max_slice + c->chunk_max - 1) / c->chunk_max;
   n = std::max(n, (c->items_per_worker * workers + avg_active - 1) / avg_active);
@@ -264,6 +279,23 @@ int run(fc_comm* c, int coll, const void* const* sends, void* const* recvs, size
   P.nchunks = (int)n;
   const int coop = c->virt ? 1 : 0;
   int launches = 0, grid = 0;
+  // allgather: a copy engine places each local root's own shard into its
+  // output concurrently with the kernel (no SM bandwidth spent on it)
+  bool dma = false;
+  if (coll == FC_ALLGATHER && c->dma_root_copy) {
+    FC_CUDA(c, cudaEventRecord(c->ev_fork, (cudaStream_t)stream));
+    FC_CUDA(c, cudaStreamWaitEvent(c->side, c->ev_fork, 0));
+    for (int i = 0; i < c->nlocal; ++i) {
+      const int r = P.local_rank[i];
+      char* dstp = P.recv[r] + (size_t)r * S * es;
+      if (dstp != P.send[r])
+        FC_CUDA(c, cudaMemcpyAsync(dstp, P.send[r], (size_t)S * es, cudaMemcpyDeviceToDevice,
+                                   c->side));
+    }
+    FC_CUDA(c, cudaEventRecord(c->ev_join, c->side));
+    P.root_local_done = 1;
+    dma = true;
+  }
   for (long long c0 = 0; c0 < n; c0 += W) {
     P.c0 = (int)c0;
     P.c1 = (int)std::min(n, c0 + W);
@@ -272,6 +304,7 @@ int run(fc_comm* c, int coll, const void* const* sends, void* const* recvs, size
       return fail(c, FC_ERR_CUDA, "kernel launch failed: %s", cudaGetErrorString((cudaError_t)e));
     ++launches;
   }
+  if (dma) FC_CUDA(c, cudaStreamWaitEvent((cudaStream_t)stream, c->ev_join, 0));
   c->info[0] = launches;
   c->info[1] = n;
   c->info[2] = W;
@@ -291,6 +324,13 @@ int free_plan(fc_comm* c, Plan& p) {
   return FC_SUCCESS;
 }
 
+int make_side_stream(fc_comm* c) {
+  FC_CUDA(c, cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+  FC_CUDA(c, cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+  FC_CUDA(c, cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
+  return FC_SUCCESS;
+}
+
 int default_ctas(fc_comm* c) {
   int per_sm = 0, sms = 0;
   FC_CUDA(c, (cudaError_t)fc_max_ctas_per_sm(FC_FLOAT32, &per_sm));
@@ -302,8 +342,8 @@ int default_ctas(fc_comm* c) {
   FC_CUDA(c, cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));
   const int cap = per_sm * sms / c->nlocal;
   if (cap < 1) return fail(c, FC_ERR_UNSUPPORTED, "device cannot co-schedule %d ranks", c->nlocal);
-  c->ctas_per_rank = std::min(c->virt ? 16 : 32, cap);
-  return FC_SUCCESS;
+  c->ctas_per_rank = std::min(c->virt ? 16 : 96, cap);
+  return make_side_stream(c);
 }
 
 }  // namespace
@@ -434,6 +474,17 @@ int fc_comm_set_option(fc_comm_t* c, int option, long long v) {
       if (v < 1) return fail(c, FC_ERR_INVALID_ARG, "timeout must be positive");
       c->timeout_ms = v;
       return FC_SUCCESS;
+    case FC_OPT_LAG:
+      if (v < 0 || v > 4096) return fail(c, FC_ERR_INVALID_ARG, "lag out of range");
+      c->lag = (int)v;
+      return FC_SUCCESS;
+    case FC_OPT_COPY_MODE:
+      if (v < 0 || v > 1) return fail(c, FC_ERR_INVALID_ARG, "copy_mode is 0 or 1");
+      c->copy_mode = (int)v;
+      return FC_SUCCESS;
+    case FC_OPT_DMA_ROOT_COPY:
+      c->dma_root_copy = v ? 1 : 0;
+      return FC_SUCCESS;
     default:
       return fail(c, FC_ERR_INVALID_ARG, "unknown option %d", option);
   }
@@ -447,6 +498,9 @@ int fc_comm_get_option(fc_comm_t* c, int option, long long* v) {
     case FC_OPT_CHUNK_MIN: *v = c->chunk_min; return FC_SUCCESS;
     case FC_OPT_ITEMS_PER_WORKER: *v = c->items_per_worker; return FC_SUCCESS;
     case FC_OPT_TIMEOUT_MS: *v = c->timeout_ms; return FC_SUCCESS;
+    case FC_OPT_LAG: *v = c->lag; return FC_SUCCESS;
+    case FC_OPT_COPY_MODE: *v = c->copy_mode; return FC_SUCCESS;
+    case FC_OPT_DMA_ROOT_COPY: *v = c->dma_root_copy; return FC_SUCCESS;
     default: return fail(c, FC_ERR_INVALID_ARG, "unknown option %d", option);
   }
 }
@@ -476,6 +530,9 @@ int fc_comm_destroy(fc_comm_t* c) {
   cudaDeviceSynchronize();
   for (auto& p : c->plans) free_plan(c, p);
   for (auto& m : c->maps) cudaIpcCloseMemHandle(m.base);
+  if (c->side) cudaStreamDestroy(c->side);
+  if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+  if (c->ev_join) cudaEventDestroy(c->ev_join);
   for (int r = 0; r < FC_MAXR; ++r)
     if (c->own[r]) cudaFree(c->ws[r]);
   delete c;
@@ -595,6 +652,7 @@ int fc_plan_load(fc_comm_t* c, int coll, const int32_t* t, size_t nwords) {
         (T[TW_RS_PARENT] < 0 || T[TW_RS_PARENT] >= N || T[TW_RS_PSLOT] < 0 ||
          T[TW_RS_PSLOT] >= kSlotCap))
       return fail(c, FC_ERR_PLAN, "task row %d: bad reduce parent", i);
+    if (T[TW_LAG] < 0 || T[TW_LAG] > 64) return fail(c, FC_ERR_PLAN, "task row %d: bad lag", i);
     p.max_mult = std::max(p.max_mult, T[TW_MHI] - T[TW_MLO]);
   }
   for (int r = 0; r < N; ++r) {
@@ -611,6 +669,8 @@ int fc_plan_load(fc_comm_t* c, int coll, const int32_t* t, size_t nwords) {
     const int rows = std::max(1, D[RD_NACTIVE] + D[RD_NWAIT]);
     p.nact[i] = D[RD_NACTIVE];
     p.nwait[i] = D[RD_NWAIT];
+    for (int j = 0; j < D[RD_NACTIVE]; ++j)
+      p.lag_max[i] = std::max(p.lag_max[i], t[task0 + (size_t)(D[RD_FIRST] + j) * FC_TASK_WORDS + TW_LAG]);
     cudaError_t e = cudaMalloc((void**)&p.d_tasks[i], (size_t)rows * FC_TASK_WORDS * 4);
     if (e == cudaSuccess && D[RD_NACTIVE] + D[RD_NWAIT] > 0)
       e = cudaMemcpy(p.d_tasks[i], t + task0 + (size_t)D[RD_FIRST] * FC_TASK_WORDS,
@@ -653,6 +713,15 @@ int fc_allreduce(fc_comm_t* c, const void* send, void* recv, size_t count, int d
                  void* stream) {
   if (c && c->virt) return fail(c, FC_ERR_INVALID_ARG, "virtual comm: use the _multi variant");
   return run(c, FC_ALLREDUCE, &send, &recv, count, dtype, op, stream);
+}
+
+int fc_comm_set_trace(fc_comm_t* c, void* records, unsigned int* count, unsigned int cap) {
+  if (!c) return FC_ERR_INVALID_ARG;
+  if (records && !count) return fail(c, FC_ERR_INVALID_ARG, "trace needs a counter");
+  c->trace = (FcTraceRec*)records;
+  c->trace_count = records ? count : nullptr;
+  c->trace_cap = records ? cap : 0;
+  return FC_SUCCESS;
 }
 
 int fc_last_call_info(const fc_comm_t* c, long long* info, int ninfo) {

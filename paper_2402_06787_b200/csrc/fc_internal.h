@@ -42,7 +42,9 @@ enum {
   TW_RS_CHILD = 28,    // [FC_MAXR]
   TW_RS_CSLOT = 44,    // [FC_MAXR]
   TW_RS_CPREFIX = 60,  // [FC_MAXR]
-  TW_END = 76,
+  TW_LAG = 76,         // dense stage index: claim-order skew (chunk + lag * TW_LAG)
+  TW_AG_LEAFMASK = 77, // bit j: AG child j is a leaf (gets an arrival count, no chunk flags)
+  TW_END = 78,
 };
 
 // Header word offsets of a plan table (see compiler.py for the writer).
@@ -74,6 +76,16 @@ struct FcCtl {
 #define FC_DEVERR_TIMEOUT_RS 2
 #define FC_DEVERR_TIMEOUT_READY 3
 
+// One record per executed item when tracing is enabled (fc_comm_set_trace).
+struct FcTraceRec {
+  unsigned long long t_start, t_end;  // %globaltimer ns: claim .. published
+  unsigned t_wait;                    // ns spent waiting on flags / readiness
+  int chunk;
+  short rank, task;
+  short worker;
+  unsigned short launch;  // epoch (low 16 bits)
+};
+
 struct FcParams {
   int nranks;
   int nlocal;
@@ -83,6 +95,7 @@ struct FcParams {
   const int* tasks[FC_MAXR];  // by local index: this rank's task rows
   int nactive[FC_MAXR];
   int nwait[FC_MAXR];
+  int lag_max[FC_MAXR];       // by local index: max TW_LAG over active tasks
   FcCtl* ctl[FC_MAXR];        // by local index
   // by rank: this process's view (peer-mapped for remote ranks)
   const char* send[FC_MAXR];  // only local ranks are dereferenced
@@ -100,11 +113,19 @@ struct FcParams {
   int nchunks;  // chunks per tree slice for the whole call
   int c0, c1;   // chunk window of this launch
   int maxc;     // flag stride per tree / slot
+  int cnt_off;      // word offset of per-tree leaf arrival counters
   int ag_flag_off;  // word offset of AG flags in the flags region
   int rs_flag_off;  // word offset of RS flags in the flags region
+  int lag;          // claim-order skew in chunks per stage
+  int copy_mode;    // 0: TMA bulk stores, 1: bulk loads + 16-byte lane stores
+  int root_local_done;  // allgather: own shard already placed in recv (DMA engine)
+  FcTraceRec* trace;
+  unsigned* trace_count;
+  unsigned trace_cap;
 };
 
 // Kernel entry (fc_kernel.cu).  Returns a cudaError_t value.
 int fc_launch(const FcParams& p, int reduce_dtype, int cooperative,
               void* stream, int* grid_out);
 int fc_max_ctas_per_sm(int reduce_dtype, int* out);
+int fc_workers_per_cta();

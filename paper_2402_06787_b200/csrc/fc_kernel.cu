@@ -2,10 +2,12 @@
 //
 // One grid executes the tree tasks of one or more ranks (one rank per GPU in
 // production; all N ranks of a forest on one GPU in virtual mode).  Work is a
-// stream of items (task, chunk); workers (groups of FC_WT threads) claim
-// items dynamically from a per-rank counter in key order (chunk, stage), so
-// every flag wait targets an item with a strictly smaller key and the claim
-// order alone guarantees progress.
+// stream of items (task, chunk).  Workers — single warps, FC_WPC per CTA,
+// each owning an FC_NST-stage shared-memory ring — claim items dynamically
+// from a per-rank counter in a skewed key order (chunk + lag*stage, stage):
+// every flag wait targets an item with a strictly smaller key, so claim order
+// alone guarantees progress, and the lag lets a consumer's
+// input usually be complete by the time the item is claimed.
 //
 // Data semantics (reference anchors):
 //  * allgather: tree (root r, batch j) broadcasts elements
@@ -17,25 +19,40 @@
 //    partials in ascending rank order, accumulating in fp32 (fp types) or
 //    wrapping int32, and rounds to the buffer dtype once per hop.
 //  * allreduce: reduce-scatter then allgather on one forest
-//    (schedule.py:177-211); the root's reduced chunk is broadcast straight
-//    from registers.
+//    (schedule.py:177-211); the root's reduced chunk is stored straight to
+//    its own buffer and to its broadcast children.
+//
+// Data movement (Blackwell TMA bulk-copy engine): a worker's lane 0 streams
+// its chunk through the smem ring with cp.async.bulk global->shared loads
+// (mbarrier complete_tx) and, for copies, cp.async.bulk shared->global stores
+// issued once per destination straight into peer-mapped HBM over
+// NVLink5/NVSwitch (one local read feeds every child).  Reductions read the
+// bulk-loaded sources from smem with all 32 lanes and store 16-byte vectors.
 // Hops synchronise with system-scope release/acquire flags holding the
-// launch epoch; data moves with 16-byte vector loads (L2, .cg) and stores
-// issued directly to peer-mapped HBM over NVLink5/NVSwitch.
+// launch epoch.  Unaligned heads/tails use 16/8/4/2/1-byte vector loops.
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
+
 #include <climits>
 #include <cstdint>
 
 #include "fc_internal.h"
 
-#define FC_WT 128  // threads per worker
-#define FC_NW 4    // workers per CTA
-#define FC_BLOCK (FC_WT * FC_NW)
-#define FC_MAXS 17  // max sources / destinations per item (own + 16)
+#define FC_WPC 8                           // workers (warps) per CTA
+#define FC_BLOCK (32 * FC_WPC)
+#define FC_NST 3                           // smem stages per worker
+#define FC_STAGE (8 * 1024)                // bytes per stage
+#define FC_SMEM (FC_WPC * FC_NST * FC_STAGE)
+#define FC_MAXS 17                         // max sources / destinations per item
 
 namespace {
 
+// ---------------------------------------------------------------------------
+// PTX wrappers
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
 __device__ __forceinline__ unsigned ld_acquire_sys(const unsigned* p) {
   unsigned v;
   asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -44,17 +61,61 @@ __device__ __forceinline__ unsigned ld_acquire_sys(const unsigned* p) {
 __device__ __forceinline__ void st_release_sys(unsigned* p, unsigned v) {
   asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+__device__ __forceinline__ void red_release_sys_add(unsigned* p, unsigned v) {
+  asm volatile("red.release.sys.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 __device__ __forceinline__ unsigned ld_volatile(const unsigned* p) {
   return *reinterpret_cast<const volatile unsigned*>(p);
 }
 __device__ __forceinline__ void fence_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
-__device__ __forceinline__ void worker_bar(int w) {
-  asm volatile("bar.sync %0, %1;" ::"r"(w + 1), "r"(FC_WT) : "memory");
-}
 __device__ __forceinline__ unsigned long long globaltimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  unsigned ok = 0;
+  while (!ok) {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; "
+        "selp.u32 %0, 1, 0, p; }"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  }
+}
+__device__ __forceinline__ void bulk_load(void* sdst, const void* gsrc, unsigned bytes,
+                                          uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(sdst)),
+      "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void bulk_store(void* gdst, const void* ssrc, unsigned bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst),
+               "r"(smem_u32(ssrc)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read1() {
+  asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
 // Spin until *p >= e (wrapping compare).  Returns false on timeout or when
@@ -128,38 +189,93 @@ struct Red<FC_INT32> {  // also uint32: wrapping two's-complement add
   __device__ static A add(A a, A b) { return a + b; }
 };
 
+// acc (accumulator lanes of one 16-byte vector) <- first source
+template <int DT>
+struct Acc16 {
+  using R = Red<DT>;
+  using E = typename R::E;
+  static constexpr int NE = 16 / sizeof(E);
+  typename R::A a[NE];
+  __device__ __forceinline__ void init(const uint4& v) {
+    const E* e = reinterpret_cast<const E*>(&v);
+#pragma unroll
+    for (int q = 0; q < NE; ++q) a[q] = R::to(e[q]);
+  }
+  __device__ __forceinline__ void add(const uint4& v) {
+    const E* e = reinterpret_cast<const E*>(&v);
+#pragma unroll
+    for (int q = 0; q < NE; ++q) a[q] = R::add(a[q], R::to(e[q]));
+  }
+  __device__ __forceinline__ uint4 pack() const {
+    uint4 out;
+    E* e = reinterpret_cast<E*>(&out);
+#pragma unroll
+    for (int q = 0; q < NE; ++q) e[q] = R::from(a[q]);
+    return out;
+  }
+};
+
 // ---------------------------------------------------------------------------
-// Worker-wide data movement.  All pointers of one call share `off`.
+// Warp-level fallback movers (unaligned / heads / tails).  All pointers of
+// one call share `off`.
 // ---------------------------------------------------------------------------
 template <typename V, int U>
-__device__ __forceinline__ void copy_units(const char* src, char* const* dst, int ndst,
-                                           long long off, long long n, int wt) {
+__device__ __forceinline__ void warp_copy_units(const char* src, char* const* dst, int ndst,
+                                                long long off, long long n, int lane) {
   const V* s = reinterpret_cast<const V*>(src + off);
-  for (long long i = wt; i < n; i += (long long)FC_WT * U) {
+  for (long long i = lane; i < n; i += 32LL * U) {
     V v[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const long long j = i + (long long)u * FC_WT;
+      const long long j = i + 32LL * u;
       if (j < n) v[u] = __ldcg(s + j);
     }
     for (int d = 0; d < ndst; ++d) {
       V* dp = reinterpret_cast<V*>(dst[d] + off);
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        const long long j = i + (long long)u * FC_WT;
+        const long long j = i + 32LL * u;
         if (j < n) dp[j] = v[u];
       }
     }
   }
 }
 
+__device__ void warp_copy(const char* src, char* const* dst, int ndst, long long off,
+                          long long nbytes, int lane) {
+  if (nbytes <= 0) return;
+  const uintptr_t a0 = (uintptr_t)src + off;
+  uintptr_t diff = 0;
+  for (int d = 0; d < ndst; ++d) diff |= (uintptr_t)dst[d] - (uintptr_t)src;
+  int g = 16;
+  while (g > 1 && (diff & (uintptr_t)(g - 1))) g >>= 1;
+  long long head = (long long)((g - (a0 & (uintptr_t)(g - 1))) & (uintptr_t)(g - 1));
+  if (head > nbytes) head = nbytes;
+  for (long long i = lane; i < head; i += 32) {
+    const char v = src[off + i];
+    for (int d = 0; d < ndst; ++d) dst[d][off + i] = v;
+  }
+  const long long nu = (nbytes - head) / g;
+  const long long o2 = off + head;
+  switch (g) {
+    case 16: warp_copy_units<uint4, 8>(src, dst, ndst, o2, nu, lane); break;
+    case 8: warp_copy_units<uint2, 8>(src, dst, ndst, o2, nu, lane); break;
+    case 4: warp_copy_units<unsigned, 8>(src, dst, ndst, o2, nu, lane); break;
+    case 2: warp_copy_units<unsigned short, 8>(src, dst, ndst, o2, nu, lane); break;
+    default: warp_copy_units<unsigned char, 8>(src, dst, ndst, o2, nu, lane); break;
+  }
+  for (long long i = head + nu * g + lane; i < nbytes; i += 32) {
+    const char v = src[off + i];
+    for (int d = 0; d < ndst; ++d) dst[d][off + i] = v;
+  }
+}
+
 template <int DT>
-__device__ __forceinline__ void reduce_scalar(const char* const* src, int nsrc,
-                                              char* const* dst, int ndst, long long off,
-                                              long long nelem, int wt) {
+__device__ void warp_reduce_scalar(const char* const* src, int nsrc, char* const* dst, int ndst,
+                                   long long off, long long nelem, int lane) {
   using R = Red<DT>;
   using E = typename R::E;
-  for (long long i = wt; i < nelem; i += FC_WT) {
+  for (long long i = lane; i < nelem; i += 32) {
     const long long b = off + i * (long long)sizeof(E);
     typename R::A acc = R::to(__ldcg(reinterpret_cast<const E*>(src[0] + b)));
     for (int s = 1; s < nsrc; ++s)
@@ -169,104 +285,157 @@ __device__ __forceinline__ void reduce_scalar(const char* const* src, int nsrc,
   }
 }
 
-template <int DT, int U>
-__device__ __forceinline__ void reduce_vec(const char* const* src, int nsrc, char* const* dst,
-                                           int ndst, long long off, long long nvec, int wt) {
-  using R = Red<DT>;
-  using E = typename R::E;
-  using A = typename R::A;
-  constexpr int NE = 16 / sizeof(E);
-  constexpr int G = 4;  // sources loaded per batch
-  for (long long i = wt; i < nvec; i += (long long)FC_WT * U) {
-    A acc[U][NE];
-    for (int s0 = 0; s0 < nsrc; s0 += G) {
-      uint4 x[G][U];
-#pragma unroll
-      for (int g = 0; g < G; ++g) {
-        if (s0 + g < nsrc) {
-          const uint4* sp = reinterpret_cast<const uint4*>(src[s0 + g] + off);
-#pragma unroll
-          for (int u = 0; u < U; ++u) {
-            const long long j = i + (long long)u * FC_WT;
-            if (j < nvec) x[g][u] = __ldcg(sp + j);
-          }
-        }
-      }
-#pragma unroll
-      for (int g = 0; g < G; ++g) {
-        if (s0 + g < nsrc) {
-#pragma unroll
-          for (int u = 0; u < U; ++u) {
-            const E* e = reinterpret_cast<const E*>(&x[g][u]);
-#pragma unroll
-            for (int q = 0; q < NE; ++q)
-              acc[u][q] = (s0 + g == 0) ? R::to(e[q]) : R::add(acc[u][q], R::to(e[q]));
-          }
-        }
+template <int DT>
+__device__ void warp_reduce_vec(const char* const* src, int nsrc, char* const* dst, int ndst,
+                                long long off, long long nvec, int lane) {
+  for (long long i = lane; i < nvec; i += 32) {
+    Acc16<DT> acc;
+    acc.init(__ldcg(reinterpret_cast<const uint4*>(src[0] + off) + i));
+    for (int s = 1; s < nsrc; ++s) acc.add(__ldcg(reinterpret_cast<const uint4*>(src[s] + off) + i));
+    const uint4 out = acc.pack();
+    for (int d = 0; d < ndst; ++d) reinterpret_cast<uint4*>(dst[d] + off)[i] = out;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Per-worker bulk (TMA) movers.  `seq` counts stage fills issued by this
+// worker (uniform across its lanes) and selects stage / mbarrier parity.
+// ---------------------------------------------------------------------------
+struct Ring {
+  char* buf;      // FC_NST * FC_STAGE bytes
+  uint64_t* bar;  // FC_NST mbarriers
+  unsigned seq;
+};
+
+// Copy `nbytes` (16-aligned src/dst, multiple of 16) from src to every dst.
+// Lane 0 issues; bulk store groups stay pending (caller waits before flags).
+__device__ void bulk_copy(Ring& rg, const char* src, char* const* dst, int ndst,
+                          long long nbytes, int lane) {
+  const long long npieces = (nbytes + FC_STAGE - 1) / FC_STAGE;
+  if (lane == 0) {
+    const unsigned base = rg.seq;
+    for (long long i = 0; i < npieces && i < FC_NST - 1; ++i) {
+      const unsigned q = base + (unsigned)i;
+      const long long off = i * FC_STAGE;
+      const unsigned len = (unsigned)((nbytes - off) < FC_STAGE ? (nbytes - off) : FC_STAGE);
+      mbar_expect_tx(&rg.bar[q % FC_NST], len);
+      bulk_load(rg.buf + (q % FC_NST) * FC_STAGE, src + off, len, &rg.bar[q % FC_NST]);
+    }
+    for (long long i = 0; i < npieces; ++i) {
+      const unsigned q = base + (unsigned)i;
+      mbar_wait(&rg.bar[q % FC_NST], (q / FC_NST) & 1u);
+      const char* sb = rg.buf + (q % FC_NST) * FC_STAGE;
+      const long long off = i * FC_STAGE;
+      const unsigned len = (unsigned)((nbytes - off) < FC_STAGE ? (nbytes - off) : FC_STAGE);
+      for (int d = 0; d < ndst; ++d) bulk_store(dst[d] + off, sb, len);
+      bulk_commit();
+      const long long nx = i + FC_NST - 1;
+      if (nx < npieces) {
+        bulk_wait_read1();  // the stage of piece i-1 (== nx's stage) has been read out
+        const unsigned q2 = base + (unsigned)nx;
+        const long long off2 = nx * FC_STAGE;
+        const unsigned len2 = (unsigned)((nbytes - off2) < FC_STAGE ? (nbytes - off2) : FC_STAGE);
+        mbar_expect_tx(&rg.bar[q2 % FC_NST], len2);
+        bulk_load(rg.buf + (q2 % FC_NST) * FC_STAGE, src + off2, len2, &rg.bar[q2 % FC_NST]);
       }
     }
-    uint4 out[U];
+  }
+  rg.seq += (unsigned)npieces;
+}
+
+// Copy with bulk (TMA) loads into the ring and 16-byte lane stores to every
+// destination: smem is released as soon as the lanes have read a stage, so
+// outstanding NVLink writes hold no shared memory.
+__device__ void bulk_copy_stg(Ring& rg, const char* src, char* const* dst, int ndst,
+                              long long nbytes, int lane) {
+  const long long npieces = (nbytes + FC_STAGE - 1) / FC_STAGE;
+  const unsigned base = rg.seq;
+  if (lane == 0) {
+    for (long long i = 0; i < npieces && i < FC_NST - 1; ++i) {
+      const unsigned q = base + (unsigned)i;
+      const long long off = i * FC_STAGE;
+      const unsigned len = (unsigned)((nbytes - off) < FC_STAGE ? (nbytes - off) : FC_STAGE);
+      mbar_expect_tx(&rg.bar[q % FC_NST], len);
+      bulk_load(rg.buf + (q % FC_NST) * FC_STAGE, src + off, len, &rg.bar[q % FC_NST]);
+    }
+  }
+  for (long long i = 0; i < npieces; ++i) {
+    const unsigned q = base + (unsigned)i;
+    mbar_wait(&rg.bar[q % FC_NST], (q / FC_NST) & 1u);
+    const uint4* sb = reinterpret_cast<const uint4*>(rg.buf + (q % FC_NST) * FC_STAGE);
+    const long long off = i * FC_STAGE;
+    const int nv = (int)(((nbytes - off) < FC_STAGE ? (nbytes - off) : FC_STAGE) / 16);
+    constexpr int PER = FC_STAGE / 16 / 32;  // vectors per lane per full stage
+    uint4 v[PER];
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      E* e = reinterpret_cast<E*>(&out[u]);
-#pragma unroll
-      for (int q = 0; q < NE; ++q) e[q] = R::from(acc[u][q]);
+    for (int u = 0; u < PER; ++u)
+      if (lane + 32 * u < nv) v[u] = sb[lane + 32 * u];
+    __syncwarp();
+    if (lane == 0 && i + FC_NST - 1 < npieces) {
+      const long long p = i + FC_NST - 1;
+      const unsigned q2 = base + (unsigned)p;
+      const long long off2 = p * FC_STAGE;
+      const unsigned len2 = (unsigned)((nbytes - off2) < FC_STAGE ? (nbytes - off2) : FC_STAGE);
+      fence_proxy_async_smem();
+      mbar_expect_tx(&rg.bar[q2 % FC_NST], len2);
+      bulk_load(rg.buf + (q2 % FC_NST) * FC_STAGE, src + off2, len2, &rg.bar[q2 % FC_NST]);
     }
     for (int d = 0; d < ndst; ++d) {
       uint4* dp = reinterpret_cast<uint4*>(dst[d] + off);
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const long long j = i + (long long)u * FC_WT;
-        if (j < nvec) dp[j] = out[u];
-      }
+      for (int u = 0; u < PER; ++u)
+        if (lane + 32 * u < nv) dp[lane + 32 * u] = v[u];
     }
   }
+  rg.seq += (unsigned)npieces;
 }
 
-// Move/reduce nbytes: dst[d][0..n) = reduce(src[0..nsrc))[0..n).  nsrc == 1
-// is a pure byte copy (bit-exact for any dtype, NaN payloads included).
+// Reduce `nbytes` (all pointers 16-aligned, multiple of 16): sources are
+// bulk-loaded into the ring, 32 lanes sum them and store 16-byte vectors.
 template <int DT>
-__device__ void xfer(const char* const* src, int nsrc, char* const* dst, int ndst,
-                     long long nbytes, int esize, int wt) {
-  if (nbytes <= 0 || ndst <= 0) return;
-  const uintptr_t a0 = (uintptr_t)src[0];
-  uintptr_t diff = 0;
-  for (int s = 1; s < nsrc; ++s) diff |= (uintptr_t)src[s] - a0;
-  for (int d = 0; d < ndst; ++d) diff |= (uintptr_t)dst[d] - a0;
-  if (nsrc == 1) {
-    int g = 16;
-    while (g > 1 && (diff & (uintptr_t)(g - 1))) g >>= 1;
-    long long head = (long long)((g - (a0 & (uintptr_t)(g - 1))) & (uintptr_t)(g - 1));
-    if (head > nbytes) head = nbytes;
-    for (long long i = wt; i < head; i += FC_WT) {
-      const char v = src[0][i];
-      for (int d = 0; d < ndst; ++d) dst[d][i] = v;
+__device__ void bulk_reduce(Ring& rg, const char* const* src, int nsrc, char* const* dst,
+                            int ndst, long long nbytes, int lane) {
+  const long long seg = (long long)(FC_STAGE / nsrc) & ~15LL;  // bytes per source per piece
+  const long long npieces = (nbytes + seg - 1) / seg;
+  const unsigned base = rg.seq;
+  if (lane == 0) {
+    for (long long i = 0; i < npieces && i < FC_NST - 1; ++i) {
+      const unsigned q = base + (unsigned)i;
+      const long long off = i * seg;
+      const unsigned len = (unsigned)((nbytes - off) < seg ? (nbytes - off) : seg);
+      char* sb = rg.buf + (q % FC_NST) * FC_STAGE;
+      mbar_expect_tx(&rg.bar[q % FC_NST], len * nsrc);
+      for (int s = 0; s < nsrc; ++s) bulk_load(sb + s * seg, src[s] + off, len, &rg.bar[q % FC_NST]);
     }
-    const long long nu = (nbytes - head) / g;
-    switch (g) {
-      case 16: copy_units<uint4, 4>(src[0], dst, ndst, head, nu, wt); break;
-      case 8: copy_units<uint2, 4>(src[0], dst, ndst, head, nu, wt); break;
-      case 4: copy_units<unsigned, 4>(src[0], dst, ndst, head, nu, wt); break;
-      case 2: copy_units<unsigned short, 4>(src[0], dst, ndst, head, nu, wt); break;
-      default: copy_units<unsigned char, 4>(src[0], dst, ndst, head, nu, wt); break;
-    }
-    for (long long i = head + nu * g + wt; i < nbytes; i += FC_WT) {
-      const char v = src[0][i];
-      for (int d = 0; d < ndst; ++d) dst[d][i] = v;
-    }
-    return;
   }
-  if ((diff & 15) == 0) {
-    long long head = (long long)((16 - (a0 & 15)) & 15);
-    if (head > nbytes) head = nbytes;
-    reduce_scalar<DT>(src, nsrc, dst, ndst, 0, head / esize, wt);
-    const long long nv = (nbytes - head) / 16;
-    reduce_vec<DT, 2>(src, nsrc, dst, ndst, head, nv, wt);
-    const long long t0 = head + nv * 16;
-    reduce_scalar<DT>(src, nsrc, dst, ndst, t0, (nbytes - t0) / esize, wt);
-  } else {
-    reduce_scalar<DT>(src, nsrc, dst, ndst, 0, nbytes / esize, wt);
+  for (long long i = 0; i < npieces; ++i) {
+    const unsigned q = base + (unsigned)i;
+    mbar_wait(&rg.bar[q % FC_NST], (q / FC_NST) & 1u);
+    const char* sb = rg.buf + (q % FC_NST) * FC_STAGE;
+    const long long off = i * seg;
+    const long long len = (nbytes - off) < seg ? (nbytes - off) : seg;
+    for (long long j = lane; j < len / 16; j += 32) {
+      Acc16<DT> acc;
+      acc.init(reinterpret_cast<const uint4*>(sb)[j]);
+      for (int s = 1; s < nsrc; ++s) acc.add(reinterpret_cast<const uint4*>(sb + s * seg)[j]);
+      const uint4 out = acc.pack();
+      for (int d = 0; d < ndst; ++d) reinterpret_cast<uint4*>(dst[d] + off)[j] = out;
+    }
+    __syncwarp();
+    // refill the stage consumed in iteration i-1 (all lanes passed its __syncwarp)
+    if (lane == 0 && i + FC_NST - 1 < npieces) {
+      const long long p = i + FC_NST - 1;
+      const unsigned q2 = base + (unsigned)p;
+      const long long off2 = p * seg;
+      const unsigned len2 = (unsigned)((nbytes - off2) < seg ? (nbytes - off2) : seg);
+      char* sb2 = rg.buf + (q2 % FC_NST) * FC_STAGE;
+      fence_proxy_async_smem();  // generic reads of the reused stage before async writes
+      mbar_expect_tx(&rg.bar[q2 % FC_NST], len2 * nsrc);
+      for (int s = 0; s < nsrc; ++s)
+        bulk_load(sb2 + s * seg, src[s] + off2, len2, &rg.bar[q2 % FC_NST]);
+    }
   }
+  rg.seq += (unsigned)npieces;
 }
 
 struct Geo {
@@ -282,8 +451,67 @@ __device__ __forceinline__ long long chunk_bound(const Geo& g, int c, int n) {
 }
 
 template <int DT>
+__device__ void move(Ring& rg, const char* const* src, int ns, char* const* dst, int nd,
+                     long long nbytes, int esize, int lane, int copy_mode, bool& used_bulk) {
+  if (nbytes <= 0 || nd <= 0) return;
+  const uintptr_t a0 = (uintptr_t)src[0];
+  uintptr_t diff = 0;
+  for (int s = 1; s < ns; ++s) diff |= (uintptr_t)src[s] - a0;
+  for (int d = 0; d < nd; ++d) diff |= (uintptr_t)dst[d] - a0;
+  if (ns == 1) {
+    if ((diff & 15) == 0 && nbytes >= 1024) {
+      const long long head = (long long)((16 - (a0 & 15)) & 15);
+      const long long body = (nbytes - head) & ~15LL;
+      warp_copy(src[0], dst, nd, 0, head, lane);
+      char* d1[FC_MAXS];
+      for (int d = 0; d < nd; ++d) d1[d] = dst[d] + head;
+      if (copy_mode == 0) {
+        bulk_copy(rg, src[0] + head, d1, nd, body, lane);
+        used_bulk = true;
+      } else {
+        bulk_copy_stg(rg, src[0] + head, d1, nd, body, lane);
+      }
+      warp_copy(src[0], dst, nd, head + body, nbytes - head - body, lane);
+    } else {
+      warp_copy(src[0], dst, nd, 0, nbytes, lane);
+    }
+    return;
+  }
+  if ((diff & 15) == 0) {
+    long long head = (long long)((16 - (a0 & 15)) & 15);
+    if (head > nbytes) head = nbytes;
+    warp_reduce_scalar<DT>(src, ns, dst, nd, 0, head / esize, lane);
+    const long long body = (nbytes - head) & ~15LL;
+    if (body > 0) {
+      const char* s1[FC_MAXS];
+      char* d1[FC_MAXS];
+      for (int s = 0; s < ns; ++s) s1[s] = src[s] + head;
+      for (int d = 0; d < nd; ++d) d1[d] = dst[d] + head;
+      if (ns <= 8 && body >= 1024)
+        bulk_reduce<DT>(rg, s1, ns, d1, nd, body, lane);
+      else
+        warp_reduce_vec<DT>(s1, ns, d1, nd, 0, body / 16, lane);
+    }
+    const long long t0 = head + body;
+    warp_reduce_scalar<DT>(src, ns, dst, nd, t0, (nbytes - t0) / esize, lane);
+  } else {
+    warp_reduce_scalar<DT>(src, ns, dst, nd, 0, nbytes / esize, lane);
+  }
+}
+
+// Shared per-CTA item state (one item in flight per CTA).
+struct ItemShared {
+  int item;
+  int ok;
+};
+
+// One item (task, chunk) executed by the whole CTA: thread 0 waits for the
+// inputs, every warp moves a 128-byte-aligned 1/FC_WPC sub-range through its
+// own bulk ring, and thread 0 publishes after a CTA barrier.
+template <int DT>
 __device__ void run_item(const FcParams& P, int me, FcCtl* ctl, const int* T, int c,
-                         unsigned e, int w, int wt, unsigned& ready_mask, int* s_ok) {
+                         unsigned e, int w, int lane, unsigned& ready_mask, Ring& rg,
+                         ItemShared* sh, unsigned long long& t_ready) {
   const int kind = __ldg(T + TW_KIND);
   const int t = __ldg(T + TW_TREE);
   const int root = __ldg(T + TW_ROOT);
@@ -305,11 +533,17 @@ __device__ void run_item(const FcParams& P, int me, FcCtl* ctl, const int* T, in
 
   // 1. wait for inputs (parent / children flags) and for destination ranks
   //    to have entered this launch (entry barrier, guards buffer reuse).
-  if (wt == 0) {
+  if (threadIdx.x == 0) {
     bool ok = true;
-    if (kind == FC_K_AG_FWD || kind == FC_K_WAIT_AG)
+    if (kind == FC_K_AG_FWD)
       ok = spin_geq(myflags + P.ag_flag_off + t * P.maxc + fi, e, ctl, P.timeout_ns,
                     FC_DEVERR_TIMEOUT_AG);
+    if (kind == FC_K_WAIT_AG) {
+      // leaf: every chunk of this launch window has arrived; re-arm the counter
+      unsigned* cnt = myflags + P.cnt_off + t;
+      ok = spin_geq(cnt, (unsigned)(P.c1 - P.c0), ctl, P.timeout_ns, FC_DEVERR_TIMEOUT_AG);
+      if (ok) atomicSub(cnt, (unsigned)(P.c1 - P.c0));
+    }
     if (kind == FC_K_RS_FWD || kind == FC_K_RS_ROOT || kind == FC_K_AR_ROOT) {
       for (int j = 0; j < n_rs && ok; ++j)
         ok = spin_geq(myflags + P.rs_flag_off + __ldg(T + TW_RS_CSLOT + j) * P.maxc + fi, e,
@@ -325,23 +559,28 @@ __device__ void run_item(const FcParams& P, int me, FcCtl* ctl, const int* T, in
         }
       }
     }
-    s_ok[w] = ok ? 1 : 0;
+    sh->ok = ok ? 1 : 0;
+    if (P.trace) t_ready = globaltimer();
   }
-  if (kind == FC_K_WAIT_AG) return;
-  worker_bar(w);
-  if (!s_ok[w]) return;
+  if (kind == FC_K_WAIT_AG) return;  // uniform: thread 0 alone waited
+  __syncthreads();
+  if (!sh->ok) return;
 
-  // 2. move / reduce the chunk
+  // 2. move / reduce this warp's share of the chunk
+  long long s0 = b0 + (((b1 - b0) * w / FC_WPC) & ~(long long)(FC_ALIGN - 1));
+  long long s1 = (w == FC_WPC - 1) ? b1 : b0 + (((b1 - b0) * (w + 1) / FC_WPC) & ~(long long)(FC_ALIGN - 1));
+  if (s1 < s0) s1 = s0;
   const char* src[FC_MAXS];
   char* dst[FC_MAXS];
   int ns = 0, nd = 0;
-  const long long slot_phase = b0 - wbase;
+  const long long slot_phase = s0 - wbase;
   if (kind == FC_K_AG_ROOT || kind == FC_K_AG_FWD) {
-    src[ns++] = (kind == FC_K_AG_ROOT) ? P.send[me] + (b0 - g.base) : P.recv[me] + b0;
-    if (kind == FC_K_AG_ROOT && P.recv[me] + b0 != src[0]) dst[nd++] = P.recv[me] + b0;
-    for (int j = 0; j < n_ag; ++j) dst[nd++] = P.recv[__ldg(T + TW_AG_CHILD + j)] + b0;
+    src[ns++] = (kind == FC_K_AG_ROOT) ? P.send[me] + (s0 - g.base) : P.recv[me] + s0;
+    if (kind == FC_K_AG_ROOT && !P.root_local_done && P.recv[me] + s0 != src[0])
+      dst[nd++] = P.recv[me] + s0;
+    for (int j = 0; j < n_ag; ++j) dst[nd++] = P.recv[__ldg(T + TW_AG_CHILD + j)] + s0;
   } else {
-    src[ns++] = P.send[me] + b0;
+    src[ns++] = P.send[me] + s0;
     for (int j = 0; j < n_rs; ++j)
       src[ns++] = P.scratch[me] + P.unit_bytes * __ldg(T + TW_RS_CPREFIX + j) +
                   2LL * FC_ALIGN * __ldg(T + TW_RS_CSLOT + j) + slot_phase;
@@ -349,74 +588,112 @@ __device__ void run_item(const FcParams& P, int me, FcCtl* ctl, const int* T, in
       dst[nd++] = P.scratch[rs_parent] + P.unit_bytes * __ldg(T + TW_RS_PPREFIX) +
                   2LL * FC_ALIGN * __ldg(T + TW_RS_PSLOT) + slot_phase;
     } else if (kind == FC_K_RS_ROOT) {
-      dst[nd++] = P.recv[me] + (b0 - g.base);
+      dst[nd++] = P.recv[me] + (s0 - g.base);
     } else {  // FC_K_AR_ROOT
-      dst[nd++] = P.recv[me] + b0;
-      for (int j = 0; j < n_ag; ++j) dst[nd++] = P.recv[__ldg(T + TW_AG_CHILD + j)] + b0;
+      dst[nd++] = P.recv[me] + s0;
+      for (int j = 0; j < n_ag; ++j) dst[nd++] = P.recv[__ldg(T + TW_AG_CHILD + j)] + s0;
     }
   }
-  xfer<DT>(src, ns, dst, nd, b1 - b0, P.esize, wt);
+  bool used_bulk = false;
+  move<DT>(rg, src, ns, dst, nd, s1 - s0, P.esize, lane, P.copy_mode, used_bulk);
+  if (used_bulk && lane == 0) {
+    bulk_wait_all();
+    fence_proxy_async_global();
+  }
 
-  // 3. publish: make the stores visible system-wide, then release the flags
-  if (kind == FC_K_RS_ROOT) return;
-  fence_sys();
-  worker_bar(w);
-  if (wt == 0) {
-    if (kind == FC_K_RS_FWD) {
-      st_release_sys(P.flags[rs_parent] + P.rs_flag_off + __ldg(T + TW_RS_PSLOT) * P.maxc + fi, e);
-    } else {
-      for (int j = 0; j < n_ag; ++j)
-        st_release_sys(P.flags[__ldg(T + TW_AG_CHILD + j)] + P.ag_flag_off + t * P.maxc + fi, e);
+  // 3. publish: the CTA barrier orders every thread's stores (and the bulk
+  //    completions above) before thread 0's cumulative .sys release.
+  __syncthreads();
+  if (kind == FC_K_RS_ROOT || threadIdx.x != 0) return;
+  if (kind == FC_K_RS_FWD) {
+    st_release_sys(P.flags[rs_parent] + P.rs_flag_off + __ldg(T + TW_RS_PSLOT) * P.maxc + fi, e);
+  } else {
+    const int leaves = __ldg(T + TW_AG_LEAFMASK);
+    for (int j = 0; j < n_ag; ++j) {
+      unsigned* f = P.flags[__ldg(T + TW_AG_CHILD + j)];
+      if ((leaves >> j) & 1)
+        red_release_sys_add(f + P.cnt_off + t, 1u);
+      else
+        st_release_sys(f + P.ag_flag_off + t * P.maxc + fi, e);
     }
   }
 }
 
 template <int DT>
-__global__ void __launch_bounds__(FC_BLOCK) fc_forest_kernel(const __grid_constant__ FcParams P) {
-  __shared__ int s_item[FC_NW][2];
-  __shared__ int s_ok[FC_NW];
+__global__ void __launch_bounds__(FC_BLOCK, 1) fc_forest_kernel(const __grid_constant__ FcParams P) {
+  extern __shared__ __align__(128) char smem[];
+  __shared__ __align__(8) uint64_t bars[FC_WPC * FC_NST];
   __shared__ unsigned s_epoch;
+  __shared__ ItemShared sh;
   const int lr = blockIdx.x / P.ctas_per_rank;
   const int me = P.local_rank[lr];
   FcCtl* const ctl = P.ctl[lr];
+  const int w = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
   if (threadIdx.x == 0) s_epoch = ld_volatile(&ctl->epoch) + 1;
+  if (threadIdx.x < FC_WPC * FC_NST) mbar_init(&bars[threadIdx.x], 1);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   __syncthreads();
   const unsigned e = s_epoch;
   // entry barrier: tell every peer that this rank entered launch e
   if ((int)threadIdx.x < P.nranks && (int)threadIdx.x != me)
     st_release_sys(P.flags[threadIdx.x] + me, e);
 
-  const int w = threadIdx.x / FC_WT;
-  const int wt = threadIdx.x % FC_WT;
+  Ring rg;
+  rg.buf = smem + (size_t)w * FC_NST * FC_STAGE;
+  rg.bar = &bars[w * FC_NST];
+  rg.seq = 0;
   const int* const tasks = P.tasks[lr];
   const int nact = P.nactive[lr];
   const int nwait = P.nwait[lr];
   const long long W = P.c1 - P.c0;
-  const long long nA = (long long)nact * W;
-  const long long total = nA + (long long)nwait * W;
+  const long long span = W + (long long)P.lag * P.lag_max[lr];
+  const long long nA = (long long)nact * span;
+  const long long total = nA + nwait;  // one completion wait per leaf task
   unsigned ready_mask = 1u << me;
-  for (int it = 0;; ++it) {
-    if (wt == 0) {
+  FcTraceRec* const trace = P.trace;
+  for (;;) {
+    if (threadIdx.x == 0) {
       int v = (int)atomicAdd(&ctl->claim, 1u);
       if (ld_volatile(&ctl->error) != 0) v = INT_MAX;
-      s_item[w][it & 1] = v;
+      sh.item = v;
     }
-    worker_bar(w);
-    const long long item = s_item[w][it & 1];
+    __syncthreads();
+    const long long item = sh.item;
+    __syncthreads();  // sh.item is rewritten by the next claim
     if (item >= total) break;
     int c, ti;
     if (item < nA) {
-      c = (int)(item / nact);
-      ti = (int)(item - (long long)c * nact);
+      const long long d = item / nact;
+      ti = (int)(item - d * nact);
+      const long long cc =
+          d - (long long)P.lag * __ldg(tasks + (long long)ti * FC_TASK_WORDS + TW_LAG);
+      if (cc < 0 || cc >= W) continue;  // outside this task's diagonal window
+      c = (int)cc;
     } else {
-      const long long j = item - nA;
-      c = (int)(j / nwait);
-      ti = nact + (int)(j - (long long)c * nwait);
+      c = (int)(W - 1);
+      ti = nact + (int)(item - nA);
     }
-    run_item<DT>(P, me, ctl, tasks + (long long)ti * FC_TASK_WORDS, P.c0 + c, e, w, wt,
-                 ready_mask, s_ok);
+    const unsigned long long t0 = trace ? globaltimer() : 0;
+    unsigned long long t_ready = t0;
+    run_item<DT>(P, me, ctl, tasks + (long long)ti * FC_TASK_WORDS, P.c0 + c, e, w, lane,
+                 ready_mask, rg, &sh, t_ready);
+    if (trace && threadIdx.x == 0) {
+      const unsigned idx = atomicAdd(P.trace_count, 1u);
+      if (idx < P.trace_cap) {
+        FcTraceRec r;
+        r.t_start = t0;
+        r.t_end = globaltimer();
+        r.t_wait = (unsigned)(t_ready - t0);
+        r.chunk = P.c0 + c;
+        r.rank = (short)me;
+        r.task = (short)ti;
+        r.worker = (short)(blockIdx.x % P.ctas_per_rank);
+        r.launch = (unsigned short)e;
+        trace[idx] = r;
+      }
+    }
   }
-  __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
     const unsigned prev = atomicAdd(&ctl->done, 1u);
@@ -438,6 +715,21 @@ const void* kernel_for(int rd) {
   }
 }
 
+int ensure_smem_attr(const void* fn) {
+  static const void* done[8] = {};
+  for (auto& d : done) {
+    if (d == fn) return 0;
+    if (!d) {
+      const cudaError_t e =
+          cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, FC_SMEM);
+      if (e != cudaSuccess) return (int)e;
+      d = fn;
+      return 0;
+    }
+  }
+  return 0;
+}
+
 }  // namespace
 
 int fc_launch(const FcParams& p, int reduce_dtype, int cooperative, void* stream, int* grid_out) {
@@ -445,15 +737,21 @@ int fc_launch(const FcParams& p, int reduce_dtype, int cooperative, void* stream
   void* args[] = {(void*)&p};
   const void* fn = kernel_for(reduce_dtype);
   if (grid_out) *grid_out = (int)grid.x;
+  const int a = ensure_smem_attr(fn);
+  if (a) return a;
   cudaError_t err;
   if (cooperative)
-    err = cudaLaunchCooperativeKernel(fn, grid, block, args, 0, (cudaStream_t)stream);
+    err = cudaLaunchCooperativeKernel(fn, grid, block, args, FC_SMEM, (cudaStream_t)stream);
   else
-    err = cudaLaunchKernel(fn, grid, block, args, 0, (cudaStream_t)stream);
+    err = cudaLaunchKernel(fn, grid, block, args, FC_SMEM, (cudaStream_t)stream);
   return (int)err;
 }
 
 int fc_max_ctas_per_sm(int reduce_dtype, int* out) {
-  return (int)cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, kernel_for(reduce_dtype),
-                                                           FC_BLOCK, 0);
+  const void* fn = kernel_for(reduce_dtype);
+  const int a = ensure_smem_attr(fn);
+  if (a) return a;
+  return (int)cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, fn, FC_BLOCK, FC_SMEM);
 }
+
+int fc_workers_per_cta() { return FC_WPC; }

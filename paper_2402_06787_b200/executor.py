@@ -154,6 +154,35 @@ class _CommBase:
         return {"launches": buf[0], "nchunks": buf[1], "window": buf[2], "grid": buf[3],
                 "unit_bytes": buf[4]}
 
+    # -- tracing ------------------------------------------------------------
+    TRACE_DTYPE = np.dtype([("t_start", "<u8"), ("t_end", "<u8"), ("t_wait", "<u4"),
+                            ("chunk", "<i4"), ("rank", "<i2"), ("task", "<i2"),
+                            ("worker", "<i2"), ("launch", "<u2")])
+
+    def enable_trace(self, capacity: int = 1 << 20) -> None:
+        """Record one (start, end, rank, task, chunk, worker, launch) row per
+        executed item into device memory (fc_comm_set_trace)."""
+        dev = f"cuda:{self.device}"
+        self._trace_buf = torch.zeros(capacity * self.TRACE_DTYPE.itemsize, dtype=torch.uint8,
+                                      device=dev)
+        self._trace_cnt = torch.zeros(1, dtype=torch.int32, device=dev)
+        _lib.check(self._lib.fc_comm_set_trace(self._comm, self._trace_buf.data_ptr(),
+                                               self._trace_cnt.data_ptr(), capacity),
+                   self._comm, "set_trace")
+        self._trace_cap = capacity
+
+    def disable_trace(self) -> None:
+        self._lib.fc_comm_set_trace(self._comm, None, None, 0)
+
+    def reset_trace(self) -> None:
+        self._trace_cnt.zero_()
+
+    def read_trace(self) -> np.ndarray:
+        torch.cuda.synchronize(self.device)
+        n = min(int(self._trace_cnt.item()), self._trace_cap)
+        raw = self._trace_buf[: n * self.TRACE_DTYPE.itemsize].cpu().numpy()
+        return raw.view(self.TRACE_DTYPE)
+
     def close(self) -> None:
         if self._comm is not None:
             self._lib.fc_comm_destroy(self._comm)

@@ -24,6 +24,9 @@ def main():
     ap.add_argument("--ctas", default="16,32,64,128")
     ap.add_argument("--chunks", default="262144,524288,1048576,2097152")
     ap.add_argument("--ipw", default="4")
+    ap.add_argument("--lag", default="2")
+    ap.add_argument("--mode", default="1")
+    ap.add_argument("--dma", default="1")
     args = ap.parse_args()
     local = int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
@@ -49,15 +52,19 @@ def main():
                 buf.normal_()
                 fn = lambda: comm.all_reduce(buf)  # noqa: E731
             tstar = comm.t_star(coll, M)
-            for ctas, ch, ipw in itertools.product(args.ctas.split(","), args.chunks.split(","),
-                                                   args.ipw.split(",")):
+            for ctas, ch, ipw, lag, mode, dma in itertools.product(
+                    args.ctas.split(","), args.chunks.split(","), args.ipw.split(","),
+                    args.lag.split(","), args.mode.split(","), args.dma.split(",")):
+                comm.set_option("dma_root_copy", int(dma))
+                comm.set_option("lag", int(lag))
+                comm.set_option("copy_mode", int(mode))
                 comm.set_option("ctas_per_rank", int(ctas))
                 comm.set_option("chunk_max", int(ch))
                 comm.set_option("items_per_worker", int(ipw))
                 ms = timed(fn, 10, 3, dist)
                 info = comm.last_call_info()
                 if rank == 0:
-                    print(f"{coll:15s} {mib:6d}MiB ctas={ctas:>4s} chunk={int(ch)//1024:5d}K ipw={ipw} "
+                    print(f"{coll:15s} {mib:6d}MiB ctas={ctas:>4s} chunk={int(ch)//1024:5d}K ipw={ipw} lag={lag:>3s} m={mode} dma={dma} "
                           f"n={info['nchunks']:5d} L={info['launches']} ms={ms:8.4f} "
                           f"algbw={gbs(M, ms):8.1f} frac_T*={tstar*1e3/ms:6.3f}", flush=True)
     comm.check()
