@@ -120,17 +120,28 @@ class Clocks:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
         sm.sort()
         return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "window": "1 s warm-up soak + timed region"}
 
 
 # ---------------------------------------------------------------------------
 # timing helpers
 # ---------------------------------------------------------------------------
-def timed(fn, steps, warmup, dist=None):
+def timed(fn, steps, warmup, dist=None, soak_s=0.0):
+    """Mean ms per step over `steps` calls (CUDA events on the current stream,
+    barrier + synchronize on both sides, max over ranks).  `soak_s` adds an
+    untimed warm-up soak of about that many seconds so clock sampling covers
+    the kernel under steady load."""
     import torch
 
     for _ in range(warmup):
         fn()
+    if soak_s > 0:
+        torch.cuda.synchronize()
+        t_end = time.perf_counter() + soak_s
+        while time.perf_counter() < t_end:
+            for _ in range(8):
+                fn()
+            torch.cuda.synchronize()
     if dist is not None:
         dist.barrier()
     torch.cuda.synchronize()
@@ -208,7 +219,8 @@ def run_single(args):
     plan = comm.plan("allgather")
     fn = lambda: comm.all_gather(outs, sends)  # noqa: E731
     with Clocks(0) as clk:
-        ms = timed(fn, args.steps, args.warmup)
+        time.sleep(0.3)
+        ms = timed(fn, args.steps, args.warmup, soak_s=1.0)
     comm.check()
     info = comm.last_call_info()
     tstar = comm.t_star("allgather", M)
@@ -313,7 +325,8 @@ def run_multi(args):
     out = comm.empty(n * S, dtype=torch.float32)
     fn = lambda: comm.all_gather(out, inp)  # noqa: E731
     with Clocks(local) as clk:
-        ms = timed(fn, args.steps, args.warmup, dist)
+        time.sleep(0.3)
+        ms = timed(fn, args.steps, args.warmup, dist, soak_s=1.0)
     comm.check()
     info = comm.last_call_info()
     tstar = comm.t_star("allgather", M)

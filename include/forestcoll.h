@@ -88,9 +88,10 @@ extern "C" {
 #define FC_OPT_CHUNK_MIN 3     /* min bytes per pipeline chunk (default 16 KiB) */
 #define FC_OPT_ITEMS_PER_WORKER 4 /* target work items per CTA (default 4) */
 #define FC_OPT_TIMEOUT_MS 5    /* device flag-wait timeout (default 10000 ms) */
-#define FC_OPT_LAG 6           /* claim-order skew, chunks per tree stage (default 16) */
+#define FC_OPT_LAG 6           /* claim-order skew, chunks per tree stage (default 64) */
 #define FC_OPT_COPY_MODE 7     /* 0: TMA bulk stores, 1: TMA loads + vector stores (default 0) */
 #define FC_OPT_DMA_ROOT_COPY 8 /* allgather: copy engine places the own shard (default 0) */
+#define FC_OPT_WORKER_WARPS 9  /* warps per work item: 1, 2, 4, 8 (default 4 real, 1 virtual) */
 
 typedef struct fc_comm fc_comm_t;
 
@@ -139,10 +140,10 @@ int fc_allreduce_multi(fc_comm_t* comm, const void* const* sends,
 /* statistics of the last collective call (launches, chunks, bytes) */
 int fc_last_call_info(const fc_comm_t* comm, long long* info, int ninfo);
 
-/* item tracing: 32-byte records {u64 t_start, u64 t_end (ns, %globaltimer),
- * u32 t_wait (ns waiting on flags), i32 chunk, i16 rank, i16 task,
- * i16 worker, u16 launch} appended at atomicAdd(*count) while
- * *count < capacity; pass records == NULL to disable. */
+/* item tracing: 40-byte records {u64 t_start, u64 t_end (ns, %globaltimer),
+ * u32 t_wait (ns waiting on flags), u32 t_move (ns moving data), i32 chunk,
+ * i16 rank, i16 task, i16 worker, u16 launch, u32 pad} appended at
+ * atomicAdd(*count) while *count < capacity; records == NULL disables. */
 int fc_comm_set_trace(fc_comm_t* comm, void* records, unsigned int* count,
                       unsigned int capacity);
 

@@ -18,7 +18,7 @@ LIB_PATH = os.path.join(LIB_DIR, "libforestcoll.so")
 FC_ALLGATHER, FC_REDUCE_SCATTER, FC_ALLREDUCE = 0, 1, 2
 FC_SUM = 0
 OPT_CTAS_PER_RANK, OPT_CHUNK_MAX, OPT_CHUNK_MIN, OPT_ITEMS_PER_WORKER, OPT_TIMEOUT_MS = 1, 2, 3, 4, 5
-OPT_LAG, OPT_COPY_MODE, OPT_DMA_ROOT_COPY = 6, 7, 8
+OPT_LAG, OPT_COPY_MODE, OPT_DMA_ROOT_COPY, OPT_WORKER_WARPS = 6, 7, 8, 9
 OPTIONS = {
     "ctas_per_rank": OPT_CTAS_PER_RANK,
     "chunk_max": OPT_CHUNK_MAX,
@@ -28,6 +28,7 @@ OPTIONS = {
     "lag": OPT_LAG,
     "copy_mode": OPT_COPY_MODE,
     "dma_root_copy": OPT_DMA_ROOT_COPY,
+    "worker_warps": OPT_WORKER_WARPS,
 }
 
 # symbol -> (restype, argtypes)

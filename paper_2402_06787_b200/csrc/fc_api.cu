@@ -68,9 +68,10 @@ struct fc_comm {
   int ctas_per_rank = 64;
   long long chunk_max = 256 << 10, chunk_min = 16 << 10, items_per_worker = 4;
   long long timeout_ms = 10000;
-  int lag = 16;
+  int lag = 64;
   int copy_mode = 1;
   int dma_root_copy = 0;
+  int worker_warps = 8;
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   FcTraceRec* trace = nullptr;
@@ -247,6 +248,7 @@ int run(fc_comm* c, int coll, const void* const* sends, void* const* recvs, size
   P.ctas_per_rank = c->ctas_per_rank;
   P.lag = c->lag;
   P.copy_mode = c->copy_mode;
+  P.worker_warps = c->worker_warps;
   P.trace = c->trace;
   P.trace_count = c->trace_count;
   P.trace_cap = c->trace_cap;
@@ -254,7 +256,7 @@ int run(fc_comm* c, int coll, const void* const* sends, void* const* recvs, size
   // chunk plan: identical on every rank (depends on S, dtype, plan, options)
   const long long slice_unit = (S + pl.k - 1) / pl.k * es;  // bytes per unit of multiplicity
   const long long max_slice = slice_unit * pl.max_mult;
-  const long long workers = (long long)c->ctas_per_rank;  // one item in flight per CTA
+  const long long workers = (long long)c->ctas_per_rank * (fc_warps_per_cta() / c->worker_warps);
   const long long avg_active = std::max(1LL, pl.active_total / N);
   long long n = (max_slice + c->chunk_max - 1) / c->chunk_max;
   n = std::max(n, (c->items_per_worker * workers + avg_active - 1) / avg_active);
@@ -343,6 +345,7 @@ int default_ctas(fc_comm* c) {
   const int cap = per_sm * sms / c->nlocal;
   if (cap < 1) return fail(c, FC_ERR_UNSUPPORTED, "device cannot co-schedule %d ranks", c->nlocal);
   c->ctas_per_rank = std::min(c->virt ? 16 : 96, cap);
+  c->worker_warps = c->virt ? 1 : 4;
   return make_side_stream(c);
 }
 
@@ -485,6 +488,11 @@ int fc_comm_set_option(fc_comm_t* c, int option, long long v) {
     case FC_OPT_DMA_ROOT_COPY:
       c->dma_root_copy = v ? 1 : 0;
       return FC_SUCCESS;
+    case FC_OPT_WORKER_WARPS:
+      if (v != 1 && v != 2 && v != 4 && v != 8)
+        return fail(c, FC_ERR_INVALID_ARG, "worker_warps must be 1, 2, 4 or 8");
+      c->worker_warps = (int)v;
+      return FC_SUCCESS;
     default:
       return fail(c, FC_ERR_INVALID_ARG, "unknown option %d", option);
   }
@@ -501,6 +509,7 @@ int fc_comm_get_option(fc_comm_t* c, int option, long long* v) {
     case FC_OPT_LAG: *v = c->lag; return FC_SUCCESS;
     case FC_OPT_COPY_MODE: *v = c->copy_mode; return FC_SUCCESS;
     case FC_OPT_DMA_ROOT_COPY: *v = c->dma_root_copy; return FC_SUCCESS;
+    case FC_OPT_WORKER_WARPS: *v = c->worker_warps; return FC_SUCCESS;
     default: return fail(c, FC_ERR_INVALID_ARG, "unknown option %d", option);
   }
 }

@@ -80,10 +80,12 @@ struct FcCtl {
 struct FcTraceRec {
   unsigned long long t_start, t_end;  // %globaltimer ns: claim .. published
   unsigned t_wait;                    // ns spent waiting on flags / readiness
+  unsigned t_move;                    // ns from ready to data moved (before publish)
   int chunk;
   short rank, task;
   short worker;
   unsigned short launch;  // epoch (low 16 bits)
+  unsigned pad;
 };
 
 struct FcParams {
@@ -119,6 +121,7 @@ struct FcParams {
   int lag;          // claim-order skew in chunks per stage
   int copy_mode;    // 0: TMA bulk stores, 1: bulk loads + 16-byte lane stores
   int root_local_done;  // allgather: own shard already placed in recv (DMA engine)
+  int worker_warps;     // warps per worker (1, 2, 4, 8): items in flight per CTA = 8 / this
   FcTraceRec* trace;
   unsigned* trace_count;
   unsigned trace_cap;
@@ -128,4 +131,4 @@ struct FcParams {
 int fc_launch(const FcParams& p, int reduce_dtype, int cooperative,
               void* stream, int* grid_out);
 int fc_max_ctas_per_sm(int reduce_dtype, int* out);
-int fc_workers_per_cta();
+int fc_warps_per_cta();

@@ -38,7 +38,8 @@
 
 #include "fc_internal.h"
 
-#define FC_WPC 8                           // workers (warps) per CTA
+#define FC_WPC 8                           // warps per CTA
+// WW (template): warps per worker; a worker holds one item in flight.
 #define FC_BLOCK (32 * FC_WPC)
 #define FC_NST 3                           // smem stages per worker
 #define FC_STAGE (8 * 1024)                // bytes per stage
@@ -68,6 +69,16 @@ __device__ __forceinline__ unsigned ld_volatile(const unsigned* p) {
   return *reinterpret_cast<const volatile unsigned*>(p);
 }
 __device__ __forceinline__ void fence_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
+// Barrier of one worker (WW warps): a warp barrier or a named CTA barrier
+// (id 0 is __syncthreads).
+template <int WW>
+__device__ __forceinline__ void worker_sync(int wk) {
+  if constexpr (WW == 1) {
+    __syncwarp();
+  } else {
+    asm volatile("bar.sync %0, %1;" ::"r"(wk + 1), "r"(WW * 32) : "memory");
+  }
+}
 __device__ __forceinline__ unsigned long long globaltimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -506,12 +517,13 @@ struct ItemShared {
 };
 
 // One item (task, chunk) executed by the whole CTA: thread 0 waits for the
-// inputs, every warp moves a 128-byte-aligned 1/FC_WPC sub-range through its
+// inputs, every warp moves a 128-byte-aligned 1/FC_WW sub-range through its
 // own bulk ring, and thread 0 publishes after a CTA barrier.
-template <int DT>
+template <int DT, int WW>
 __device__ void run_item(const FcParams& P, int me, FcCtl* ctl, const int* T, int c,
                          unsigned e, int w, int lane, unsigned& ready_mask, Ring& rg,
-                         ItemShared* sh, unsigned long long& t_ready) {
+                         ItemShared* sh, unsigned long long& t_ready,
+                         unsigned long long& t_moved) {
   const int kind = __ldg(T + TW_KIND);
   const int t = __ldg(T + TW_TREE);
   const int root = __ldg(T + TW_ROOT);
@@ -533,7 +545,10 @@ __device__ void run_item(const FcParams& P, int me, FcCtl* ctl, const int* T, in
 
   // 1. wait for inputs (parent / children flags) and for destination ranks
   //    to have entered this launch (entry barrier, guards buffer reuse).
-  if (threadIdx.x == 0) {
+  const int wl = w % WW;  // warp index within the worker
+  const int wk = w / WW;  // worker index within the CTA
+  const bool leader = (wl == 0 && lane == 0);
+  if (leader) {
     bool ok = true;
     if (kind == FC_K_AG_FWD)
       ok = spin_geq(myflags + P.ag_flag_off + t * P.maxc + fi, e, ctl, P.timeout_ns,
@@ -562,13 +577,13 @@ __device__ void run_item(const FcParams& P, int me, FcCtl* ctl, const int* T, in
     sh->ok = ok ? 1 : 0;
     if (P.trace) t_ready = globaltimer();
   }
-  if (kind == FC_K_WAIT_AG) return;  // uniform: thread 0 alone waited
-  __syncthreads();
+  if (kind == FC_K_WAIT_AG) return;  // uniform: the leader alone waited
+  worker_sync<WW>(wk);
   if (!sh->ok) return;
 
   // 2. move / reduce this warp's share of the chunk
-  long long s0 = b0 + (((b1 - b0) * w / FC_WPC) & ~(long long)(FC_ALIGN - 1));
-  long long s1 = (w == FC_WPC - 1) ? b1 : b0 + (((b1 - b0) * (w + 1) / FC_WPC) & ~(long long)(FC_ALIGN - 1));
+  long long s0 = b0 + (((b1 - b0) * wl / WW) & ~(long long)(FC_ALIGN - 1));
+  long long s1 = (wl == WW - 1) ? b1 : b0 + (((b1 - b0) * (wl + 1) / WW) & ~(long long)(FC_ALIGN - 1));
   if (s1 < s0) s1 = s0;
   const char* src[FC_MAXS];
   char* dst[FC_MAXS];
@@ -603,8 +618,9 @@ __device__ void run_item(const FcParams& P, int me, FcCtl* ctl, const int* T, in
 
   // 3. publish: the CTA barrier orders every thread's stores (and the bulk
   //    completions above) before thread 0's cumulative .sys release.
-  __syncthreads();
-  if (kind == FC_K_RS_ROOT || threadIdx.x != 0) return;
+  worker_sync<WW>(wk);
+  if (P.trace && leader) t_moved = globaltimer();
+  if (kind == FC_K_RS_ROOT || !leader) return;
   if (kind == FC_K_RS_FWD) {
     st_release_sys(P.flags[rs_parent] + P.rs_flag_off + __ldg(T + TW_RS_PSLOT) * P.maxc + fi, e);
   } else {
@@ -619,12 +635,13 @@ __device__ void run_item(const FcParams& P, int me, FcCtl* ctl, const int* T, in
   }
 }
 
-template <int DT>
+template <int DT, int WW>
 __global__ void __launch_bounds__(FC_BLOCK, 1) fc_forest_kernel(const __grid_constant__ FcParams P) {
+  constexpr int FC_NWK = FC_WPC / WW;
   extern __shared__ __align__(128) char smem[];
   __shared__ __align__(8) uint64_t bars[FC_WPC * FC_NST];
   __shared__ unsigned s_epoch;
-  __shared__ ItemShared sh;
+  __shared__ ItemShared sh_all[FC_NWK];
   const int lr = blockIdx.x / P.ctas_per_rank;
   const int me = P.local_rank[lr];
   FcCtl* const ctl = P.ctl[lr];
@@ -639,6 +656,9 @@ __global__ void __launch_bounds__(FC_BLOCK, 1) fc_forest_kernel(const __grid_con
   if ((int)threadIdx.x < P.nranks && (int)threadIdx.x != me)
     st_release_sys(P.flags[threadIdx.x] + me, e);
 
+  const int wk = w / WW;
+  const bool lead = (w % WW == 0) && lane == 0;
+  ItemShared& sh = sh_all[wk];
   Ring rg;
   rg.buf = smem + (size_t)w * FC_NST * FC_STAGE;
   rg.bar = &bars[w * FC_NST];
@@ -653,14 +673,14 @@ __global__ void __launch_bounds__(FC_BLOCK, 1) fc_forest_kernel(const __grid_con
   unsigned ready_mask = 1u << me;
   FcTraceRec* const trace = P.trace;
   for (;;) {
-    if (threadIdx.x == 0) {
+    if (lead) {
       int v = (int)atomicAdd(&ctl->claim, 1u);
       if (ld_volatile(&ctl->error) != 0) v = INT_MAX;
       sh.item = v;
     }
-    __syncthreads();
+    worker_sync<WW>(wk);
     const long long item = sh.item;
-    __syncthreads();  // sh.item is rewritten by the next claim
+    worker_sync<WW>(wk);  // sh.item is rewritten by the next claim
     if (item >= total) break;
     int c, ti;
     if (item < nA) {
@@ -675,25 +695,28 @@ __global__ void __launch_bounds__(FC_BLOCK, 1) fc_forest_kernel(const __grid_con
       ti = nact + (int)(item - nA);
     }
     const unsigned long long t0 = trace ? globaltimer() : 0;
-    unsigned long long t_ready = t0;
-    run_item<DT>(P, me, ctl, tasks + (long long)ti * FC_TASK_WORDS, P.c0 + c, e, w, lane,
-                 ready_mask, rg, &sh, t_ready);
-    if (trace && threadIdx.x == 0) {
+    unsigned long long t_ready = t0, t_moved = t0;
+    run_item<DT, WW>(P, me, ctl, tasks + (long long)ti * FC_TASK_WORDS, P.c0 + c, e, w, lane,
+                 ready_mask, rg, &sh, t_ready, t_moved);
+    if (trace && lead) {
       const unsigned idx = atomicAdd(P.trace_count, 1u);
       if (idx < P.trace_cap) {
         FcTraceRec r;
         r.t_start = t0;
         r.t_end = globaltimer();
         r.t_wait = (unsigned)(t_ready - t0);
+        r.t_move = t_moved > t_ready ? (unsigned)(t_moved - t_ready) : 0u;
+        r.pad = 0;
         r.chunk = P.c0 + c;
         r.rank = (short)me;
         r.task = (short)ti;
-        r.worker = (short)(blockIdx.x % P.ctas_per_rank);
+        r.worker = (short)((blockIdx.x % P.ctas_per_rank) * FC_NWK + wk);
         r.launch = (unsigned short)e;
         trace[idx] = r;
       }
     }
   }
+  __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
     const unsigned prev = atomicAdd(&ctl->done, 1u);
@@ -706,17 +729,27 @@ __global__ void __launch_bounds__(FC_BLOCK, 1) fc_forest_kernel(const __grid_con
   }
 }
 
-const void* kernel_for(int rd) {
+template <int WW>
+const void* kernel_for_ww(int rd) {
   switch (rd) {
-    case FC_BFLOAT16: return (const void*)fc_forest_kernel<FC_BFLOAT16>;
-    case FC_FLOAT16: return (const void*)fc_forest_kernel<FC_FLOAT16>;
-    case FC_INT32: return (const void*)fc_forest_kernel<FC_INT32>;
-    default: return (const void*)fc_forest_kernel<FC_FLOAT32>;
+    case FC_BFLOAT16: return (const void*)fc_forest_kernel<FC_BFLOAT16, WW>;
+    case FC_FLOAT16: return (const void*)fc_forest_kernel<FC_FLOAT16, WW>;
+    case FC_INT32: return (const void*)fc_forest_kernel<FC_INT32, WW>;
+    default: return (const void*)fc_forest_kernel<FC_FLOAT32, WW>;
+  }
+}
+
+const void* kernel_for(int rd, int ww) {
+  switch (ww) {
+    case 1: return kernel_for_ww<1>(rd);
+    case 2: return kernel_for_ww<2>(rd);
+    case 4: return kernel_for_ww<4>(rd);
+    default: return kernel_for_ww<8>(rd);
   }
 }
 
 int ensure_smem_attr(const void* fn) {
-  static const void* done[8] = {};
+  static const void* done[32] = {};
   for (auto& d : done) {
     if (d == fn) return 0;
     if (!d) {
@@ -735,7 +768,7 @@ int ensure_smem_attr(const void* fn) {
 int fc_launch(const FcParams& p, int reduce_dtype, int cooperative, void* stream, int* grid_out) {
   const dim3 grid(p.nlocal * p.ctas_per_rank), block(FC_BLOCK);
   void* args[] = {(void*)&p};
-  const void* fn = kernel_for(reduce_dtype);
+  const void* fn = kernel_for(reduce_dtype, p.worker_warps);
   if (grid_out) *grid_out = (int)grid.x;
   const int a = ensure_smem_attr(fn);
   if (a) return a;
@@ -748,10 +781,10 @@ int fc_launch(const FcParams& p, int reduce_dtype, int cooperative, void* stream
 }
 
 int fc_max_ctas_per_sm(int reduce_dtype, int* out) {
-  const void* fn = kernel_for(reduce_dtype);
+  const void* fn = kernel_for(reduce_dtype, 8);
   const int a = ensure_smem_attr(fn);
   if (a) return a;
   return (int)cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, fn, FC_BLOCK, FC_SMEM);
 }
 
-int fc_workers_per_cta() { return FC_WPC; }
+int fc_warps_per_cta() { return FC_WPC; }

@@ -34,7 +34,9 @@ def report(rec: np.ndarray, plan, launch=None) -> str:
             x = rr[rr["task"] == ti]
             kind = KIND_NAMES[tasks[int(ti)].kind]
             dur = (x["t_end"] - x["t_start"]) / 1e3
+            pub = dur - x["t_wait"] / 1e3 - x["t_move"] / 1e3
             lines.append(f"    task {ti:2d} {kind:8s} tree {tasks[int(ti)].tree:2d} n={x.size:4d} "
-                         f"mean {dur.mean():7.2f} us (wait {x['t_wait'].mean() / 1e3:7.2f}) "
+                         f"mean {dur.mean():7.2f} us (wait {x['t_wait'].mean() / 1e3:6.2f} "
+                         f"move {x['t_move'].mean() / 1e3:6.2f} pub {pub.mean():5.2f}) "
                          f"first {(x['t_start'].min() - t0) / 1e3:7.1f} last {(x['t_end'].max() - t0) / 1e3:7.1f}")
     return "\n".join(lines)

@@ -26,7 +26,8 @@ def main():
     ap.add_argument("--ipw", default="4")
     ap.add_argument("--lag", default="2")
     ap.add_argument("--mode", default="1")
-    ap.add_argument("--dma", default="1")
+    ap.add_argument("--dma", default="0")
+    ap.add_argument("--ww", default="8")
     args = ap.parse_args()
     local = int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
@@ -52,9 +53,11 @@ def main():
                 buf.normal_()
                 fn = lambda: comm.all_reduce(buf)  # noqa: E731
             tstar = comm.t_star(coll, M)
-            for ctas, ch, ipw, lag, mode, dma in itertools.product(
+            for ctas, ch, ipw, lag, mode, dma, ww in itertools.product(
                     args.ctas.split(","), args.chunks.split(","), args.ipw.split(","),
-                    args.lag.split(","), args.mode.split(","), args.dma.split(",")):
+                    args.lag.split(","), args.mode.split(","), args.dma.split(","),
+                    args.ww.split(",")):
+                comm.set_option("worker_warps", int(ww))
                 comm.set_option("dma_root_copy", int(dma))
                 comm.set_option("lag", int(lag))
                 comm.set_option("copy_mode", int(mode))
@@ -64,7 +67,7 @@ def main():
                 ms = timed(fn, 10, 3, dist)
                 info = comm.last_call_info()
                 if rank == 0:
-                    print(f"{coll:15s} {mib:6d}MiB ctas={ctas:>4s} chunk={int(ch)//1024:5d}K ipw={ipw} lag={lag:>3s} m={mode} dma={dma} "
+                    print(f"{coll:15s} {mib:6d}MiB ctas={ctas:>4s} chunk={int(ch)//1024:5d}K ipw={ipw} lag={lag:>3s} m={mode} dma={dma} ww={ww} "
                           f"n={info['nchunks']:5d} L={info['launches']} ms={ms:8.4f} "
                           f"algbw={gbs(M, ms):8.1f} frac_T*={tstar*1e3/ms:6.3f}", flush=True)
     comm.check()
