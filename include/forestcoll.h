@@ -92,6 +92,8 @@ extern "C" {
 #define FC_OPT_COPY_MODE 7     /* 0: TMA bulk stores, 1: TMA loads + vector stores (default 0) */
 #define FC_OPT_DMA_ROOT_COPY 8 /* allgather: copy engine places the own shard (default 0) */
 #define FC_OPT_WORKER_WARPS 9  /* warps per work item: 1, 2, 4, 8 (default 4 real, 1 virtual) */
+#define FC_OPT_PROTO 10        /* -1 auto, 0 chunk flags + fences, 1 LL128 lines (default -1) */
+#define FC_OPT_LL_MAX 11       /* auto: LL128 when bytes per rank <= this (default 64 MiB) */
 
 typedef struct fc_comm fc_comm_t;
 

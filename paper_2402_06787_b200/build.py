@@ -32,8 +32,8 @@ def sources():
 
 
 def inputs():
-    return sources() + sorted(glob.glob(os.path.join(CSRC, "*.h"))) + [
-        os.path.join(REPO, "include", "forestcoll.h")]
+    return sources() + sorted(glob.glob(os.path.join(CSRC, "*.h"))) + sorted(
+        glob.glob(os.path.join(CSRC, "*.cuh"))) + [os.path.join(REPO, "include", "forestcoll.h")]
 
 
 def stale() -> bool:
@@ -44,20 +44,42 @@ def stale() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
+    """Compile every translation unit in parallel (-c), then link the .so."""
     if not force and not stale():
         return OUT
     os.makedirs(os.path.dirname(OUT), exist_ok=True)
     nvcc = os.environ.get("NVCC", "nvcc")
+    objdir = os.path.join(PKG, "lib", "obj")
+    os.makedirs(objdir, exist_ok=True)
+    compile_flags = [f for f in NVCC_FLAGS if f != "-shared"]
+    procs = []
+    objs = []
+    for src in sources():
+        obj = os.path.join(objdir, os.path.basename(src)[:-3] + ".o")
+        objs.append(obj)
+        procs.append((src, subprocess.Popen([nvcc, *compile_flags, "-c", "-o", obj, src],
+                                            stdout=subprocess.PIPE, stderr=subprocess.PIPE,
+                                            text=True)))
+    log = []
+    failed = False
+    for src, pr in procs:
+        out, err = pr.communicate()
+        log.append(f"== {os.path.basename(src)}\n{out}{err}")
+        if pr.returncode != 0:
+            failed = True
+            sys.stderr.write(out + err)
+    with open(os.path.join(PKG, "lib", "ptxas.log"), "w") as f:
+        f.write("\n".join(log))
+    if failed:
+        raise RuntimeError("nvcc failed building libforestcoll.so")
     tmp = OUT + ".tmp"
-    cmd = [nvcc, *NVCC_FLAGS, "-o", tmp, *sources()]
-    r = subprocess.run(cmd, capture_output=True, text=True)
+    r = subprocess.run([nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared",
+                        "-Xcompiler", "-fPIC", "-o", tmp, *objs], capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
-        raise RuntimeError("nvcc failed building libforestcoll.so")
+        raise RuntimeError("nvcc link failed for libforestcoll.so")
     if verbose:
-        sys.stderr.write(r.stderr)
-    with open(os.path.join(PKG, "lib", "ptxas.log"), "w") as f:
-        f.write(r.stderr)
+        sys.stderr.write("\n".join(log))
     os.replace(tmp, OUT)
     return OUT
 

@@ -39,7 +39,7 @@ MAGIC = 0x50434C46
 VERSION = 1
 HEADER_WORDS = 16
 RANKDESC_WORDS = 8
-TASK_WORDS = 80
+TASK_WORDS = 128
 COLLECTIVE_CODE = {ALLGATHER: 0, REDUCE_SCATTER: 1, ALLREDUCE: 2}
 
 K_AG_ROOT, K_AG_FWD, K_RS_FWD, K_RS_ROOT, K_AR_ROOT, K_WAIT_AG = 1, 2, 3, 4, 5, 6
@@ -53,6 +53,7 @@ TW_AG_PARENT, TW_N_AG_CHILD, TW_AG_CHILD = 6, 7, 8
 TW_RS_PARENT, TW_RS_PSLOT, TW_RS_PPREFIX, TW_N_RS_CHILD = 24, 25, 26, 27
 TW_RS_CHILD, TW_RS_CSLOT, TW_RS_CPREFIX = 28, 44, 60
 TW_LAG, TW_AG_LEAFMASK = 76, 77
+TW_AG_MYSLOT, TW_AG_MYPREFIX, TW_AG_CSLOT, TW_AG_CPREFIX = 78, 79, 80, 96
 
 
 @dataclass
@@ -91,6 +92,10 @@ class Task:
     rs_cprefix: tuple = ()
     lag: int = 0  # dense stage index (claim-order skew), set by lower()
     leafmask: int = 0  # bit j: ag_children[j] is a leaf of this tree
+    ag_myslot: int = -1  # LL staging slot receiving this tree's broadcast here
+    ag_myprefix: int = 0
+    ag_cslots: tuple = ()  # the children's staging slots for this tree
+    ag_cprefix: tuple = ()
 
 
 @dataclass
@@ -106,6 +111,8 @@ class Plan:
     slot_units: list
     nslots: list
     table: np.ndarray
+    ag_slot_units: list = field(default_factory=list)
+    ag_nslots: list = field(default_factory=list)
 
     @property
     def max_depth(self) -> int:
@@ -288,6 +295,24 @@ def lower(schedule, ranks=None, collective: str | None = None) -> Plan:
                     else:
                         tasks[v].append(Task(K_WAIT_AG, **kw))
 
+    # broadcast staging slots (fenceless LL protocol): one per (tree, non-root rank)
+    ag_slot_of = {}
+    ag_units = [0] * n
+    ag_nslots = [0] * n
+    if coll in (ALLGATHER, ALLREDUCE):
+        for t in trees:
+            for v in range(n):
+                if v != t.root:
+                    ag_slot_of[(t.index, v)] = (ag_nslots[v], ag_units[v])
+                    ag_nslots[v] += 1
+                    ag_units[v] += t.multiplicity
+        for v in range(n):
+            for x in tasks[v]:
+                if x.kind in (K_AG_ROOT, K_AG_FWD, K_AR_ROOT, K_WAIT_AG):
+                    if x.kind in (K_AG_FWD, K_WAIT_AG):
+                        x.ag_myslot, x.ag_myprefix = ag_slot_of[(x.tree, v)]
+                    x.ag_cslots = tuple(ag_slot_of[(x.tree, ch)][0] for ch in x.ag_children)
+                    x.ag_cprefix = tuple(ag_slot_of[(x.tree, ch)][1] for ch in x.ag_children)
     # dense stage index, global over ranks: the kernel claims item (c, task)
     # at diagonal c + lag * index, so dependencies stay at smaller diagonals
     dense = {st: i for i, st in enumerate(sorted({x.stage for ts in tasks for x in ts}))}
@@ -303,16 +328,22 @@ def lower(schedule, ranks=None, collective: str | None = None) -> Plan:
         tasks[v] = act + wai
         nactive.append(len(act))
         nwait.append(len(wai))
-    table = encode(coll, n, k, trees, tasks, nactive, nwait, slot_units, nslots)
-    return Plan(coll, n, k, ranks, trees, tasks, nactive, nwait, slot_units, nslots, table)
+    table = encode(coll, n, k, trees, tasks, nactive, nwait, slot_units, nslots, ag_units,
+                   ag_nslots)
+    return Plan(coll, n, k, ranks, trees, tasks, nactive, nwait, slot_units, nslots, table,
+                ag_units, ag_nslots)
 
 
-def encode(coll, n, k, trees, tasks, nactive, nwait, slot_units, nslots) -> np.ndarray:
+def encode(coll, n, k, trees, tasks, nactive, nwait, slot_units, nslots, ag_units=None,
+           ag_nslots=None) -> np.ndarray:
     ntasks = sum(len(t) for t in tasks)
     words = HEADER_WORDS + n * RANKDESC_WORDS + ntasks * TASK_WORDS
     a = np.zeros(words, dtype=np.int32)
-    a[0:10] = [MAGIC, VERSION, COLLECTIVE_CODE[coll], n, k, len(trees), ntasks, TASK_WORDS,
-               max(slot_units) if slot_units else 0, max(nslots) if nslots else 0]
+    ag_units = ag_units or [0]
+    ag_nslots = ag_nslots or [0]
+    a[0:12] = [MAGIC, VERSION, COLLECTIVE_CODE[coll], n, k, len(trees), ntasks, TASK_WORDS,
+               max(slot_units) if slot_units else 0, max(nslots) if nslots else 0,
+               max(ag_units), max(ag_nslots)]
     first = 0
     pos = HEADER_WORDS + n * RANKDESC_WORDS
     for v in range(n):
@@ -337,6 +368,11 @@ def encode(coll, n, k, trees, tasks, nactive, nwait, slot_units, nslots) -> np.n
             row[TW_RS_CPREFIX:TW_RS_CPREFIX + m] = t.rs_cprefix
             row[TW_LAG] = t.lag
             row[TW_AG_LEAFMASK] = t.leafmask
+            row[TW_AG_MYSLOT] = t.ag_myslot
+            row[TW_AG_MYPREFIX] = t.ag_myprefix
+            g = len(t.ag_cslots)
+            row[TW_AG_CSLOT:TW_AG_CSLOT + g] = t.ag_cslots
+            row[TW_AG_CPREFIX:TW_AG_CPREFIX + g] = t.ag_cprefix
             pos += TASK_WORDS
     return a
 

@@ -48,6 +48,7 @@ struct Reg {
 struct Plan {
   bool loaded = false;
   int nranks = 0, k = 0, ntrees = 0, max_slot_units = 0, max_slots = 0, max_mult = 0;
+  int max_ag_slot_units = 0, max_ag_slots = 0;
   long long active_total = 0;
   int* d_tasks[FC_MAXR] = {};
   int nact[FC_MAXR] = {}, nwait[FC_MAXR] = {}, lag_max[FC_MAXR] = {};
@@ -72,6 +73,8 @@ struct fc_comm {
   int copy_mode = 1;
   int dma_root_copy = 0;
   int worker_warps = 8;
+  int proto = -1;                  // -1 auto, 0 chunk flags, 1 LL128
+  long long ll_max = 64LL << 20;   // auto: LL128 when bytes moved per rank <= this
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   FcTraceRec* trace = nullptr;
@@ -279,6 +282,34 @@ int run(fc_comm* c, int coll, const void* const* sends, void* const* recvs, size
     P.unit_bytes = unit_for(W);
   }
   P.nchunks = (int)n;
+  // LL128 for small/medium messages: one window, 8-byte aligned slices, and
+  // staging for every in-edge of the call fits in scratch
+  int proto = 0;
+  if (c->proto != 0 && n <= kMaxC) {
+    bool aligned = (stride * es) % 8 == 0;
+    for (int i = 0; i < c->nlocal; ++i)
+      aligned = aligned && ((uintptr_t)sends[i] % 8 == 0) && ((uintptr_t)recvs[i] % 8 == 0);
+    for (int r = 0; r < N && aligned; ++r) {
+      long long Sr = std::max(0LL, std::min(S, total - (long long)r * stride));
+      for (int m = 0; m <= pl.k && aligned; ++m) aligned = ((Sr * m / pl.k) * es) % 8 == 0;
+    }
+    const long long unit_lines = ((S + pl.k - 1) / pl.k * es + 119) / 120;
+    const long long llu = unit_lines * 128;
+    const long long rs_need = (long long)pl.max_slot_units * llu + 256LL * pl.max_slots;
+    const long long ag_base = (rs_need + 255) / 256 * 256;
+    const long long need = ag_base + (long long)pl.max_ag_slot_units * llu + 256LL * pl.max_ag_slots;
+    const long long moved = (coll == FC_REDUCE_SCATTER) ? total * es : S * es * N;
+    const bool want = c->proto == 1 || moved <= c->ll_max;
+    if (aligned && want && need <= (long long)c->scratch_bytes) {
+      proto = 1;
+      W = n;
+      P.ll_unit_bytes = llu;
+      P.ll_ag_base = ag_base;
+    } else if (c->proto == 1) {
+      return fail(c, FC_ERR_UNSUPPORTED, "LL protocol forced but not applicable (alignment/scratch)");
+    }
+  }
+  P.proto = proto;
   const int coop = c->virt ? 1 : 0;
   int launches = 0, grid = 0;
   // allgather: a copy engine places each local root's own shard into its
@@ -312,6 +343,7 @@ int run(fc_comm* c, int coll, const void* const* sends, void* const* recvs, size
   c->info[2] = W;
   c->info[3] = grid;
   c->info[4] = P.unit_bytes;
+  c->info[5] = proto;
   return FC_SUCCESS;
 }
 
@@ -493,6 +525,14 @@ int fc_comm_set_option(fc_comm_t* c, int option, long long v) {
         return fail(c, FC_ERR_INVALID_ARG, "worker_warps must be 1, 2, 4 or 8");
       c->worker_warps = (int)v;
       return FC_SUCCESS;
+    case FC_OPT_PROTO:
+      if (v < -1 || v > 1) return fail(c, FC_ERR_INVALID_ARG, "proto is -1 (auto), 0 or 1");
+      c->proto = (int)v;
+      return FC_SUCCESS;
+    case FC_OPT_LL_MAX:
+      if (v < 0) return fail(c, FC_ERR_INVALID_ARG, "ll_max < 0");
+      c->ll_max = v;
+      return FC_SUCCESS;
     default:
       return fail(c, FC_ERR_INVALID_ARG, "unknown option %d", option);
   }
@@ -510,6 +550,8 @@ int fc_comm_get_option(fc_comm_t* c, int option, long long* v) {
     case FC_OPT_COPY_MODE: *v = c->copy_mode; return FC_SUCCESS;
     case FC_OPT_DMA_ROOT_COPY: *v = c->dma_root_copy; return FC_SUCCESS;
     case FC_OPT_WORKER_WARPS: *v = c->worker_warps; return FC_SUCCESS;
+    case FC_OPT_PROTO: *v = c->proto; return FC_SUCCESS;
+    case FC_OPT_LL_MAX: *v = c->ll_max; return FC_SUCCESS;
     default: return fail(c, FC_ERR_INVALID_ARG, "unknown option %d", option);
   }
 }
@@ -641,6 +683,9 @@ int fc_plan_load(fc_comm_t* c, int coll, const int32_t* t, size_t nwords) {
   p.ntrees = ntrees;
   p.max_slot_units = t[TH_MAX_SLOT_UNITS];
   p.max_slots = t[TH_MAX_SLOTS];
+  p.max_ag_slot_units = t[TH_MAX_AG_SLOT_UNITS];
+  p.max_ag_slots = t[TH_MAX_AG_SLOTS];
+  if (p.max_ag_slots > kSlotCap) return fail(c, FC_ERR_PLAN, "too many staging slots per rank");
   // validate every row
   for (int i = 0; i < ntasks; ++i) {
     const int32_t* T = t + task0 + (size_t)i * FC_TASK_WORDS;
@@ -678,7 +723,7 @@ int fc_plan_load(fc_comm_t* c, int coll, const int32_t* t, size_t nwords) {
     const int rows = std::max(1, D[RD_NACTIVE] + D[RD_NWAIT]);
     p.nact[i] = D[RD_NACTIVE];
     p.nwait[i] = D[RD_NWAIT];
-    for (int j = 0; j < D[RD_NACTIVE]; ++j)
+    for (int j = 0; j < D[RD_NACTIVE] + D[RD_NWAIT]; ++j)
       p.lag_max[i] = std::max(p.lag_max[i], t[task0 + (size_t)(D[RD_FIRST] + j) * FC_TASK_WORDS + TW_LAG]);
     cudaError_t e = cudaMalloc((void**)&p.d_tasks[i], (size_t)rows * FC_TASK_WORDS * 4);
     if (e == cudaSuccess && D[RD_NACTIVE] + D[RD_NWAIT] > 0)

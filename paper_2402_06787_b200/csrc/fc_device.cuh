@@ -1,3 +1,4 @@
+#pragma once
 // Persistent sm_100a executor kernel for ForestColl forests.
 //
 // One grid executes the tree tasks of one or more ranks (one rank per GPU in
@@ -37,6 +38,8 @@
 #include <cstdint>
 
 #include "fc_internal.h"
+
+#define FC_SMEM_BYTES (FC_WPC * FC_NST * FC_STAGE)
 
 #define FC_WPC 8                           // warps per CTA
 // WW (template): warps per worker; a worker holds one item in flight.
@@ -225,6 +228,47 @@ struct Acc16 {
     return out;
   }
 };
+
+// 8-byte (one LL payload word) variant of Acc16.
+template <int DT>
+struct Acc8 {
+  using R = Red<DT>;
+  using E = typename R::E;
+  static constexpr int NE = 8 / sizeof(E);
+  typename R::A a[NE];
+  __device__ __forceinline__ void init(unsigned long long v) {
+    const E* e = reinterpret_cast<const E*>(&v);
+#pragma unroll
+    for (int q = 0; q < NE; ++q) a[q] = R::to(e[q]);
+  }
+  __device__ __forceinline__ void add(unsigned long long v) {
+    const E* e = reinterpret_cast<const E*>(&v);
+#pragma unroll
+    for (int q = 0; q < NE; ++q) a[q] = R::add(a[q], R::to(e[q]));
+  }
+  __device__ __forceinline__ unsigned long long pack() const {
+    unsigned long long out;
+    E* e = reinterpret_cast<E*>(&out);
+#pragma unroll
+    for (int q = 0; q < NE; ++q) e[q] = R::from(a[q]);
+    return out;
+  }
+};
+
+// ---------------------------------------------------------------------------
+// LL128 lines: 120 payload bytes + an 8-byte flag per 128-byte line, written
+// by 8 lanes with one 16-byte store each (lane 7 carries the flag).  NVLink
+// delivers a warp's 128-byte line store whole, so a reader that sees the
+// flag sees the payload: no fence, no separate flag, per-line cut-through.
+// ---------------------------------------------------------------------------
+#define FC_LL_PAY 120
+__device__ __forceinline__ void st_line16(char* p, unsigned long long a, unsigned long long b) {
+  asm volatile("st.volatile.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
+}
+__device__ __forceinline__ void ld_line16(const char* p, unsigned long long& a,
+                                          unsigned long long& b) {
+  asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
+}
 
 // ---------------------------------------------------------------------------
 // Warp-level fallback movers (unaligned / heads / tails).  All pointers of
@@ -635,7 +679,190 @@ __device__ void run_item(const FcParams& P, int me, FcCtl* ctl, const int* T, in
   }
 }
 
+#define FC_LL_UNROLL 8  // 4-line batches per warp iteration (32 lines = 3.75 KiB payload)
+
+// Poll FC_LL_UNROLL 4-line batches (lane group g = lane/8 owns line base+4u+g)
+// until every valid line carries `flag`.  Returns false on timeout / error.
+__device__ __forceinline__ bool ll_poll(const char* const* line, const bool* valid,
+                                        unsigned long long flag, int lane,
+                                        unsigned long long* a, unsigned long long* b,
+                                        FcCtl* ctl, long long timeout_ns) {
+  unsigned long long t0 = 0;
+  for (unsigned it = 0;; ++it) {
+#pragma unroll
+    for (int u = 0; u < FC_LL_UNROLL; ++u)
+      if (valid[u]) ld_line16(line[u], a[u], b[u]);
+    int mine = 1;
+#pragma unroll
+    for (int u = 0; u < FC_LL_UNROLL; ++u)
+      mine &= (!valid[u] || (lane & 7) != 7 || b[u] == flag) ? 1 : 0;
+    const int grp = __shfl_sync(0xffffffffu, mine, (lane & ~7) | 7);
+    if (__all_sync(0xffffffffu, grp)) return true;
+    if ((it & 255u) == 255u) {
+      int bad = 0;
+      if (lane == 0) {
+        if (!t0) t0 = globaltimer();
+        if (ld_volatile(&ctl->error) != 0) bad = 1;
+        else if ((long long)(globaltimer() - t0) > timeout_ns) {
+          atomicCAS(&ctl->error, 0u, (unsigned)FC_DEVERR_TIMEOUT_AG);
+          bad = 1;
+        }
+      }
+      if (__shfl_sync(0xffffffffu, bad, 0)) return false;
+    }
+  }
+}
+
+// One item in the LL protocol.  Lines of the chunk are dealt to the worker's
+// warps 4*FC_LL_UNROLL at a time; lane group g (8 lanes) handles one 128-byte
+// line per batch, with all batches' loads in flight together.
 template <int DT, int WW>
+__device__ void run_item_ll(const FcParams& P, int me, FcCtl* ctl, const int* T, int c,
+                            unsigned e, int w, int lane, unsigned& ready_mask, ItemShared* sh,
+                            unsigned long long& t_ready) {
+  constexpr int U = FC_LL_UNROLL;
+  const int kind = __ldg(T + TW_KIND);
+  const int root = __ldg(T + TW_ROOT);
+  const long long es = P.esize;
+  long long Sr = P.total_elems - (long long)root * P.stride_elems;
+  Sr = Sr < 0 ? 0 : (Sr > P.shard_elems ? P.shard_elems : Sr);
+  const long long base = (long long)root * P.stride_elems * es;
+  const long long lo = base + (Sr * __ldg(T + TW_MLO) / P.k) * es;
+  const long long hi = base + (Sr * __ldg(T + TW_MHI) / P.k) * es;
+  const long long L = (hi - lo + FC_LL_PAY - 1) / FC_LL_PAY;
+  const long long l0 = L * c / P.nchunks, l1 = L * (c + 1) / P.nchunks;
+  const long long lw = L * P.c0 / P.nchunks;
+  const int n_ag = __ldg(T + TW_N_AG_CHILD);
+  const int n_rs = __ldg(T + TW_N_RS_CHILD);
+  const int rs_parent = __ldg(T + TW_RS_PARENT);
+  const int wl = w % WW;
+  const int wk = w / WW;
+  const bool leader = (wl == 0 && lane == 0);
+  const unsigned long long flag = (unsigned long long)e;
+
+  // entry barrier only (no chunk flags in LL): destinations must have entered
+  if (leader) {
+    bool ok = true;
+    if (kind != FC_K_WAIT_AG && kind != FC_K_RS_ROOT) {
+      const int nx = (kind == FC_K_RS_FWD) ? 1 : n_ag;
+      for (int j = 0; j < nx && ok; ++j) {
+        const int x = (kind == FC_K_RS_FWD) ? rs_parent : __ldg(T + TW_AG_CHILD + j);
+        if (!((ready_mask >> x) & 1u)) {
+          ok = spin_geq(P.flags[me] + x, e, ctl, P.timeout_ns, FC_DEVERR_TIMEOUT_READY);
+          if (ok) ready_mask |= 1u << x;
+        }
+      }
+    }
+    sh->ok = ok ? 1 : 0;
+    if (P.trace) t_ready = globaltimer();
+  }
+  worker_sync<WW>(wk);
+  if (!sh->ok) return;
+
+  const int g = lane >> 3, gl = lane & 7;
+  const long long slot_ofs = -lw * 128LL;  // line l of the window at slot + (l - lw)*128
+  auto slot_ptr = [&](int rank, long long region, int slot, int prefix) -> char* {
+    return P.scratch[rank] + region + P.ll_unit_bytes * prefix + 256LL * slot + slot_ofs;
+  };
+  const bool polls = (kind == FC_K_AG_FWD || kind == FC_K_WAIT_AG);
+  const char* my_ag = polls ? slot_ptr(me, P.ll_ag_base, __ldg(T + TW_AG_MYSLOT),
+                                       __ldg(T + TW_AG_MYPREFIX)) : nullptr;
+  // payload words of this lane in a line: gl<7 -> 2*gl, 2*gl+1 ; gl==7 -> 14 (+flag)
+  const int q0 = 2 * gl;
+  const bool two = gl != 7;
+  const char* local_src = nullptr;  // payload source, indexed by absolute byte offset
+  if (kind == FC_K_AG_ROOT) local_src = P.send[me] - base;
+  if (kind == FC_K_RS_FWD || kind == FC_K_RS_ROOT || kind == FC_K_AR_ROOT) local_src = P.send[me];
+  char* out_local = nullptr;  // payload destination in a local buffer
+  if (polls || kind == FC_K_AR_ROOT) out_local = P.recv[me];
+  if (kind == FC_K_AG_ROOT && !P.root_local_done && P.recv[me] + lo != P.send[me] + (lo - base))
+    out_local = P.recv[me];
+  if (kind == FC_K_RS_ROOT) out_local = P.recv[me] - base;  // out has S elements
+
+  for (long long lb = l0 + 4LL * U * wl; lb < l1; lb += 4LL * U * WW) {
+    bool valid[U], v0[U], v1[U];
+    long long pay[U];
+    unsigned long long w0[U], w1[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const long long l = lb + 4 * u + g;
+      valid[u] = l < l1;
+      pay[u] = lo + (long long)FC_LL_PAY * l;
+      v0[u] = valid[u] && pay[u] + 8LL * q0 + 8 <= hi;
+      v1[u] = valid[u] && two && pay[u] + 8LL * (q0 + 1) + 8 <= hi;
+      w0[u] = 0;
+      w1[u] = 0;
+    }
+    if (polls) {
+      const char* lp[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) lp[u] = my_ag + (lb + 4 * u + g) * 128 + 16 * gl;
+      if (!ll_poll(lp, valid, flag, lane, w0, w1, ctl, P.timeout_ns)) return;
+    } else {
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const unsigned long long* src =
+            reinterpret_cast<const unsigned long long*>(local_src + pay[u]) + q0;
+        if (v0[u]) w0[u] = __ldcg(src);
+        if (v1[u]) w1[u] = __ldcg(src + 1);
+      }
+      if (kind != FC_K_AG_ROOT && n_rs > 0) {
+        Acc8<DT> a0[U], a1[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          a0[u].init(w0[u]);
+          a1[u].init(w1[u]);
+        }
+        for (int j = 0; j < n_rs; ++j) {
+          const char* cl = slot_ptr(me, 0, __ldg(T + TW_RS_CSLOT + j), __ldg(T + TW_RS_CPREFIX + j));
+          const char* lp[U];
+          unsigned long long x0[U], x1[U];
+#pragma unroll
+          for (int u = 0; u < U; ++u) lp[u] = cl + (lb + 4 * u + g) * 128 + 16 * gl;
+          if (!ll_poll(lp, valid, flag, lane, x0, x1, ctl, P.timeout_ns)) return;
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            a0[u].add(x0[u]);
+            a1[u].add(x1[u]);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          w0[u] = a0[u].pack();
+          w1[u] = a1[u].pack();
+        }
+      }
+    }
+    // local payload write
+    if (out_local) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        unsigned long long* o = reinterpret_cast<unsigned long long*>(out_local + pay[u]) + q0;
+        if (v0[u]) o[0] = w0[u];
+        if (v1[u]) o[1] = w1[u];
+      }
+    }
+    // line stores to peers' staging
+    char* dl[FC_MAXS];
+    int nl = 0;
+    if (kind == FC_K_RS_FWD) {
+      dl[nl++] = slot_ptr(rs_parent, 0, __ldg(T + TW_RS_PSLOT), __ldg(T + TW_RS_PPREFIX));
+    } else if (kind == FC_K_AG_ROOT || kind == FC_K_AG_FWD || kind == FC_K_AR_ROOT) {
+      for (int j = 0; j < n_ag; ++j)
+        dl[nl++] = slot_ptr(__ldg(T + TW_AG_CHILD + j), P.ll_ag_base, __ldg(T + TW_AG_CSLOT + j),
+                            __ldg(T + TW_AG_CPREFIX + j));
+    }
+    for (int d = 0; d < nl; ++d) {
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (valid[u])
+          st_line16(dl[d] + (lb + 4 * u + g) * 128 + 16 * gl, w0[u], two ? w1[u] : flag);
+    }
+  }
+  worker_sync<WW>(wk);
+}
+
+template <int DT, int WW, int PROTO>
 __global__ void __launch_bounds__(FC_BLOCK, 1) fc_forest_kernel(const __grid_constant__ FcParams P) {
   constexpr int FC_NWK = FC_WPC / WW;
   extern __shared__ __align__(128) char smem[];
@@ -668,8 +895,10 @@ __global__ void __launch_bounds__(FC_BLOCK, 1) fc_forest_kernel(const __grid_con
   const int nwait = P.nwait[lr];
   const long long W = P.c1 - P.c0;
   const long long span = W + (long long)P.lag * P.lag_max[lr];
-  const long long nA = (long long)nact * span;
-  const long long total = nA + nwait;  // one completion wait per leaf task
+  // LL: leaf tasks are real items (they copy their lines out of staging)
+  const int nitem = PROTO ? nact + nwait : nact;
+  const long long nA = (long long)nitem * span;
+  const long long total = nA + (PROTO ? 0 : nwait);  // simple: one completion wait per leaf
   unsigned ready_mask = 1u << me;
   FcTraceRec* const trace = P.trace;
   for (;;) {
@@ -684,8 +913,8 @@ __global__ void __launch_bounds__(FC_BLOCK, 1) fc_forest_kernel(const __grid_con
     if (item >= total) break;
     int c, ti;
     if (item < nA) {
-      const long long d = item / nact;
-      ti = (int)(item - d * nact);
+      const long long d = item / nitem;
+      ti = (int)(item - d * nitem);
       const long long cc =
           d - (long long)P.lag * __ldg(tasks + (long long)ti * FC_TASK_WORDS + TW_LAG);
       if (cc < 0 || cc >= W) continue;  // outside this task's diagonal window
@@ -696,8 +925,12 @@ __global__ void __launch_bounds__(FC_BLOCK, 1) fc_forest_kernel(const __grid_con
     }
     const unsigned long long t0 = trace ? globaltimer() : 0;
     unsigned long long t_ready = t0, t_moved = t0;
-    run_item<DT, WW>(P, me, ctl, tasks + (long long)ti * FC_TASK_WORDS, P.c0 + c, e, w, lane,
-                 ready_mask, rg, &sh, t_ready, t_moved);
+    if constexpr (PROTO == 1)
+      run_item_ll<DT, WW>(P, me, ctl, tasks + (long long)ti * FC_TASK_WORDS, P.c0 + c, e, w,
+                          lane, ready_mask, &sh, t_ready);
+    else
+      run_item<DT, WW>(P, me, ctl, tasks + (long long)ti * FC_TASK_WORDS, P.c0 + c, e, w, lane,
+                       ready_mask, rg, &sh, t_ready, t_moved);
     if (trace && lead) {
       const unsigned idx = atomicAdd(P.trace_count, 1u);
       if (idx < P.trace_cap) {
@@ -729,62 +962,24 @@ __global__ void __launch_bounds__(FC_BLOCK, 1) fc_forest_kernel(const __grid_con
   }
 }
 
-template <int WW>
-const void* kernel_for_ww(int rd) {
-  switch (rd) {
-    case FC_BFLOAT16: return (const void*)fc_forest_kernel<FC_BFLOAT16, WW>;
-    case FC_FLOAT16: return (const void*)fc_forest_kernel<FC_FLOAT16, WW>;
-    case FC_INT32: return (const void*)fc_forest_kernel<FC_INT32, WW>;
-    default: return (const void*)fc_forest_kernel<FC_FLOAT32, WW>;
-  }
-}
-
-const void* kernel_for(int rd, int ww) {
-  switch (ww) {
-    case 1: return kernel_for_ww<1>(rd);
-    case 2: return kernel_for_ww<2>(rd);
-    case 4: return kernel_for_ww<4>(rd);
-    default: return kernel_for_ww<8>(rd);
-  }
-}
-
-int ensure_smem_attr(const void* fn) {
-  static const void* done[32] = {};
-  for (auto& d : done) {
-    if (d == fn) return 0;
-    if (!d) {
-      const cudaError_t e =
-          cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, FC_SMEM);
-      if (e != cudaSuccess) return (int)e;
-      d = fn;
-      return 0;
-    }
-  }
-  return 0;
-}
 
 }  // namespace
 
-int fc_launch(const FcParams& p, int reduce_dtype, int cooperative, void* stream, int* grid_out) {
-  const dim3 grid(p.nlocal * p.ctas_per_rank), block(FC_BLOCK);
-  void* args[] = {(void*)&p};
-  const void* fn = kernel_for(reduce_dtype, p.worker_warps);
-  if (grid_out) *grid_out = (int)grid.x;
-  const int a = ensure_smem_attr(fn);
-  if (a) return a;
-  cudaError_t err;
-  if (cooperative)
-    err = cudaLaunchCooperativeKernel(fn, grid, block, args, FC_SMEM, (cudaStream_t)stream);
-  else
-    err = cudaLaunchKernel(fn, grid, block, args, FC_SMEM, (cudaStream_t)stream);
-  return (int)err;
-}
-
-int fc_max_ctas_per_sm(int reduce_dtype, int* out) {
-  const void* fn = kernel_for(reduce_dtype, 8);
-  const int a = ensure_smem_attr(fn);
-  if (a) return a;
-  return (int)cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, fn, FC_BLOCK, FC_SMEM);
-}
-
-int fc_warps_per_cta() { return FC_WPC; }
+// Kernel pointer for one (dtype, worker warps, protocol) instantiation.
+#define FC_DEFINE_KERNEL_TABLE(NAME, DT)                                          \
+  const void* NAME(int ww, int proto) {                                           \
+    if (proto) {                                                                  \
+      switch (ww) {                                                               \
+        case 1: return (const void*)fc_forest_kernel<DT, 1, 1>;                   \
+        case 2: return (const void*)fc_forest_kernel<DT, 2, 1>;                   \
+        case 4: return (const void*)fc_forest_kernel<DT, 4, 1>;                   \
+        default: return (const void*)fc_forest_kernel<DT, 8, 1>;                  \
+      }                                                                           \
+    }                                                                             \
+    switch (ww) {                                                                 \
+      case 1: return (const void*)fc_forest_kernel<DT, 1, 0>;                     \
+      case 2: return (const void*)fc_forest_kernel<DT, 2, 0>;                     \
+      case 4: return (const void*)fc_forest_kernel<DT, 4, 0>;                     \
+      default: return (const void*)fc_forest_kernel<DT, 8, 0>;                    \
+    }                                                                             \
+  }

@@ -12,7 +12,7 @@
 #define FC_TABLE_VERSION 1
 #define FC_HEADER_WORDS 16
 #define FC_RANKDESC_WORDS 8
-#define FC_TASK_WORDS 80
+#define FC_TASK_WORDS 128
 
 // Task kinds (one task = one tree as seen from one rank).  See DESIGN.md §3.
 enum {
@@ -44,7 +44,11 @@ enum {
   TW_RS_CPREFIX = 60,  // [FC_MAXR]
   TW_LAG = 76,         // dense stage index: claim-order skew (chunk + lag * TW_LAG)
   TW_AG_LEAFMASK = 77, // bit j: AG child j is a leaf (gets an arrival count, no chunk flags)
-  TW_END = 78,
+  TW_AG_MYSLOT = 78,   // LL protocol: staging slot receiving this tree here (-1 at the root)
+  TW_AG_MYPREFIX = 79,
+  TW_AG_CSLOT = 80,    // [FC_MAXR] children's staging slots
+  TW_AG_CPREFIX = 96,  // [FC_MAXR]
+  TW_END = 112,
 };
 
 // Header word offsets of a plan table (see compiler.py for the writer).
@@ -59,6 +63,8 @@ enum {
   TH_TASK_WORDS = 7,
   TH_MAX_SLOT_UNITS = 8,
   TH_MAX_SLOTS = 9,
+  TH_MAX_AG_SLOT_UNITS = 10,
+  TH_MAX_AG_SLOTS = 11,
 };
 // Rank descriptor words: first task, n active, n wait, slot units, n slots.
 enum { RD_FIRST = 0, RD_NACTIVE = 1, RD_NWAIT = 2, RD_SLOT_UNITS = 3, RD_NSLOTS = 4 };
@@ -122,6 +128,9 @@ struct FcParams {
   int copy_mode;    // 0: TMA bulk stores, 1: bulk loads + 16-byte lane stores
   int root_local_done;  // allgather: own shard already placed in recv (DMA engine)
   int worker_warps;     // warps per worker (1, 2, 4, 8): items in flight per CTA = 8 / this
+  int proto;            // 0: chunk flags + fences, 1: LL128 lines (flag in every 128 B)
+  long long ll_unit_bytes;  // LL: staging bytes per unit multiplicity per window
+  long long ll_ag_base;     // LL: scratch offset of the broadcast staging region
   FcTraceRec* trace;
   unsigned* trace_count;
   unsigned trace_cap;

@@ -1,0 +1,74 @@
+// Kernel selection and launch (host side of the kernel TUs).
+#include <cuda_runtime.h>
+
+#include "fc_internal.h"
+
+#define FC_WPC 8
+#define FC_BLOCK (32 * FC_WPC)
+#define FC_SMEM_BYTES (8 * 3 * 8 * 1024)
+
+const void* fc_kernel_ptr_f32(int ww, int proto);
+const void* fc_kernel_ptr_bf16(int ww, int proto);
+const void* fc_kernel_ptr_f16(int ww, int proto);
+const void* fc_kernel_ptr_i32(int ww, int proto);
+
+namespace {
+
+const void* kernel_for(int rd, int ww, int proto) {
+  switch (rd) {
+    case FC_BFLOAT16: return fc_kernel_ptr_bf16(ww, proto);
+    case FC_FLOAT16: return fc_kernel_ptr_f16(ww, proto);
+    case FC_INT32: return fc_kernel_ptr_i32(ww, proto);
+    default: return fc_kernel_ptr_f32(ww, proto);
+  }
+}
+
+int ensure_smem_attr(const void* fn) {
+  static const void* done[64] = {};
+  for (auto& d : done) {
+    if (d == fn) return 0;
+    if (!d) {
+      const cudaError_t e =
+          cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, FC_SMEM_BYTES);
+      if (e != cudaSuccess) return (int)e;
+      d = fn;
+      return 0;
+    }
+  }
+  return 0;
+}
+
+}  // namespace
+
+int fc_launch(const FcParams& p, int reduce_dtype, int cooperative, void* stream, int* grid_out) {
+  const dim3 grid(p.nlocal * p.ctas_per_rank), block(FC_BLOCK);
+  void* args[] = {(void*)&p};
+  const void* fn = kernel_for(reduce_dtype, p.worker_warps, p.proto);
+  if (grid_out) *grid_out = (int)grid.x;
+  const int a = ensure_smem_attr(fn);
+  if (a) return a;
+  cudaError_t err;
+  if (cooperative)
+    err = cudaLaunchCooperativeKernel(fn, grid, block, args, FC_SMEM_BYTES, (cudaStream_t)stream);
+  else
+    err = cudaLaunchKernel(fn, grid, block, args, FC_SMEM_BYTES, (cudaStream_t)stream);
+  return (int)err;
+}
+
+int fc_max_ctas_per_sm(int reduce_dtype, int* out) {
+  int best = 1 << 30;
+  for (int proto = 0; proto < 2; ++proto) {
+    const void* fn = kernel_for(reduce_dtype, 8, proto);
+    const int a = ensure_smem_attr(fn);
+    if (a) return a;
+    int v = 0;
+    const cudaError_t e =
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, fn, FC_BLOCK, FC_SMEM_BYTES);
+    if (e != cudaSuccess) return (int)e;
+    if (v < best) best = v;
+  }
+  *out = best;
+  return 0;
+}
+
+int fc_warps_per_cta() { return FC_WPC; }

@@ -152,7 +152,7 @@ class _CommBase:
         buf = (ctypes.c_longlong * 8)()
         self._lib.fc_last_call_info(self._comm, buf, 8)
         return {"launches": buf[0], "nchunks": buf[1], "window": buf[2], "grid": buf[3],
-                "unit_bytes": buf[4]}
+                "unit_bytes": buf[4], "proto": "ll128" if buf[5] else "flags"}
 
     # -- tracing ------------------------------------------------------------
     TRACE_DTYPE = np.dtype([("t_start", "<u8"), ("t_end", "<u8"), ("t_wait", "<u4"),

@@ -37,19 +37,26 @@ def dev():
     return torch.device("cuda:0")
 
 
-def _comm(s, **kw):
+def _comm(s, proto="auto", **kw):
     from paper_2402_06787_b200 import VirtualComm
 
-    return VirtualComm(schedules={s.collective: s}, **kw)
+    opts = {"timeout_ms": 20000}
+    if proto == "flags":
+        opts["proto"] = 0
+    return VirtualComm(schedules={s.collective: s}, options=opts, **kw)
 
 
+PROTOS = ["auto", "flags"]  # auto = LL128 whenever slices are 8-byte aligned
+
+
+@pytest.mark.parametrize("proto", PROTOS)
 @pytest.mark.parametrize("name", golden_names("allgather"))
 @pytest.mark.parametrize("S", [1, 37, 4096, 262144 + 3])
-def test_allgather_virtual(dev, name, S):
+def test_allgather_virtual(dev, name, S, proto):
     from oracle import forest_oracle as fo
 
     s = load_golden(name)
-    comm = _comm(s)
+    comm = _comm(s, proto)
     n = comm.nranks
     gen = torch.Generator().manual_seed(1234)
     sends = [torch.randint(0, 2**31 - 1, (S,), generator=gen, dtype=torch.int32).view(torch.float32).to(dev)
@@ -62,14 +69,15 @@ def test_allgather_virtual(dev, name, S):
         assert np.array_equal(_bits(_np(outs[r])), _bits(ref[r])), f"rank {r}"
 
 
+@pytest.mark.parametrize("proto", PROTOS)
 @pytest.mark.parametrize("name", golden_names("reduce_scatter"))
 @pytest.mark.parametrize("dtype", ["float32", "bfloat16", "int32", "float16"])
-@pytest.mark.parametrize("S", [5, 1000, 65536 + 7])
-def test_reduce_scatter_virtual(dev, name, dtype, S):
+@pytest.mark.parametrize("S", [5, 1000, 65536 + 8])
+def test_reduce_scatter_virtual(dev, name, dtype, S, proto):
     from oracle import forest_oracle as fo
 
     s = load_golden(name)
-    comm = _comm(s)
+    comm = _comm(s, proto)
     n = comm.nranks
     gen = torch.Generator().manual_seed(99)
     ins = [_rand(n * S, dtype, gen, dev) for _ in range(n)]
@@ -81,14 +89,15 @@ def test_reduce_scatter_virtual(dev, name, dtype, S):
         assert np.array_equal(_bits(_np(outs[r])), _bits(ref[r])), f"rank {r}"
 
 
+@pytest.mark.parametrize("proto", PROTOS)
 @pytest.mark.parametrize("name", golden_names("allreduce"))
 @pytest.mark.parametrize("dtype", ["bfloat16", "float32", "int32"])
 @pytest.mark.parametrize("count", [3, 1001, 1 << 18])
-def test_allreduce_virtual(dev, name, dtype, count):
+def test_allreduce_virtual(dev, name, dtype, count, proto):
     from oracle import forest_oracle as fo
 
     s = load_golden(name)
-    comm = _comm(s)
+    comm = _comm(s, proto)
     n = comm.nranks
     gen = torch.Generator().manual_seed(7)
     ins = [_rand(count, dtype, gen, dev) for _ in range(n)]
@@ -98,3 +107,41 @@ def test_allreduce_virtual(dev, name, dtype, count):
     ref = fo.allreduce(s, [_np(x) for x in ins], dtype)
     for r in range(n):
         assert np.array_equal(_bits(_np(outs[r])), _bits(ref[r])), f"rank {r}"
+
+
+@pytest.mark.parametrize("name", ["nvs8_allgather", "groups300_allgather", "random1_allgather"])
+def test_ll128_is_used_for_aligned_medium_messages(dev, name):
+    s = load_golden(name)
+    comm = _comm(s)
+    n = comm.nranks
+    S = 6 * 10924  # 8-byte aligned batch slices for k in {1, 2, 3, 6, 7?}
+    S = S - S % (2 * s.k)
+    sends = [torch.randn(S, device=dev) for _ in range(n)]
+    outs = [torch.empty(n * S, device=dev) for _ in range(n)]
+    comm.all_gather(outs, sends)
+    comm.check()
+    assert comm.last_call_info()["proto"] == "ll128"
+    cat = torch.cat(sends)
+    for o in outs:
+        assert torch.equal(o, cat)
+
+
+@pytest.mark.parametrize("proto", PROTOS)
+def test_back_to_back_reuse_and_windows(dev, proto):
+    """Many calls on one set of buffers, and forced multi-launch windows."""
+    from oracle import forest_oracle as fo
+
+    s = load_golden("nvs8_reduce_scatter")
+    comm = _comm(s, proto, scratch_bytes=1 << 20)
+    comm.set_option("chunk_max", 16 << 10)
+    n = comm.nranks
+    gen = torch.Generator().manual_seed(5)
+    S = 1 << 17
+    outs = [torch.zeros(S, device=dev) for _ in range(n)]
+    for it in range(4):
+        ins = [torch.empty(n * S).uniform_(-1, 1, generator=gen).to(dev) for _ in range(n)]
+        comm.reduce_scatter(outs, ins)
+        ref = fo.reduce_scatter(s, [x.cpu().numpy() for x in ins], "float32")
+        for r in range(n):
+            assert np.array_equal(outs[r].cpu().numpy().view(np.uint32), ref[r].view(np.uint32))
+    comm.check()

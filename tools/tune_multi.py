@@ -27,7 +27,8 @@ def main():
     ap.add_argument("--lag", default="2")
     ap.add_argument("--mode", default="1")
     ap.add_argument("--dma", default="0")
-    ap.add_argument("--ww", default="8")
+    ap.add_argument("--ww", default="4")
+    ap.add_argument("--proto", default="-1")
     args = ap.parse_args()
     local = int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
@@ -53,10 +54,11 @@ def main():
                 buf.normal_()
                 fn = lambda: comm.all_reduce(buf)  # noqa: E731
             tstar = comm.t_star(coll, M)
-            for ctas, ch, ipw, lag, mode, dma, ww in itertools.product(
+            for ctas, ch, ipw, lag, mode, dma, ww, proto in itertools.product(
                     args.ctas.split(","), args.chunks.split(","), args.ipw.split(","),
                     args.lag.split(","), args.mode.split(","), args.dma.split(","),
-                    args.ww.split(",")):
+                    args.ww.split(","), args.proto.split(",")):
+                comm.set_option("proto", int(proto))
                 comm.set_option("worker_warps", int(ww))
                 comm.set_option("dma_root_copy", int(dma))
                 comm.set_option("lag", int(lag))
@@ -67,7 +69,7 @@ def main():
                 ms = timed(fn, 10, 3, dist)
                 info = comm.last_call_info()
                 if rank == 0:
-                    print(f"{coll:15s} {mib:6d}MiB ctas={ctas:>4s} chunk={int(ch)//1024:5d}K ipw={ipw} lag={lag:>3s} m={mode} dma={dma} ww={ww} "
+                    print(f"{coll:15s} {mib:6d}MiB ctas={ctas:>4s} chunk={int(ch)//1024:5d}K ipw={ipw} lag={lag:>3s} ww={ww} p={info['proto']} "
                           f"n={info['nchunks']:5d} L={info['launches']} ms={ms:8.4f} "
                           f"algbw={gbs(M, ms):8.1f} frac_T*={tstar*1e3/ms:6.3f}", flush=True)
     comm.check()
