@@ -83,17 +83,19 @@ extern "C" {
 #define FC_SUM 0
 
 /* options for fc_comm_set_option */
-#define FC_OPT_CTAS_PER_RANK 1 /* CTAs per rank (default 96 real, 16 virtual) */
-#define FC_OPT_CHUNK_MAX 2     /* max bytes per pipeline chunk (default 256 KiB) */
+#define FC_OPT_CTAS_PER_RANK 1 /* CTAs per rank (default 128 real, 16 virtual) */
+#define FC_OPT_CHUNK_MAX 2     /* max bytes per chunk, flag protocol (default 256 KiB) */
 #define FC_OPT_CHUNK_MIN 3     /* min bytes per pipeline chunk (default 16 KiB) */
 #define FC_OPT_ITEMS_PER_WORKER 4 /* target work items per CTA (default 4) */
 #define FC_OPT_TIMEOUT_MS 5    /* device flag-wait timeout (default 10000 ms) */
 #define FC_OPT_LAG 6           /* claim-order skew, chunks per tree stage (default 64) */
 #define FC_OPT_COPY_MODE 7     /* 0: TMA bulk stores, 1: TMA loads + vector stores (default 0) */
 #define FC_OPT_DMA_ROOT_COPY 8 /* allgather: copy engine places the own shard (default 0) */
-#define FC_OPT_WORKER_WARPS 9  /* warps per work item: 1, 2, 4, 8 (default 4 real, 1 virtual) */
+#define FC_OPT_WORKER_WARPS 9  /* warps per work item: 1, 2, 4, 8 (default 8 real, 1 virtual) */
 #define FC_OPT_PROTO 10        /* -1 auto, 0 chunk flags + fences, 1 LL128 lines (default -1) */
-#define FC_OPT_LL_MAX 11       /* auto: LL128 when bytes per rank <= this (default 64 MiB) */
+#define FC_OPT_LL_MAX 11       /* auto: LL128 when bytes per rank <= this (default 512 MiB) */
+#define FC_OPT_LL_CHUNK_MAX 12 /* max bytes per chunk, LL128 protocol (default 64 KiB) */
+#define FC_OPT_LL_WORKER_WARPS 13 /* warps per work item, LL128 (default 4 real, 1 virtual) */
 
 typedef struct fc_comm fc_comm_t;
 

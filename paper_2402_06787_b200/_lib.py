@@ -19,7 +19,7 @@ FC_ALLGATHER, FC_REDUCE_SCATTER, FC_ALLREDUCE = 0, 1, 2
 FC_SUM = 0
 OPT_CTAS_PER_RANK, OPT_CHUNK_MAX, OPT_CHUNK_MIN, OPT_ITEMS_PER_WORKER, OPT_TIMEOUT_MS = 1, 2, 3, 4, 5
 OPT_LAG, OPT_COPY_MODE, OPT_DMA_ROOT_COPY, OPT_WORKER_WARPS = 6, 7, 8, 9
-OPT_PROTO, OPT_LL_MAX = 10, 11
+OPT_PROTO, OPT_LL_MAX, OPT_LL_CHUNK_MAX, OPT_LL_WORKER_WARPS = 10, 11, 12, 13
 OPTIONS = {
     "ctas_per_rank": OPT_CTAS_PER_RANK,
     "chunk_max": OPT_CHUNK_MAX,
@@ -32,6 +32,8 @@ OPTIONS = {
     "worker_warps": OPT_WORKER_WARPS,
     "proto": OPT_PROTO,
     "ll_max": OPT_LL_MAX,
+    "ll_chunk_max": OPT_LL_CHUNK_MAX,
+    "ll_worker_warps": OPT_LL_WORKER_WARPS,
 }
 
 # symbol -> (restype, argtypes)

@@ -74,7 +74,9 @@ struct fc_comm {
   int dma_root_copy = 0;
   int worker_warps = 8;
   int proto = -1;                  // -1 auto, 0 chunk flags, 1 LL128
-  long long ll_max = 64LL << 20;   // auto: LL128 when bytes moved per rank <= this
+  long long ll_chunk_max = 64 << 10;
+  int ll_worker_warps = 4;
+  long long ll_max = 512LL << 20;  // auto: LL128 when bytes moved per rank <= this (and staging fits)
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   FcTraceRec* trace = nullptr;
@@ -256,36 +258,23 @@ int run(fc_comm* c, int coll, const void* const* sends, void* const* recvs, size
   P.trace_count = c->trace_count;
   P.trace_cap = c->trace_cap;
 
-  // chunk plan: identical on every rank (depends on S, dtype, plan, options)
+  // Protocol and chunk plan: identical on every rank (they depend only on S,
+  // dtype, the plan and the options, which must match across ranks).
   const long long slice_unit = (S + pl.k - 1) / pl.k * es;  // bytes per unit of multiplicity
   const long long max_slice = slice_unit * pl.max_mult;
-  const long long workers = (long long)c->ctas_per_rank * (fc_warps_per_cta() / c->worker_warps);
   const long long avg_active = std::max(1LL, pl.active_total / N);
-  long long n = (max_slice + c->chunk_max - 1) / c->chunk_max;
-  n = std::max(n, (c->items_per_worker * workers + avg_active - 1) / avg_active);
-  n = std::min(n, std::max(1LL, max_slice / std::max(1LL, c->chunk_min)));
-  n = std::max(n, 1LL);
-  if (n > (1LL << 30)) n = 1LL << 30;
-  long long W = std::min<long long>(n, kMaxC);
-  auto unit_for = [&](long long w) {
-    return (long long)align_up((size_t)((slice_unit * w + n - 1) / n), FC_ALIGN);
+  auto chunks_for = [&](long long chunk_max, int ww) {
+    const long long workers = (long long)c->ctas_per_rank * (fc_warps_per_cta() / ww);
+    long long n = (max_slice + chunk_max - 1) / chunk_max;
+    n = std::max(n, (c->items_per_worker * workers + avg_active - 1) / avg_active);
+    n = std::min(n, std::max(1LL, max_slice / std::max(1LL, c->chunk_min)));
+    return std::min(std::max(n, 1LL), 1LL << 30);
   };
-  if (coll != FC_ALLGATHER) {
-    auto need = [&](long long w) {
-      return (long long)pl.max_slot_units * unit_for(w) + 2LL * FC_ALIGN * pl.max_slots;
-    };
-    while (W > 1 && need(W) > (long long)c->scratch_bytes) W = std::max(1LL, W / 2);
-    if (need(W) > (long long)c->scratch_bytes)
-      return fail(c, FC_ERR_INVALID_ARG,
-                  "scratch too small: %lld bytes needed per window, %zu available",
-                  need(W), c->scratch_bytes);
-    P.unit_bytes = unit_for(W);
-  }
-  P.nchunks = (int)n;
-  // LL128 for small/medium messages: one window, 8-byte aligned slices, and
-  // staging for every in-edge of the call fits in scratch
+  // LL128 (small/medium messages): single window, 8-byte aligned slices, and
+  // staging for every in-edge of the call fits in scratch.
   int proto = 0;
-  if (c->proto != 0 && n <= kMaxC) {
+  long long n = 0, W = 0;
+  if (c->proto != 0) {
     bool aligned = (stride * es) % 8 == 0;
     for (int i = 0; i < c->nlocal; ++i)
       aligned = aligned && ((uintptr_t)sends[i] % 8 == 0) && ((uintptr_t)recvs[i] % 8 == 0);
@@ -293,7 +282,7 @@ int run(fc_comm* c, int coll, const void* const* sends, void* const* recvs, size
       long long Sr = std::max(0LL, std::min(S, total - (long long)r * stride));
       for (int m = 0; m <= pl.k && aligned; ++m) aligned = ((Sr * m / pl.k) * es) % 8 == 0;
     }
-    const long long unit_lines = ((S + pl.k - 1) / pl.k * es + 119) / 120;
+    const long long unit_lines = (slice_unit + 119) / 120;
     const long long llu = unit_lines * 128;
     const long long rs_need = (long long)pl.max_slot_units * llu + 256LL * pl.max_slots;
     const long long ag_base = (rs_need + 255) / 256 * 256;
@@ -302,13 +291,34 @@ int run(fc_comm* c, int coll, const void* const* sends, void* const* recvs, size
     const bool want = c->proto == 1 || moved <= c->ll_max;
     if (aligned && want && need <= (long long)c->scratch_bytes) {
       proto = 1;
+      n = std::min<long long>(chunks_for(c->ll_chunk_max, c->ll_worker_warps), kMaxC);
       W = n;
       P.ll_unit_bytes = llu;
       P.ll_ag_base = ag_base;
+      P.worker_warps = c->ll_worker_warps;
     } else if (c->proto == 1) {
       return fail(c, FC_ERR_UNSUPPORTED, "LL protocol forced but not applicable (alignment/scratch)");
     }
   }
+  if (proto == 0) {
+    n = chunks_for(c->chunk_max, c->worker_warps);
+    W = std::min<long long>(n, kMaxC);
+    auto unit_for = [&](long long w) {
+      return (long long)align_up((size_t)((slice_unit * w + n - 1) / n), FC_ALIGN);
+    };
+    if (coll != FC_ALLGATHER) {
+      auto need = [&](long long w) {
+        return (long long)pl.max_slot_units * unit_for(w) + 2LL * FC_ALIGN * pl.max_slots;
+      };
+      while (W > 1 && need(W) > (long long)c->scratch_bytes) W = std::max(1LL, W / 2);
+      if (need(W) > (long long)c->scratch_bytes)
+        return fail(c, FC_ERR_INVALID_ARG,
+                    "scratch too small: %lld bytes needed per window, %zu available",
+                    need(W), c->scratch_bytes);
+      P.unit_bytes = unit_for(W);
+    }
+  }
+  P.nchunks = (int)n;
   P.proto = proto;
   const int coop = c->virt ? 1 : 0;
   int launches = 0, grid = 0;
@@ -376,8 +386,9 @@ int default_ctas(fc_comm* c) {
   FC_CUDA(c, cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));
   const int cap = per_sm * sms / c->nlocal;
   if (cap < 1) return fail(c, FC_ERR_UNSUPPORTED, "device cannot co-schedule %d ranks", c->nlocal);
-  c->ctas_per_rank = std::min(c->virt ? 16 : 96, cap);
-  c->worker_warps = c->virt ? 1 : 4;
+  c->ctas_per_rank = std::min(c->virt ? 16 : 128, cap);
+  c->worker_warps = c->virt ? 1 : 8;
+  c->ll_worker_warps = c->virt ? 1 : 4;
   return make_side_stream(c);
 }
 
@@ -533,6 +544,15 @@ int fc_comm_set_option(fc_comm_t* c, int option, long long v) {
       if (v < 0) return fail(c, FC_ERR_INVALID_ARG, "ll_max < 0");
       c->ll_max = v;
       return FC_SUCCESS;
+    case FC_OPT_LL_CHUNK_MAX:
+      if (v < 1024) return fail(c, FC_ERR_INVALID_ARG, "ll_chunk_max too small");
+      c->ll_chunk_max = v;
+      return FC_SUCCESS;
+    case FC_OPT_LL_WORKER_WARPS:
+      if (v != 1 && v != 2 && v != 4 && v != 8)
+        return fail(c, FC_ERR_INVALID_ARG, "ll_worker_warps must be 1, 2, 4 or 8");
+      c->ll_worker_warps = (int)v;
+      return FC_SUCCESS;
     default:
       return fail(c, FC_ERR_INVALID_ARG, "unknown option %d", option);
   }
@@ -552,6 +572,8 @@ int fc_comm_get_option(fc_comm_t* c, int option, long long* v) {
     case FC_OPT_WORKER_WARPS: *v = c->worker_warps; return FC_SUCCESS;
     case FC_OPT_PROTO: *v = c->proto; return FC_SUCCESS;
     case FC_OPT_LL_MAX: *v = c->ll_max; return FC_SUCCESS;
+    case FC_OPT_LL_CHUNK_MAX: *v = c->ll_chunk_max; return FC_SUCCESS;
+    case FC_OPT_LL_WORKER_WARPS: *v = c->ll_worker_warps; return FC_SUCCESS;
     default: return fail(c, FC_ERR_INVALID_ARG, "unknown option %d", option);
   }
 }

@@ -42,7 +42,8 @@ REDUCIBLE = {torch.int32, torch.float16, torch.float32, torch.bfloat16}
 if hasattr(torch, "uint32"):
     REDUCIBLE.add(torch.uint32)
 OPS = {"sum": 0}
-DEFAULT_SCRATCH = 1 << 30
+DEFAULT_SCRATCH = 2 << 30  # per rank: reduction scratch + LL128 staging
+VIRTUAL_SCRATCH = 1 << 30
 
 
 def _dtype_args(t: torch.Tensor, count: int):
@@ -344,7 +345,7 @@ class VirtualComm(_CommBase):
     multi-GPU path (SURVEY.md §4 "virtual ranks" mode).
     """
 
-    def __init__(self, topology=None, *, nranks=None, device=0, scratch_bytes=DEFAULT_SCRATCH,
+    def __init__(self, topology=None, *, nranks=None, device=0, scratch_bytes=VIRTUAL_SCRATCH,
                  schedules=None, validate=True, prune=True, options=None):
         doc = _as_doc(topology)
         if doc is None:

@@ -60,11 +60,13 @@ def main():
                     args.ww.split(","), args.proto.split(",")):
                 comm.set_option("proto", int(proto))
                 comm.set_option("worker_warps", int(ww))
+                comm.set_option("ll_worker_warps", int(ww))
                 comm.set_option("dma_root_copy", int(dma))
                 comm.set_option("lag", int(lag))
                 comm.set_option("copy_mode", int(mode))
                 comm.set_option("ctas_per_rank", int(ctas))
                 comm.set_option("chunk_max", int(ch))
+                comm.set_option("ll_chunk_max", int(ch))
                 comm.set_option("items_per_worker", int(ipw))
                 ms = timed(fn, 10, 3, dist)
                 info = comm.last_call_info()
