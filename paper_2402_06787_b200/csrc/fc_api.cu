@@ -386,9 +386,11 @@ int default_ctas(fc_comm* c) {
   FC_CUDA(c, cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));
   const int cap = per_sm * sms / c->nlocal;
   if (cap < 1) return fail(c, FC_ERR_UNSUPPORTED, "device cannot co-schedule %d ranks", c->nlocal);
-  c->ctas_per_rank = std::min(c->virt ? 16 : 128, cap);
+  c->ctas_per_rank = std::min(c->virt ? std::max(1, 128 / c->nlocal) : 128, cap);
   c->worker_warps = c->virt ? 1 : 8;
   c->ll_worker_warps = c->virt ? 1 : 4;
+  // virtual ranks share one HBM: LL staging doubles the traffic, so keep it for small calls
+  if (c->virt) c->ll_max = 16LL << 20;
   return make_side_stream(c);
 }
 
