@@ -46,6 +46,18 @@ def main():
     comm = ForestCollComm(topo, rank=rank, world_size=n, device=local,
                           options={"timeout_ms": 20000})
     fails = []
+    for proto in (-1, 0):  # auto (LL128 where aligned) and the chunk-flag protocol
+        comm.set_option("proto", proto)
+        fails += [f"proto={proto}: {f}" for f in run_all(comm, rank, n, dev)]
+    comm.check()
+    print(f"RANK {rank} {'OK' if not fails else 'FAIL ' + '; '.join(fails)}", flush=True)
+    comm.close()
+    dist.destroy_process_group()
+    sys.exit(1 if fails else 0)
+
+
+def run_all(comm, rank, n, dev):
+    fails = []
     # allgather: odd and aligned sizes, bit patterns
     for S in (1, 333, 4096, 1 << 20, (1 << 22) + 5):
         for seed in (10, 11):
@@ -89,11 +101,7 @@ def main():
         if not np.array_equal(got.view(np.uint8), ref.view(np.uint8)):
             fails.append(f"allgather repeat {it}")
             break
-    comm.check()
-    print(f"RANK {rank} {'OK' if not fails else 'FAIL ' + '; '.join(fails)}", flush=True)
-    comm.close()
-    dist.destroy_process_group()
-    sys.exit(1 if fails else 0)
+    return fails
 
 
 if __name__ == "__main__":

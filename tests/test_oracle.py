@@ -169,3 +169,19 @@ def test_allreduce_shard_rule():
     assert fo.allreduce_shard(1000, 8, 4) == 128
     assert fo.allreduce_shard(1, 8, 2) == 64
     assert fo.allreduce_shard(0, 8, 4) == 0
+
+
+@pytest.mark.parametrize("name", golden_names("allgather"))
+def test_c_oracle_matches_numpy_oracle(name):
+    from oracle import c_oracle
+
+    s = load_golden(name)
+    n = s.num_compute
+    rng = np.random.default_rng(11)
+    for S in (1, 5, 1000):
+        sends = [rng.integers(0, 2**32, S, dtype=np.uint64).astype(np.uint32) for _ in range(n)]
+        recvs = [np.zeros(n * S, dtype=np.uint32) for _ in range(n)]
+        c_oracle.allgather(c_oracle.FlatForest(s), sends, recvs, threads=4)
+        ref = fo.allgather(s, sends)
+        for a, b in zip(recvs, ref):
+            assert np.array_equal(a, b)
