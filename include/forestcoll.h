@@ -96,6 +96,7 @@ extern "C" {
 #define FC_OPT_LL_MAX 11       /* auto: LL128 when bytes per rank <= this (default 512 MiB) */
 #define FC_OPT_LL_CHUNK_MAX 12 /* max bytes per chunk, LL128 protocol (default 64 KiB) */
 #define FC_OPT_LL_WORKER_WARPS 13 /* warps per work item, LL128 (default 4 real, 1 virtual) */
+#define FC_OPT_NVLS_CTAS 14    /* CTAs of the NVLS (multicast) kernel (default 32) */
 
 typedef struct fc_comm fc_comm_t;
 
@@ -143,6 +144,24 @@ int fc_allreduce_multi(fc_comm_t* comm, const void* const* sends,
 
 /* statistics of the last collective call (launches, chunks, bytes) */
 int fc_last_call_info(const fc_comm_t* comm, long long* info, int ninfo);
+
+/* NVLS engine (NVSwitch multicast / in-switch aggregation) for forests whose
+ * switch hops are pruned (schedule.py:237-306).  Setup is collective:
+ * rank 0 fc_nvls_create -> pass the handle (its int32 at byte offset 4 is a
+ * POSIX fd: send it over a unix socket with SCM_RIGHTS and patch in the
+ * receiver's fd) -> every rank fc_nvls_attach -> barrier -> every rank
+ * fc_nvls_bind (returns the local base of a symmetric pool; buffers passed
+ * to fc_nvls_* must lie inside it). */
+int fc_nvls_supported(int device);
+int fc_nvls_create(fc_comm_t* comm, size_t bytes, void* handle);
+int fc_nvls_attach(fc_comm_t* comm, const void* handle);
+int fc_nvls_bind(fc_comm_t* comm, void** pool);
+int fc_nvls_allgather(fc_comm_t* comm, const void* send, void* recv,
+                      size_t sendcount, int dtype, void* stream);
+int fc_nvls_reduce_scatter(fc_comm_t* comm, const void* send, void* recv,
+                           size_t recvcount, int dtype, int op, void* stream);
+int fc_nvls_allreduce(fc_comm_t* comm, void* buf, size_t count, int dtype,
+                      int op, void* stream);
 
 /* item tracing: 40-byte records {u64 t_start, u64 t_end (ns, %globaltimer),
  * u32 t_wait (ns waiting on flags), u32 t_move (ns moving data), i32 chunk,

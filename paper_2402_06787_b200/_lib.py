@@ -19,7 +19,7 @@ FC_ALLGATHER, FC_REDUCE_SCATTER, FC_ALLREDUCE = 0, 1, 2
 FC_SUM = 0
 OPT_CTAS_PER_RANK, OPT_CHUNK_MAX, OPT_CHUNK_MIN, OPT_ITEMS_PER_WORKER, OPT_TIMEOUT_MS = 1, 2, 3, 4, 5
 OPT_LAG, OPT_COPY_MODE, OPT_DMA_ROOT_COPY, OPT_WORKER_WARPS = 6, 7, 8, 9
-OPT_PROTO, OPT_LL_MAX, OPT_LL_CHUNK_MAX, OPT_LL_WORKER_WARPS = 10, 11, 12, 13
+OPT_PROTO, OPT_LL_MAX, OPT_LL_CHUNK_MAX, OPT_LL_WORKER_WARPS, OPT_NVLS_CTAS = 10, 11, 12, 13, 14
 OPTIONS = {
     "ctas_per_rank": OPT_CTAS_PER_RANK,
     "chunk_max": OPT_CHUNK_MAX,
@@ -34,6 +34,7 @@ OPTIONS = {
     "ll_max": OPT_LL_MAX,
     "ll_chunk_max": OPT_LL_CHUNK_MAX,
     "ll_worker_warps": OPT_LL_WORKER_WARPS,
+    "nvls_ctas": OPT_NVLS_CTAS,
 }
 
 # symbol -> (restype, argtypes)
@@ -65,6 +66,13 @@ SIGNATURES = {
     "fc_allreduce_multi": (_I, [_P, _P, _P, _SZ, _I, _I, _P]),
     "fc_last_call_info": (_I, [_P, ctypes.POINTER(_LL), _I]),
     "fc_comm_set_trace": (_I, [_P, _P, _P, ctypes.c_uint]),
+    "fc_nvls_supported": (_I, [_I]),
+    "fc_nvls_create": (_I, [_P, _SZ, _P]),
+    "fc_nvls_attach": (_I, [_P, _P]),
+    "fc_nvls_bind": (_I, [_P, ctypes.POINTER(_P)]),
+    "fc_nvls_allgather": (_I, [_P, _P, _P, _SZ, _I, _P]),
+    "fc_nvls_reduce_scatter": (_I, [_P, _P, _P, _SZ, _I, _I, _P]),
+    "fc_nvls_allreduce": (_I, [_P, _P, _SZ, _I, _I, _P]),
 }
 
 _LIB = []

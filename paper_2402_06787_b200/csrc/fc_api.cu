@@ -78,6 +78,13 @@ struct fc_comm {
   int ll_worker_warps = 4;
   long long ll_max = 512LL << 20;  // auto: LL128 when bytes moved per rank <= this (and staging fits)
   cudaStream_t side = nullptr;
+  // NVLS pool (multicast object bound to a per-rank physical allocation)
+  unsigned long long nvls_mc = 0, nvls_mem = 0;
+  char* nvls_mc_va = nullptr;
+  char* nvls_uc_va = nullptr;
+  size_t nvls_bytes = 0;
+  int nvls_bound = 0;
+  int nvls_ctas = 32;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   FcTraceRec* trace = nullptr;
   unsigned* trace_count = nullptr;
@@ -135,7 +142,8 @@ int alloc_workspace(fc_comm* c, char** out) {
 
 int setup_layout(fc_comm* c, size_t scratch_bytes) {
   c->flags_off = kCtlBytes;
-  c->flags_words = FC_READY_WORDS + kTreeCap + (size_t)(kTreeCap + kSlotCap) * kMaxC;
+  c->flags_words = FC_READY_WORDS + kTreeCap + (size_t)(kTreeCap + kSlotCap) * kMaxC +
+                   2 * FC_MAXR;  // + NVLS entry/exit barrier words
   c->scratch_off = align_up(c->flags_off + c->flags_words * 4, 4096);
   c->scratch_bytes = align_up(scratch_bytes, 4096);
   c->ws_bytes = c->scratch_off + c->scratch_bytes;
@@ -394,6 +402,129 @@ int default_ctas(fc_comm* c) {
   return make_side_stream(c);
 }
 
+// -- driver entry points (no -lcuda: resolved through the runtime) ---------
+struct Drv {
+  CUresult (*getDevice)(CUdevice*, int);
+  CUresult (*getAttr)(int*, CUdevice_attribute, CUdevice);
+  CUresult (*mcCreate)(CUmemGenericAllocationHandle*, const CUmulticastObjectProp*);
+  CUresult (*mcAddDevice)(CUmemGenericAllocationHandle, CUdevice);
+  CUresult (*mcBindMem)(CUmemGenericAllocationHandle, size_t, CUmemGenericAllocationHandle, size_t,
+                        size_t, unsigned long long);
+  CUresult (*mcUnbind)(CUmemGenericAllocationHandle, CUdevice, size_t, size_t);
+  CUresult (*mcGranularity)(size_t*, const CUmulticastObjectProp*, CUmulticastGranularity_flags);
+  CUresult (*exportHandle)(void*, CUmemGenericAllocationHandle, CUmemAllocationHandleType,
+                           unsigned long long);
+  CUresult (*importHandle)(CUmemGenericAllocationHandle*, void*, CUmemAllocationHandleType);
+  CUresult (*memCreate)(CUmemGenericAllocationHandle*, size_t, const CUmemAllocationProp*,
+                        unsigned long long);
+  CUresult (*addrReserve)(CUdeviceptr*, size_t, size_t, CUdeviceptr, unsigned long long);
+  CUresult (*memMap)(CUdeviceptr, size_t, size_t, CUmemGenericAllocationHandle, unsigned long long);
+  CUresult (*setAccess)(CUdeviceptr, size_t, const CUmemAccessDesc*, size_t);
+  CUresult (*memUnmap)(CUdeviceptr, size_t);
+  CUresult (*memRelease)(CUmemGenericAllocationHandle);
+  CUresult (*addrFree)(CUdeviceptr, size_t);
+  bool ok = false;
+};
+
+const Drv& drv() {
+  static Drv d;
+  static bool tried = false;
+  if (tried) return d;
+  tried = true;
+  auto get = [](const char* name, void** fn) {
+    cudaDriverEntryPointQueryResult q;
+    return cudaGetDriverEntryPoint(name, fn, cudaEnableDefault, &q) == cudaSuccess &&
+           q == cudaDriverEntryPointSuccess;
+  };
+  d.ok = get("cuDeviceGet", (void**)&d.getDevice) &&
+         get("cuDeviceGetAttribute", (void**)&d.getAttr) &&
+         get("cuMulticastCreate", (void**)&d.mcCreate) &&
+         get("cuMulticastAddDevice", (void**)&d.mcAddDevice) &&
+         get("cuMulticastBindMem", (void**)&d.mcBindMem) &&
+         get("cuMulticastUnbind", (void**)&d.mcUnbind) &&
+         get("cuMulticastGetGranularity", (void**)&d.mcGranularity) &&
+         get("cuMemExportToShareableHandle", (void**)&d.exportHandle) &&
+         get("cuMemImportFromShareableHandle", (void**)&d.importHandle) &&
+         get("cuMemCreate", (void**)&d.memCreate) &&
+         get("cuMemAddressReserve", (void**)&d.addrReserve) && get("cuMemMap", (void**)&d.memMap) &&
+         get("cuMemSetAccess", (void**)&d.setAccess) && get("cuMemUnmap", (void**)&d.memUnmap) &&
+         get("cuMemRelease", (void**)&d.memRelease) && get("cuMemAddressFree", (void**)&d.addrFree);
+  return d;
+}
+
+#define FC_DRV(c, call)                                                              \
+  do {                                                                               \
+    CUresult r_ = (call);                                                            \
+    if (r_ != CUDA_SUCCESS) return fail((c), FC_ERR_CUDA, "%s failed (CUresult %d)", #call, (int)r_); \
+  } while (0)
+
+struct NvlsBlob {
+  uint32_t magic;
+  int32_t fd;  // POSIX file descriptor of the multicast object (valid in the holder)
+  uint64_t bytes;
+};
+constexpr uint32_t kNvlsMagic = 0x534c564e;  // 'NVLS'
+static_assert(sizeof(NvlsBlob) <= kHandleBytes, "nvls blob size");
+
+CUmulticastObjectProp mc_prop(fc_comm* c, size_t bytes) {
+  CUmulticastObjectProp prop;
+  memset(&prop, 0, sizeof(prop));
+  prop.numDevices = (unsigned)c->nranks;
+  prop.size = bytes;
+  prop.handleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
+  return prop;
+}
+
+int run_nvls(fc_comm* c, int mode, const void* send, void* buf, void* out, size_t count, int dtype,
+             void* stream) {
+  if (!c || !c->nvls_bound) return fail(c, FC_ERR_INVALID_ARG, "NVLS pool is not set up");
+  const int es = esize_of(dtype);
+  if (!es) return fail(c, FC_ERR_INVALID_ARG, "unknown dtype %d", dtype);
+  int rd = FC_FLOAT32;
+  if (mode != 0) {
+    rd = reduce_kind(dtype);
+    if (rd < 0) return fail(c, FC_ERR_UNSUPPORTED, "dtype %d cannot be reduced", dtype);
+  }
+  const uintptr_t b = (uintptr_t)buf, lo = (uintptr_t)c->nvls_uc_va;
+  const int N = c->nranks;
+  long long shard, total;
+  if (mode == 2) {
+    const long long a = FC_ALIGN / es;
+    long long S = ((long long)count + N - 1) / N;
+    S = (S + a - 1) / a * a;
+    shard = S * es;
+    total = (long long)count * es;
+  } else {
+    shard = (long long)count * es;
+    total = shard * N;
+  }
+  if (total == 0) return FC_SUCCESS;
+  if (b < lo || b + (size_t)total > lo + c->nvls_bytes)
+    return fail(c, FC_ERR_NOT_REGISTERED, "buffer %p is not inside the NVLS pool", buf);
+  if ((b - lo) % 16 || shard % 16 || total % 16)
+    return fail(c, FC_ERR_UNSUPPORTED, "NVLS needs 16-byte aligned shards");
+  FcNvlsParams P;
+  memset(&P, 0, sizeof(P));
+  P.nranks = N;
+  P.rank = c->rank;
+  P.mode = mode;
+  P.dtype = rd;
+  P.bar_off = (int)(c->flags_words - 2 * FC_MAXR);
+  P.ctl = (FcCtl*)c->ws[c->rank];
+  for (int r = 0; r < N; ++r) P.flags[r] = (unsigned*)(c->ws[r] + c->flags_off);
+  P.mc = c->nvls_mc_va + (b - lo);
+  P.send = (const char*)send;
+  P.out = (char*)out;
+  P.shard_bytes = shard;
+  P.total_bytes = total;
+  P.timeout_ns = c->timeout_ms * 1000000LL;
+  const int e = fc_nvls_launch(P, c->nvls_ctas, stream);
+  if (e) return fail(c, FC_ERR_CUDA, "NVLS launch failed: %s", cudaGetErrorString((cudaError_t)e));
+  c->info[0] = 1;
+  c->info[5] = 2;  // engine: nvls
+  return FC_SUCCESS;
+}
+
 }  // namespace
 
 extern "C" {
@@ -546,6 +677,10 @@ int fc_comm_set_option(fc_comm_t* c, int option, long long v) {
       if (v < 0) return fail(c, FC_ERR_INVALID_ARG, "ll_max < 0");
       c->ll_max = v;
       return FC_SUCCESS;
+    case FC_OPT_NVLS_CTAS:
+      if (v < 1 || v > 1024) return fail(c, FC_ERR_INVALID_ARG, "nvls_ctas out of range");
+      c->nvls_ctas = (int)v;
+      return FC_SUCCESS;
     case FC_OPT_LL_CHUNK_MAX:
       if (v < 1024) return fail(c, FC_ERR_INVALID_ARG, "ll_chunk_max too small");
       c->ll_chunk_max = v;
@@ -575,6 +710,7 @@ int fc_comm_get_option(fc_comm_t* c, int option, long long* v) {
     case FC_OPT_PROTO: *v = c->proto; return FC_SUCCESS;
     case FC_OPT_LL_MAX: *v = c->ll_max; return FC_SUCCESS;
     case FC_OPT_LL_CHUNK_MAX: *v = c->ll_chunk_max; return FC_SUCCESS;
+    case FC_OPT_NVLS_CTAS: *v = c->nvls_ctas; return FC_SUCCESS;
     case FC_OPT_LL_WORKER_WARPS: *v = c->ll_worker_warps; return FC_SUCCESS;
     default: return fail(c, FC_ERR_INVALID_ARG, "unknown option %d", option);
   }
@@ -605,6 +741,17 @@ int fc_comm_destroy(fc_comm_t* c) {
   cudaDeviceSynchronize();
   for (auto& p : c->plans) free_plan(c, p);
   for (auto& m : c->maps) cudaIpcCloseMemHandle(m.base);
+  if (c->nvls_bound) {
+    const Drv& d = drv();
+    d.memUnmap((CUdeviceptr)c->nvls_mc_va, c->nvls_bytes);
+    d.addrFree((CUdeviceptr)c->nvls_mc_va, c->nvls_bytes);
+    d.memUnmap((CUdeviceptr)c->nvls_uc_va, c->nvls_bytes);
+    d.addrFree((CUdeviceptr)c->nvls_uc_va, c->nvls_bytes);
+    CUdevice dev;
+    if (d.getDevice(&dev, c->device) == CUDA_SUCCESS) d.mcUnbind(c->nvls_mc, dev, 0, c->nvls_bytes);
+    d.memRelease(c->nvls_mem);
+  }
+  if (c->nvls_mc) drv().memRelease(c->nvls_mc);
   if (c->side) cudaStreamDestroy(c->side);
   if (c->ev_fork) cudaEventDestroy(c->ev_fork);
   if (c->ev_join) cudaEventDestroy(c->ev_join);
@@ -806,6 +953,114 @@ int fc_last_call_info(const fc_comm_t* c, long long* info, int ninfo) {
   if (!c || !info) return FC_ERR_INVALID_ARG;
   for (int i = 0; i < ninfo && i < 8; ++i) info[i] = c->info[i];
   return FC_SUCCESS;
+}
+
+int fc_nvls_supported(int device) {
+  const Drv& d = drv();
+  if (!d.ok) return 0;
+  CUdevice dev;
+  int v = 0;
+  if (d.getDevice(&dev, device) != CUDA_SUCCESS) return 0;
+  if (d.getAttr(&v, CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED, dev) != CUDA_SUCCESS) return 0;
+  return v;
+}
+
+int fc_nvls_create(fc_comm_t* c, size_t bytes, void* handle) {
+  if (!c || !handle || c->virt) return FC_ERR_INVALID_ARG;
+  const Drv& d = drv();
+  if (!d.ok) return fail(c, FC_ERR_UNSUPPORTED, "driver multicast entry points unavailable");
+  FC_CUDA(c, cudaSetDevice(c->device));
+  CUmulticastObjectProp prop = mc_prop(c, bytes);
+  size_t gran = 0;
+  FC_DRV(c, d.mcGranularity(&gran, &prop, CU_MULTICAST_GRANULARITY_RECOMMENDED));
+  bytes = (bytes + gran - 1) / gran * gran;
+  prop.size = bytes;
+  CUmemGenericAllocationHandle mc;
+  FC_DRV(c, d.mcCreate(&mc, &prop));
+  NvlsBlob blob;
+  memset(&blob, 0, sizeof(blob));
+  blob.magic = kNvlsMagic;
+  blob.bytes = bytes;
+  int fd = -1;
+  FC_DRV(c, d.exportHandle(&fd, mc, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR, 0));
+  blob.fd = fd;
+  c->nvls_mc = mc;
+  c->nvls_bytes = bytes;
+  memset(handle, 0, kHandleBytes);
+  memcpy(handle, &blob, sizeof(blob));
+  return FC_SUCCESS;
+}
+
+int fc_nvls_attach(fc_comm_t* c, const void* handle) {
+  if (!c || !handle || c->virt) return FC_ERR_INVALID_ARG;
+  const Drv& d = drv();
+  if (!d.ok) return fail(c, FC_ERR_UNSUPPORTED, "driver multicast entry points unavailable");
+  FC_CUDA(c, cudaSetDevice(c->device));
+  NvlsBlob blob;
+  memcpy(&blob, handle, sizeof(blob));
+  if (blob.magic != kNvlsMagic) return fail(c, FC_ERR_INVALID_ARG, "bad NVLS handle");
+  if (!c->nvls_mc) {
+    CUmemGenericAllocationHandle mc;
+    FC_DRV(c, d.importHandle(&mc, (void*)(uintptr_t)blob.fd,
+                             CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR));
+    c->nvls_mc = mc;
+    c->nvls_bytes = blob.bytes;
+  }
+  CUdevice dev;
+  FC_DRV(c, d.getDevice(&dev, c->device));
+  FC_DRV(c, d.mcAddDevice(c->nvls_mc, dev));
+  return FC_SUCCESS;
+}
+
+// After every rank attached (caller barrier): bind local memory, map the
+// multicast and unicast views.  Returns the unicast base (the pool).
+int fc_nvls_bind(fc_comm_t* c, void** pool) {
+  if (!c || !pool || !c->nvls_mc) return FC_ERR_INVALID_ARG;
+  const Drv& d = drv();
+  FC_CUDA(c, cudaSetDevice(c->device));
+  CUmemAllocationProp ap;
+  memset(&ap, 0, sizeof(ap));
+  ap.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+  ap.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  ap.location.id = c->device;
+  ap.requestedHandleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
+  CUmemGenericAllocationHandle mem;
+  FC_DRV(c, d.memCreate(&mem, c->nvls_bytes, &ap, 0));
+  c->nvls_mem = mem;
+  FC_DRV(c, d.mcBindMem(c->nvls_mc, 0, mem, 0, c->nvls_bytes, 0));
+  CUmemAccessDesc acc;
+  memset(&acc, 0, sizeof(acc));
+  acc.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  acc.location.id = c->device;
+  acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+  CUdeviceptr uc = 0, mcva = 0;
+  FC_DRV(c, d.addrReserve(&uc, c->nvls_bytes, 0, 0, 0));
+  FC_DRV(c, d.memMap(uc, c->nvls_bytes, 0, mem, 0));
+  FC_DRV(c, d.setAccess(uc, c->nvls_bytes, &acc, 1));
+  FC_DRV(c, d.addrReserve(&mcva, c->nvls_bytes, 0, 0, 0));
+  FC_DRV(c, d.memMap(mcva, c->nvls_bytes, 0, c->nvls_mc, 0));
+  FC_DRV(c, d.setAccess(mcva, c->nvls_bytes, &acc, 1));
+  c->nvls_uc_va = (char*)uc;
+  c->nvls_mc_va = (char*)mcva;
+  FC_CUDA(c, cudaMemset(c->nvls_uc_va, 0, c->nvls_bytes));
+  FC_CUDA(c, cudaDeviceSynchronize());
+  c->nvls_bound = 1;
+  *pool = c->nvls_uc_va;
+  return FC_SUCCESS;
+}
+
+int fc_nvls_allgather(fc_comm_t* c, const void* send, void* recv, size_t sendcount, int dtype,
+                      void* stream) {
+  return run_nvls(c, 0, send, recv, nullptr, sendcount, dtype, stream);
+}
+int fc_nvls_reduce_scatter(fc_comm_t* c, const void* send, void* recv, size_t recvcount,
+                           int dtype, int op, void* stream) {
+  if (op != FC_SUM) return fail(c, FC_ERR_UNSUPPORTED, "reduction op %d unsupported", op);
+  return run_nvls(c, 1, nullptr, (void*)send, recv, recvcount, dtype, stream);
+}
+int fc_nvls_allreduce(fc_comm_t* c, void* buf, size_t count, int dtype, int op, void* stream) {
+  if (op != FC_SUM) return fail(c, FC_ERR_UNSUPPORTED, "reduction op %d unsupported", op);
+  return run_nvls(c, 2, nullptr, buf, nullptr, count, dtype, stream);
 }
 
 }  // extern "C"

@@ -136,8 +136,25 @@ struct FcParams {
   unsigned trace_cap;
 };
 
+// NVLS (NVSwitch multicast) engine: executes a ForestColl forest whose
+// NVSwitch hops are pruned for multicast / in-switch aggregation
+// (schedule.py:237-306): every root writes its shard once into the switch.
+struct FcNvlsParams {
+  int nranks, rank, mode, dtype;  // mode: 0 allgather, 1 reduce-scatter, 2 allreduce
+  int bar_off;                    // word offset of the NVLS barrier words (2 * FC_MAXR)
+  FcCtl* ctl;
+  unsigned int* flags[FC_MAXR];
+  char* mc;                       // multicast VA of the pool (+ buffer offset)
+  const char* send;               // allgather source (any device buffer)
+  char* out;                      // reduce-scatter destination (any device buffer)
+  long long shard_bytes;          // bytes per root shard
+  long long total_bytes;          // bytes of the N-shard buffer in the pool
+  long long timeout_ns;
+};
+
 // Kernel entry (fc_kernel.cu).  Returns a cudaError_t value.
 int fc_launch(const FcParams& p, int reduce_dtype, int cooperative,
               void* stream, int* grid_out);
 int fc_max_ctas_per_sm(int reduce_dtype, int* out);
 int fc_warps_per_cta();
+int fc_nvls_launch(const FcNvlsParams& p, int ctas, void* stream);

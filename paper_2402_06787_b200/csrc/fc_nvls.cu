@@ -1,0 +1,176 @@
+// NVLS engine: the ForestColl forest on one multicast/aggregation-capable
+// NVSwitch, executed with multimem instructions.
+//
+// With the switch flagged multicast/aggregation, the reference prunes every
+// tree down to one send per root into the switch (prune_multicast /
+// prune_aggregation, pkg/src/collsched/schedule.py:237-306; "each GPU then
+// sends 1 unit into nvs instead of 7").  Executing the
+// pruned forest therefore means:
+//   allgather:      root r stores shard r once to the multicast address
+//                   (multimem.st) and the switch replicates it to every GPU;
+//   reduce-scatter: root r reads shard r once through the switch with
+//                   in-network aggregation (multimem.ld_reduce);
+//   allreduce:      both, on the same shard.
+// Buffers live in a symmetric pool bound to a CUDA multicast object.
+// In-switch fp reductions use the switch's accumulation order (fp32
+// accumulate for bf16/fp16), so fp results match the tree oracle only within
+// tolerance; int32 sums are exact.
+#include <cuda_runtime.h>
+
+#include <climits>
+#include <cstdint>
+
+#include "fc_internal.h"
+
+#define FC_NVLS_THREADS 512
+
+namespace {
+
+__device__ __forceinline__ unsigned ld_acquire_sys(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned* p, unsigned v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ bool wait_peers(const FcNvlsParams& P, int base, unsigned e) {
+  const unsigned* f = P.flags[P.rank] + P.bar_off + base;
+  const unsigned long long t0 = globaltimer();
+  for (int p = 0; p < P.nranks; ++p) {
+    if (p == P.rank) continue;
+    while ((int)(ld_acquire_sys(f + p) - e) < 0) {
+      if ((long long)(globaltimer() - t0) > P.timeout_ns) {
+        atomicCAS(&P.ctl->error, 0u, (unsigned)FC_DEVERR_TIMEOUT_READY);
+        return false;
+      }
+    }
+  }
+  return true;
+}
+
+__device__ __forceinline__ void mm_st(char* p, const uint4& v) {
+  asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p),
+               "f"(__uint_as_float(v.x)), "f"(__uint_as_float(v.y)), "f"(__uint_as_float(v.z)),
+               "f"(__uint_as_float(v.w))
+               : "memory");
+}
+
+template <int DT>
+__device__ __forceinline__ uint4 mm_ld_reduce(const char* p) {
+  uint4 r;
+  if constexpr (DT == FC_FLOAT32) {
+    float a, b, c, d;
+    asm volatile("multimem.ld_reduce.relaxed.sys.global.add.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(a), "=f"(b), "=f"(c), "=f"(d)
+                 : "l"(p)
+                 : "memory");
+    r = make_uint4(__float_as_uint(a), __float_as_uint(b), __float_as_uint(c), __float_as_uint(d));
+  } else if constexpr (DT == FC_BFLOAT16) {
+    asm volatile("multimem.ld_reduce.relaxed.sys.global.add.acc::f32.v4.bf16x2 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p)
+                 : "memory");
+  } else if constexpr (DT == FC_FLOAT16) {
+    asm volatile("multimem.ld_reduce.relaxed.sys.global.add.acc::f32.v4.f16x2 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p)
+                 : "memory");
+  } else {  // int32 / uint32: wrapping add, scalar multimem ops
+    const unsigned* q = reinterpret_cast<const unsigned*>(p);
+    unsigned v[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      asm volatile("multimem.ld_reduce.relaxed.sys.global.add.u32 %0, [%1];"
+                   : "=r"(v[i])
+                   : "l"(q + i)
+                   : "memory");
+    r = make_uint4(v[0], v[1], v[2], v[3]);
+  }
+  return r;
+}
+
+template <int DT>
+__global__ void __launch_bounds__(FC_NVLS_THREADS) fc_nvls_kernel(const __grid_constant__ FcNvlsParams P) {
+  __shared__ unsigned s_e;
+  __shared__ int s_ok;
+  FcCtl* ctl = P.ctl;
+  if (threadIdx.x == 0) {
+    s_e = *reinterpret_cast<volatile unsigned*>(&ctl->epoch) + 1;
+  }
+  __syncthreads();
+  const unsigned e = s_e;
+  // entry barrier: peers' inputs are ready and their outputs may be written
+  if (blockIdx.x == 0 && (int)threadIdx.x < P.nranks && (int)threadIdx.x != P.rank)
+    st_release_sys(P.flags[threadIdx.x] + P.bar_off + P.rank, e);
+  if (threadIdx.x == 0) s_ok = wait_peers(P, 0, e) ? 1 : 0;
+  __syncthreads();
+  if (s_ok) {
+    const long long r0 = (long long)P.rank * P.shard_bytes;
+    long long len = P.total_bytes - r0;
+    len = len < 0 ? 0 : (len > P.shard_bytes ? P.shard_bytes : len);
+    const long long nv = len / 16;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    constexpr int U = 4;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += stride * U) {
+      uint4 v[U];
+      if (P.mode == 0) {
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (i + u * stride < nv) v[u] = __ldcg(reinterpret_cast<const uint4*>(P.send) + i + u * stride);
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (i + u * stride < nv) mm_st(P.mc + r0 + 16 * (i + u * stride), v[u]);
+      } else {
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (i + u * stride < nv) v[u] = mm_ld_reduce<DT>(P.mc + r0 + 16 * (i + u * stride));
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          if (i + u * stride >= nv) continue;
+          if (P.mode == 1)
+            reinterpret_cast<uint4*>(P.out)[i + u * stride] = v[u];
+          else
+            mm_st(P.mc + r0 + 16 * (i + u * stride), v[u]);
+        }
+      }
+    }
+  }
+  asm volatile("fence.proxy.alias;" ::: "memory");
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned prev = atomicAdd(&ctl->done, 1u);
+    if (prev == gridDim.x - 1) {
+      // exit barrier: every peer finished writing into / reading from this GPU
+      for (int t = 0; t < P.nranks; ++t)
+        if (t != P.rank) st_release_sys(P.flags[t] + P.bar_off + FC_MAXR + P.rank, e);
+      wait_peers(P, FC_MAXR, e);
+      asm volatile("fence.proxy.alias;" ::: "memory");
+      ctl->done = 0;
+      __threadfence();
+      atomicExch(&ctl->epoch, e);
+    }
+  }
+}
+
+}  // namespace
+
+int fc_nvls_launch(const FcNvlsParams& p, int ctas, void* stream) {
+  void* args[] = {(void*)&p};
+  const void* fn;
+  switch (p.dtype) {
+    case FC_BFLOAT16: fn = (const void*)fc_nvls_kernel<FC_BFLOAT16>; break;
+    case FC_FLOAT16: fn = (const void*)fc_nvls_kernel<FC_FLOAT16>; break;
+    case FC_INT32: fn = (const void*)fc_nvls_kernel<FC_INT32>; break;
+    default: fn = (const void*)fc_nvls_kernel<FC_FLOAT32>; break;
+  }
+  return (int)cudaLaunchKernel(fn, dim3(ctas), dim3(FC_NVLS_THREADS), args, 0,
+                               (cudaStream_t)stream);
+}

@@ -153,7 +153,7 @@ class _CommBase:
         buf = (ctypes.c_longlong * 8)()
         self._lib.fc_last_call_info(self._comm, buf, 8)
         return {"launches": buf[0], "nchunks": buf[1], "window": buf[2], "grid": buf[3],
-                "unit_bytes": buf[4], "proto": "ll128" if buf[5] else "flags"}
+                "unit_bytes": buf[4], "proto": {0: "flags", 1: "ll128", 2: "nvls"}[buf[5]]}
 
     # -- tracing ------------------------------------------------------------
     TRACE_DTYPE = np.dtype([("t_start", "<u8"), ("t_end", "<u8"), ("t_wait", "<u4"),
@@ -211,7 +211,7 @@ class ForestCollComm(_CommBase):
 
     def __init__(self, topology=None, *, rank=None, world_size=None, device=None, group=None,
                  scratch_bytes=DEFAULT_SCRATCH, schedules=None, validate=True, prune=True,
-                 options=None):
+                 options=None, nvls_bytes=0):
         import torch.distributed as dist
 
         if rank is None or world_size is None:
@@ -247,6 +247,100 @@ class ForestCollComm(_CommBase):
             blob = ctypes.create_string_buffer(b"".join(allh), hb * world_size)
             _lib.check(self._lib.fc_comm_connect(self._comm, blob), self._comm, "comm_connect")
         self._registered = {}
+        self._nvls_base = None
+        self._nvls_bytes = 0
+        self._nvls_next = 0
+        if nvls_bytes and world_size > 1:
+            self._setup_nvls(int(nvls_bytes))
+
+    # -- NVLS (multicast) engine ----------------------------------------------
+    def _setup_nvls(self, nbytes):
+        """Collective: bind a symmetric pool to an NVSwitch multicast object.
+        Every rank must call with the same size; falls back (pool disabled) on
+        all ranks together when any rank lacks multicast support."""
+        import torch.distributed as dist
+
+        ok = bool(self._lib.fc_nvls_supported(self.device))
+        if not all(self._allgather_obj(ok)):
+            return
+        import socket
+        import struct
+        import uuid
+
+        hb = self._lib.fc_handle_bytes()
+        blob = ctypes.create_string_buffer(hb)
+        srv = None
+        if self.rank == 0:
+            _lib.check(self._lib.fc_nvls_create(self._comm, nbytes, blob), self._comm, "nvls_create")
+            addr = f"\0forestcoll-nvls-{uuid.uuid4().hex}"
+            srv = socket.socket(socket.AF_UNIX, socket.SOCK_STREAM)
+            srv.bind(addr)
+            srv.listen(self.nranks)
+        else:
+            addr = None
+        blob0, addr = self._allgather_obj((blob.raw, addr))[0]
+        h = ctypes.create_string_buffer(blob0, hb)
+        # the multicast object travels as a POSIX fd (SCM_RIGHTS over a unix socket)
+        if self.rank == 0:
+            fd = struct.unpack_from("<i", blob0, 4)[0]
+            for _ in range(self.nranks - 1):
+                conn, _ = srv.accept()
+                socket.send_fds(conn, [b"f"], [fd])
+                conn.close()
+            srv.close()
+        else:
+            cli = socket.socket(socket.AF_UNIX, socket.SOCK_STREAM)
+            cli.connect(addr)
+            _, fds, _, _ = socket.recv_fds(cli, 1, 1)
+            cli.close()
+            struct.pack_into("<i", h, 4, fds[0])
+        _lib.check(self._lib.fc_nvls_attach(self._comm, h), self._comm, "nvls_attach")
+        dist.barrier(group=self._group)
+        base = ctypes.c_void_p()
+        _lib.check(self._lib.fc_nvls_bind(self._comm, ctypes.byref(base)), self._comm, "nvls_bind")
+        dist.barrier(group=self._group)
+        self._nvls_base = base.value
+        self._nvls_bytes = nbytes
+
+    @property
+    def nvls_enabled(self) -> bool:
+        return self._nvls_base is not None
+
+    def nvls_empty(self, numel: int, dtype=torch.float32) -> torch.Tensor:
+        """A tensor in the symmetric NVLS pool (bump-allocated: every rank must
+        allocate the same sequence of sizes).  Valid while the comm lives."""
+        if not self.nvls_enabled:
+            raise Unsupported("NVLS pool is not set up (nvls_bytes=0 or no multicast support)")
+        es = torch.tensor([], dtype=dtype).element_size()
+        off = (self._nvls_next + 4095) // 4096 * 4096
+        if off + numel * es > self._nvls_bytes:
+            raise InvalidArgument("NVLS pool exhausted")
+        self._nvls_next = off + numel * es
+        typestr = {1: "|u1", 2: "<i2", 4: "<i4", 8: "<i8"}[es]
+
+        class _CAI:
+            pass
+
+        holder = _CAI()
+        holder.__cuda_array_interface__ = {"shape": (numel,), "typestr": typestr,
+                                           "data": (self._nvls_base + off, False), "version": 3}
+        t = torch.as_tensor(holder, device=f"cuda:{self.device}")
+        return t.view(dtype)
+
+    def _in_pool(self, t) -> bool:
+        if not self.nvls_enabled:
+            return False
+        a = t.data_ptr()
+        return self._nvls_base <= a and a + t.numel() * t.element_size() <= self._nvls_base + self._nvls_bytes
+
+    def _switch_capable(self, capability: str) -> bool:
+        """The topology routes every pair through one switch that declares
+        `capability` (multicast / aggregation): the pruned forest then sends
+        each shard into the switch once (schedule.py:237-306)."""
+        if self.topology is None:
+            return False
+        sws = [n for n in self.topology["nodes"] if n["kind"] == "switch"]
+        return len(sws) == 1 and bool(sws[0].get(capability, False))
 
     def _allgather_obj(self, obj):
         import torch.distributed as dist
@@ -295,9 +389,15 @@ class ForestCollComm(_CommBase):
         self._check_tensor(out, self.device, "output")
         if out.dtype != inp.dtype or out.numel() != inp.numel() * self.nranks:
             raise InvalidArgument("output must hold world_size x input elements of the same dtype")
+        count, code = _dtype_args(inp, inp.numel())
+        if self._in_pool(out) and self._switch_capable("multicast"):
+            self.schedule(ALLGATHER)
+            _lib.check(self._lib.fc_nvls_allgather(self._comm, inp.data_ptr(), out.data_ptr(),
+                                                   count, code, self._stream()),
+                       self._comm, "nvls_allgather")
+            return out
         self.plan(ALLGATHER)
         self.register(out)
-        count, code = _dtype_args(inp, inp.numel())
         _lib.check(self._lib.fc_allgather(self._comm, inp.data_ptr(), out.data_ptr(), count, code,
                                           self._stream()), self._comm, "allgather")
         return out
@@ -312,6 +412,12 @@ class ForestCollComm(_CommBase):
             raise InvalidArgument("input must hold world_size x output elements of the same dtype")
         if inp.dtype not in REDUCIBLE:
             raise Unsupported(f"dtype {inp.dtype} cannot be reduced")
+        if self._in_pool(inp) and self._switch_capable("aggregation"):
+            self.schedule(REDUCE_SCATTER)
+            _lib.check(self._lib.fc_nvls_reduce_scatter(
+                self._comm, inp.data_ptr(), out.data_ptr(), out.numel(), DTYPE_CODE[inp.dtype],
+                _op_code(op), self._stream()), self._comm, "nvls_reduce_scatter")
+            return out
         self.plan(REDUCE_SCATTER)
         _lib.check(self._lib.fc_reduce_scatter(self._comm, inp.data_ptr(), out.data_ptr(),
                                                out.numel(), DTYPE_CODE[inp.dtype], _op_code(op),
@@ -329,6 +435,13 @@ class ForestCollComm(_CommBase):
             raise InvalidArgument("output must match the buffer")
         if buf.dtype not in REDUCIBLE:
             raise Unsupported(f"dtype {buf.dtype} cannot be reduced")
+        if (out is buf and self._in_pool(buf) and self._switch_capable("multicast")
+                and self._switch_capable("aggregation")):
+            self.schedule(ALLREDUCE)
+            _lib.check(self._lib.fc_nvls_allreduce(self._comm, buf.data_ptr(), buf.numel(),
+                                                   DTYPE_CODE[buf.dtype], _op_code(op),
+                                                   self._stream()), self._comm, "nvls_allreduce")
+            return out
         self.plan(ALLREDUCE)
         self.register(out)
         _lib.check(self._lib.fc_allreduce(self._comm, buf.data_ptr(), out.data_ptr(), buf.numel(),

@@ -42,7 +42,8 @@ def topologies():
     out = {}
     for n in (2, 4, 8):
         out[f"nvs{n}"] = (topology.nvswitch_doc(n), COLLS, True)
-    out["nvs8_mc"] = (topology.nvswitch_doc(8, multicast=True), COLLS, True)
+    for n in (2, 4, 8):
+        out[f"nvs{n}_mc"] = (topology.nvswitch_doc(n, multicast=True), COLLS, True)
     for beta in (450, 300, 100):
         out[f"groups{beta}"] = (topology.groups_switch_doc(beta), COLLS, True)
     out["fig3a"] = (json.loads(cs.serialize_topology(

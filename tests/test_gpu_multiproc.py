@@ -30,3 +30,20 @@ def test_multiproc_parity(n):
     out = r.stdout + r.stderr
     assert r.returncode == 0, out[-4000:]
     assert out.count(" OK") >= n, out[-4000:]
+
+
+@pytest.mark.parametrize("n", [2, 4])
+def test_nvls_engine_parity(n):
+    """Pruned forests on a multicast/aggregation NVSwitch run through the
+    NVLS (multimem) engine: allgather bit-exact, int32 exact, fp within tolerance."""
+    if _ngpus() < n:
+        pytest.skip(f"needs {n} GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(29700 + n),
+           os.path.join(HERE, "mp", "nvls_worker.py")]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900)
+    out = r.stdout + r.stderr
+    assert r.returncode == 0, out[-4000:]
+    if "SKIP" in out:
+        pytest.skip("no multicast support on this box")
+    assert out.count(" OK") >= n, out[-4000:]
