@@ -1,0 +1,135 @@
+"""GPU API behaviour: argument checking, dtype/op support, unaligned views,
+empty calls, the Executor surface, tracing, and device-side fault detection."""
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import GOLDEN, load_golden
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def dev():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return torch.device("cuda:0")
+
+
+def _vc(name, **kw):
+    from paper_2402_06787_b200 import VirtualComm
+
+    s = load_golden(name)
+    return VirtualComm(schedules={s.collective: s}, scratch_bytes=256 << 20, **kw)
+
+
+def test_argument_errors(dev):
+    from paper_2402_06787_b200 import InvalidArgument, Unsupported
+
+    comm = _vc("nvs4_reduce_scatter")
+    n = comm.nranks
+    ins = [torch.zeros(n * 8, device=dev) for _ in range(n)]
+    outs = [torch.zeros(8, device=dev) for _ in range(n)]
+    with pytest.raises(InvalidArgument):
+        comm.reduce_scatter(outs[:-1], ins)
+    with pytest.raises(InvalidArgument):
+        comm.reduce_scatter([torch.zeros(8, device=dev, dtype=torch.bfloat16)] * n, ins)
+    with pytest.raises(Unsupported):
+        comm.reduce_scatter(outs, ins, op="max")
+    with pytest.raises(Unsupported):
+        comm.reduce_scatter([o.double() for o in outs], [i.double() for i in ins])
+    with pytest.raises(InvalidArgument):
+        comm.reduce_scatter([o.cpu() for o in outs], ins)
+
+
+def test_empty_and_bytes(dev):
+    comm = _vc("nvs4_allgather")
+    n = comm.nranks
+    comm.all_gather([torch.empty(0, device=dev) for _ in range(n)],
+                    [torch.empty(0, device=dev) for _ in range(n)])
+    for dt in (torch.uint8, torch.int8, torch.float64, torch.float8_e4m3fn):
+        S = 333
+        sends = [torch.randint(0, 255, (S,), dtype=torch.uint8).view(torch.uint8).to(dev).view(dt)
+                 if dt.itemsize == 1 else torch.randn(S, dtype=torch.float64, device=dev)
+                 for _ in range(n)]
+        outs = [torch.empty(n * S, dtype=dt, device=dev) for _ in range(n)]
+        comm.all_gather(outs, sends)
+        cat = torch.cat([s.view(torch.uint8) for s in sends])
+        for o in outs:
+            assert torch.equal(o.view(torch.uint8), cat)
+    comm.check()
+
+
+@pytest.mark.parametrize("offset", [1, 2, 3])
+def test_unaligned_views(dev, offset):
+    """Views whose data pointers are not 16-byte aligned take the scalar /
+    narrow-vector paths (LL128 needs 8-byte alignment) and stay exact."""
+    from oracle import forest_oracle as fo
+
+    comm = _vc("nvs8_reduce_scatter")
+    s = comm.schedule("reduce_scatter")
+    n, S = comm.nranks, 4099
+    base = [torch.randn(n * S + offset, device=dev) for _ in range(n)]
+    ins = [b[offset:] for b in base]
+    obase = [torch.zeros(S + offset, device=dev) for _ in range(n)]
+    outs = [b[offset:] for b in obase]
+    comm.reduce_scatter(outs, ins)
+    ref = fo.reduce_scatter(s, [x.cpu().numpy() for x in ins], "float32")
+    for r in range(n):
+        assert np.array_equal(outs[r].cpu().numpy().view(np.uint32), ref[r].view(np.uint32))
+    comm.check()
+
+
+def test_executor_from_json_path(dev):
+    import os
+
+    from paper_2402_06787_b200 import Executor
+
+    path = os.path.join(GOLDEN, "schedules", "groups450_allreduce.json")
+    ex = Executor(path, virtual=True, validate=False)
+    n = ex.comm.nranks
+    bufs = [torch.full((1000,), float(r + 1), device=dev) for r in range(n)]
+    ex.all_reduce(bufs)
+    for b in bufs:
+        assert torch.all(b == n * (n + 1) / 2)
+    ex.close()
+
+
+def test_trace_records(dev):
+    comm = _vc("nvs8_allgather")
+    n = comm.nranks
+    comm.enable_trace(1 << 16)
+    sends = [torch.randn(1 << 16, device=dev) for _ in range(n)]
+    outs = [torch.empty(n << 16, device=dev) for _ in range(n)]
+    comm.all_gather(outs, sends)
+    rec = comm.read_trace()
+    assert rec.size > 0
+    assert set(np.unique(rec["rank"])) == set(range(n))
+    assert np.all(rec["t_end"] >= rec["t_start"])
+    comm.disable_trace()
+
+
+def test_device_timeout_is_reported_not_hung(dev):
+    """Fault injection: a forest whose root never sends.  The leaf's wait
+    times out on the device, the kernel exits, check() raises DeviceError."""
+    import ctypes
+
+    from paper_2402_06787_b200 import DeviceError, _lib
+    from paper_2402_06787_b200 import compiler as C
+
+    comm = _vc("nvs2_allgather", options={"timeout_ms": 300, "proto": 0})
+    plan = comm.plan("allgather")
+    bad = plan.table.copy()
+    task0 = C.HEADER_WORDS + plan.nranks * C.RANKDESC_WORDS
+    for i in range(sum(map(len, plan.tasks))):
+        row = bad[task0 + i * C.TASK_WORDS:task0 + (i + 1) * C.TASK_WORDS]
+        if row[C.TW_KIND] == C.K_AG_ROOT and row[C.TW_ROOT] == 0:
+            row[C.TW_N_AG_CHILD] = 0  # root 0 "forgets" its child
+    _lib.check(comm._lib.fc_plan_load(comm._comm, 0, bad.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
+                                      bad.size), comm._comm)
+    sends = [torch.randn(4096, device=dev) for _ in range(2)]
+    outs = [torch.empty(8192, device=dev) for _ in range(2)]
+    comm.all_gather(outs, sends)
+    with pytest.raises(DeviceError):
+        comm.check()

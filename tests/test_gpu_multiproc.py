@@ -47,3 +47,14 @@ def test_nvls_engine_parity(n):
     if "SKIP" in out:
         pytest.skip("no multicast support on this box")
     assert out.count(" OK") >= n, out[-4000:]
+
+
+def test_ddp_comm_hook():
+    if _ngpus() < 2:
+        pytest.skip("needs 2 GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", "29750",
+           os.path.join(HERE, "mp", "ddp_worker.py")]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900)
+    out = r.stdout + r.stderr
+    assert r.returncode == 0 and out.count(" OK") >= 2, out[-4000:]
