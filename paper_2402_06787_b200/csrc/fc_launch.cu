@@ -23,6 +23,8 @@ const void* kernel_for(int rd, int ww, int proto) {
   }
 }
 
+int smem_for(int proto) { return proto ? 0 : FC_SMEM_BYTES; }  // LL128 keeps no smem ring
+
 int ensure_smem_attr(const void* fn) {
   static const void* done[64] = {};
   for (auto& d : done) {
@@ -48,10 +50,11 @@ int fc_launch(const FcParams& p, int reduce_dtype, int cooperative, void* stream
   const int a = ensure_smem_attr(fn);
   if (a) return a;
   cudaError_t err;
+  const int smem = smem_for(p.proto);
   if (cooperative)
-    err = cudaLaunchCooperativeKernel(fn, grid, block, args, FC_SMEM_BYTES, (cudaStream_t)stream);
+    err = cudaLaunchCooperativeKernel(fn, grid, block, args, smem, (cudaStream_t)stream);
   else
-    err = cudaLaunchKernel(fn, grid, block, args, FC_SMEM_BYTES, (cudaStream_t)stream);
+    err = cudaLaunchKernel(fn, grid, block, args, smem, (cudaStream_t)stream);
   return (int)err;
 }
 
