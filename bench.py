@@ -449,7 +449,39 @@ def sweep_multi(comm, dist, n, dev, args):
         rec("allreduce", M, ms, nm, "bfloat16")
         comm.deregister(buf)
     comm.check()
+    if n == 8:
+        res["sparse_stress"] = sparse_stress(dist, dev, args)
     return res
+
+
+def sparse_stress(dist, dev, args):
+    """BASELINE configs[4]: the 2-groups-of-4 box joined only by two bridge
+    pairs.  The forest is the reference's packing for
+    that graph; it runs on the physical NVSwitch, so achieved bandwidth can
+    exceed the declared graph's T*."""
+    import torch
+
+    from paper_2402_06787_b200 import ForestCollComm
+    from paper_2402_06787_b200.topology import groups_switch_doc
+
+    out = []
+    rank = dist.get_rank()
+    for beta in (450, 300, 100):
+        c = ForestCollComm(groups_switch_doc(beta), rank=rank, world_size=8,
+                           device=dev.index, scratch_bytes=1 << 30)
+        M = args.msg_mib * MIB
+        S = M // 8 // 4
+        inp = torch.randn(S, device=dev)
+        o = c.empty(8 * S, dtype=torch.float32)
+        ms = timed(lambda: c.all_gather(o, inp), max(5, args.steps), 3, dist)
+        t = c.t_star("allgather", M)
+        out.append({"topology": f"groups_switch({beta})", "k": c.schedule("allgather").k,
+                    "collective": "allgather", "M_bytes": M, "ms": round(ms, 4),
+                    "algbw_GBps": round(gbs(M, ms), 2), "graph_t_star_ms": round(t * 1e3, 4),
+                    "frac_of_graph_t_star": round(t * 1e3 / ms, 4)})
+        c.check()
+        c.close()
+    return out
 
 
 # ---------------------------------------------------------------------------
