@@ -187,7 +187,7 @@ def cpu_allgather_timer(schedule, shard_bytes, threads=None):
     return step, threads, sample
 
 
-def cpu_baseline_allgather(schedule, shard_bytes, budget_s=15.0):
+def cpu_baseline_allgather(schedule, shard_bytes, budget_s=10.0):
     """Bounded CPU-baseline sample for the N=1 bench line (rank 0 only)."""
     step, threads, sample = cpu_allgather_timer(schedule, shard_bytes)
     step()
@@ -196,7 +196,7 @@ def cpu_baseline_allgather(schedule, shard_bytes, budget_s=15.0):
         step()
         reps += 1
         el = time.perf_counter() - t0
-        if el > budget_s or reps >= 20:
+        if el > budget_s or reps >= 2000:
             break
     per = el / reps
     M = schedule.num_compute * shard_bytes

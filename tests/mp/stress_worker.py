@@ -1,0 +1,67 @@
+"""torchrun worker: randomized soak of back-to-back collectives (mixed
+collective, size, dtype, protocol, buffer reuse) checked against closed
+forms — allgather = concatenation, int32 reductions = exact sums.  Catches
+races in the epoch / entry-barrier / flag protocol that single calls miss."""
+
+import os
+import random
+import sys
+
+REPO = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, REPO)
+
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+from paper_2402_06787_b200 import ForestCollComm  # noqa: E402
+from paper_2402_06787_b200.topology import nvswitch_doc  # noqa: E402
+
+
+def main():
+    iters = int(sys.argv[1]) if len(sys.argv) > 1 else 200
+    local = int(os.environ["LOCAL_RANK"])
+    torch.cuda.set_device(local)
+    dev = torch.device(f"cuda:{local}")
+    dist.init_process_group("nccl", device_id=dev)
+    rank, n = dist.get_rank(), dist.get_world_size()
+    comm = ForestCollComm(nvswitch_doc(n), rank=rank, world_size=n, device=local,
+                          scratch_bytes=256 << 20, options={"timeout_ms": 20000})
+    rng = random.Random(1234)  # same sequence on every rank
+    # a few persistent (registered) output buffers, reused across calls
+    pools = {dt: comm.empty(n * (1 << 21), dtype=dt) for dt in (torch.float32, torch.int32)}
+    fails = 0
+    for it in range(iters):
+        coll = rng.choice(["allgather", "reduce_scatter", "allreduce"])
+        proto = rng.choice([-1, 0])
+        comm.set_option("proto", proto)
+        comm.set_option("chunk_max", rng.choice([16 << 10, 64 << 10, 256 << 10]))
+        S = rng.choice([1, 17, 256, 4096, 65536 + 8, 1 << 20, (1 << 21) - 4])
+        g = torch.Generator().manual_seed(it)
+        if coll == "allgather":
+            allin = torch.randint(-2**31, 2**31 - 1, (n, S), generator=g, dtype=torch.int32)
+            out = pools[torch.float32][: n * S].view(torch.int32)
+            comm.all_gather(out, allin[rank].to(dev))
+            ok = torch.equal(out.cpu(), allin.reshape(-1))
+        elif coll == "reduce_scatter":
+            allin = torch.randint(-2**20, 2**20, (n, n * S), generator=g, dtype=torch.int32)
+            out = torch.empty(S, dtype=torch.int32, device=dev)
+            comm.reduce_scatter(out, allin[rank].to(dev))
+            ok = torch.equal(out.cpu(), allin.sum(0, dtype=torch.int64).to(torch.int32)[rank * S:(rank + 1) * S])
+        else:
+            allin = torch.randint(-2**20, 2**20, (n, n * S), generator=g, dtype=torch.int32)
+            buf = pools[torch.int32][: n * S]
+            buf.copy_(allin[rank].to(dev))
+            comm.all_reduce(buf)
+            ok = torch.equal(buf.cpu(), allin.sum(0, dtype=torch.int64).to(torch.int32))
+        if not ok:
+            fails += 1
+            print(f"rank {rank} iter {it} {coll} S={S} proto={proto} MISMATCH", flush=True)
+    comm.check()
+    print(f"STRESS rank {rank} {'OK' if not fails else f'FAIL {fails}'} ({iters} calls)", flush=True)
+    comm.close()
+    dist.destroy_process_group()
+    sys.exit(1 if fails else 0)
+
+
+if __name__ == "__main__":
+    main()

@@ -58,3 +58,15 @@ def test_ddp_comm_hook():
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=900)
     out = r.stdout + r.stderr
     assert r.returncode == 0 and out.count(" OK") >= 2, out[-4000:]
+
+
+@pytest.mark.parametrize("n", [2, 4, 8])
+def test_randomized_soak(n):
+    if _ngpus() < n:
+        pytest.skip(f"needs {n} GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(29800 + n),
+           os.path.join(HERE, "mp", "stress_worker.py"), "150"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=1200)
+    out = r.stdout + r.stderr
+    assert r.returncode == 0 and out.count("STRESS") >= n, out[-4000:]
