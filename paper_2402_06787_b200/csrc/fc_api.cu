@@ -815,8 +815,8 @@ int fc_buffer_register(fc_comm_t* c, const void* ptr, size_t bytes, const void* 
     reg.peer[r] = base + b.offset;
   }
   for (auto& r : c->regs)
-    if (r.lo == reg.lo) {
-      r = reg;
+    if (r.lo == reg.lo) {  // same base: keep the widest registered extent
+      if (reg.hi > r.hi) r = reg;
       return FC_SUCCESS;
     }
   c->regs.push_back(reg);

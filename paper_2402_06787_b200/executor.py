@@ -357,8 +357,9 @@ class ForestCollComm(_CommBase):
         same-sized tensors).  Outputs of all_gather / all_reduce must be
         registered; first use registers automatically."""
         key = (t.data_ptr(), t.numel() * t.element_size())
-        if key in self._registered or self.nranks == 1:
-            return
+        if self.nranks == 1 or any(lo <= key[0] and key[0] + key[1] <= lo + nb
+                                   for lo, nb in self._registered):
+            return  # already mapped (views of a registered buffer included)
         hb = self._lib.fc_handle_bytes()
         mine = ctypes.create_string_buffer(hb)
         _lib.check(self._lib.fc_buffer_export(self._comm, key[0], key[1], mine), self._comm,
@@ -370,6 +371,8 @@ class ForestCollComm(_CommBase):
         self._registered[key] = t  # keep the allocation alive while mapped
 
     def deregister(self, t: torch.Tensor) -> None:
+        """Drop the peer mapping of a buffer registered with exactly this
+        (pointer, size); views of it are covered by the same entry."""
         key = (t.data_ptr(), t.numel() * t.element_size())
         if self._registered.pop(key, None) is not None:
             self._lib.fc_buffer_deregister(self._comm, key[0])
