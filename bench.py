@@ -366,7 +366,10 @@ def run_multi(args):
 
     extra = {}
     if not args.quick:
-        extra = sweep_multi(comm, dist, n, dev, args)
+        try:
+            extra = sweep_multi(comm, dist, n, dev, args)
+        except Exception as exc:  # the sweep is supplementary: never lose the headline line
+            extra = {"sweep_error": f"{type(exc).__name__}: {exc}"[:300]}
     if rank == 0:
         line = {
             "metric": "collective algbw GB/s (ForestColl allgather, M = total output bytes per rank)",
@@ -450,7 +453,10 @@ def sweep_multi(comm, dist, n, dev, args):
         comm.deregister(buf)
     comm.check()
     if n == 8:
-        res["sparse_stress"] = sparse_stress(dist, dev, args)
+        try:
+            res["sparse_stress"] = sparse_stress(dist, dev, args)
+        except Exception as exc:
+            res["sparse_stress_error"] = f"{type(exc).__name__}: {exc}"[:300]
     return res
 
 

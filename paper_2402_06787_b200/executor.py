@@ -222,6 +222,7 @@ class ForestCollComm(_CommBase):
         if device is None:
             device = int(os.environ.get("LOCAL_RANK", torch.cuda.current_device()))
         self.rank, self.device = rank, device
+        self._prune_default = prune
         self._group = None
         if world_size > 1:
             self._group = group if group is not None else dist.new_group(backend="gloo")
@@ -232,6 +233,8 @@ class ForestCollComm(_CommBase):
             buses = self._allgather_obj(_pci_bus_id(device))
             doc, self.topology_source = discover_for_torch(world_size,
                                                            None if None in buses else buses)
+        if self.topology_source == "nvml" and not schedules:
+            doc = self._usable_topology(doc, world_size)
         super().__init__(doc, world_size, schedules, validate, prune)
         comm = ctypes.c_void_p()
         _lib.check(self._lib.fc_comm_init(rank, world_size, device, int(scratch_bytes),
@@ -341,6 +344,26 @@ class ForestCollComm(_CommBase):
             return False
         sws = [n for n in self.topology["nodes"] if n["kind"] == "switch"]
         return len(sws) == 1 and bool(sws[0].get(capability, False))
+
+    def _usable_topology(self, doc, world_size):
+        """An NVML topology whose schedule is neither cached nor generatable
+        here (no reference generator on this machine) falls back, on every
+        rank alike, to the nominal NVSwitch model when NVML shows a single
+        switch (the forest shape of a uniform NVSwitch does not depend on
+        the bandwidth value)."""
+        from .generator import cache_key, _cache_paths
+        from ._refpath import import_collsched
+
+        cached = any(os.path.exists(p) for p in _cache_paths(cache_key(doc, ALLGATHER, self._prune_default)))
+        ok = cached or import_collsched() is not None
+        if all(self._allgather_obj(ok)):
+            return doc
+        nominal = nvswitch_doc(world_size)
+        switches = [n for n in doc["nodes"] if n["kind"] == "switch"]
+        if len(switches) == 1:
+            self.topology_source = "nvml->nominal (schedule not cached, no generator)"
+            return nominal
+        return doc
 
     def _allgather_obj(self, obj):
         import torch.distributed as dist
