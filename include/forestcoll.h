@@ -107,6 +107,11 @@ int fc_comm_init(int rank, int nranks, int device, size_t scratch_bytes,
                  fc_comm_t** out);
 int fc_comm_init_virtual(int nranks, int device, size_t scratch_bytes,
                          fc_comm_t** out);
+/* several ranks per process/device (one cooperative grid): fc_comm_export
+ * then writes one handle per local rank, and output buffers are registered
+ * with the _multi variants (one pointer per local rank). */
+int fc_comm_init_ranks(const int* ranks, int nlocal, int nranks, int device,
+                       size_t scratch_bytes, fc_comm_t** out);
 int fc_comm_export(fc_comm_t* comm, void* handle);
 int fc_comm_connect(fc_comm_t* comm, const void* handles);
 int fc_comm_set_option(fc_comm_t* comm, int option, long long value);
@@ -120,6 +125,10 @@ int fc_buffer_export(fc_comm_t* comm, const void* ptr, size_t bytes,
 int fc_buffer_register(fc_comm_t* comm, const void* ptr, size_t bytes,
                        const void* handles);
 int fc_buffer_deregister(fc_comm_t* comm, const void* ptr);
+int fc_buffer_export_multi(fc_comm_t* comm, const void* const* ptrs, size_t bytes,
+                           void* handles);
+int fc_buffer_register_multi(fc_comm_t* comm, const void* const* ptrs,
+                             size_t bytes, const void* handles);
 
 int fc_plan_load(fc_comm_t* comm, int collective, const int32_t* table,
                  size_t nwords);

@@ -22,7 +22,7 @@ __version__ = "0.1.0"
 def __getattr__(name):
     # torch-dependent classes load lazily so the host-side modules (topology,
     # compiler, generator) import without torch or a GPU.
-    if name in ("ForestCollComm", "VirtualComm", "Executor"):
+    if name in ("ForestCollComm", "VirtualComm", "MultiRankComm", "Executor"):
         from . import executor
 
         return getattr(executor, name)

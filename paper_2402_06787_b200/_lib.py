@@ -47,6 +47,9 @@ SIGNATURES = {
     "fc_handle_bytes": (_SZ, []),
     "fc_comm_init": (_I, [_I, _I, _I, _SZ, ctypes.POINTER(_P)]),
     "fc_comm_init_virtual": (_I, [_I, _I, _SZ, ctypes.POINTER(_P)]),
+    "fc_comm_init_ranks": (_I, [_P, _I, _I, _I, _SZ, ctypes.POINTER(_P)]),
+    "fc_buffer_export_multi": (_I, [_P, _P, _SZ, _P]),
+    "fc_buffer_register_multi": (_I, [_P, _P, _SZ, _P]),
     "fc_comm_export": (_I, [_P, _P]),
     "fc_comm_connect": (_I, [_P, _P]),
     "fc_comm_set_option": (_I, [_P, _I, _LL]),

@@ -60,6 +60,8 @@ typedef CUresult (*PFN_getRange)(CUdeviceptr*, size_t*, CUdeviceptr);
 
 struct fc_comm {
   int rank = 0, nranks = 0, device = 0, virt = 0, nlocal = 0, connected = 0;
+  int local[FC_MAXR] = {};      // rank ids executed by this process (grid order)
+  bool is_local[FC_MAXR] = {};
   size_t ws_bytes = 0, flags_off = 0, flags_words = 0, scratch_off = 0, scratch_bytes = 0;
   char* ws[FC_MAXR] = {};
   bool own[FC_MAXR] = {};
@@ -227,7 +229,7 @@ int run(fc_comm* c, int coll, const void* const* sends, void* const* recvs, size
     P.flags[r] = (unsigned*)(c->ws[r] + c->flags_off);
   }
   for (int i = 0; i < c->nlocal; ++i) {
-    const int r = c->virt ? i : c->rank;
+    const int r = c->local[i];
     P.local_rank[i] = r;
     P.tasks[i] = pl.d_tasks[i];
     P.nactive[i] = pl.nact[i];
@@ -245,7 +247,8 @@ int run(fc_comm* c, int coll, const void* const* sends, void* const* recvs, size
                   "output buffer %p (%zu bytes) is not registered (fc_buffer_register)",
                   recvs[0], need);
     const size_t delta = (uintptr_t)recvs[0] - reg->lo;
-    for (int r = 0; r < N; ++r) P.recv[r] = reg->peer[r] + delta;
+    for (int r = 0; r < N; ++r)
+      if (!c->is_local[r]) P.recv[r] = reg->peer[r] + delta;
   }
   P.shard_elems = S;
   P.stride_elems = stride;
@@ -328,7 +331,7 @@ int run(fc_comm* c, int coll, const void* const* sends, void* const* recvs, size
   }
   P.nchunks = (int)n;
   P.proto = proto;
-  const int coop = c->virt ? 1 : 0;
+  const int coop = c->nlocal > 1 ? 1 : 0;  // local ranks wait on each other in one grid
   int launches = 0, grid = 0;
   // allgather: a copy engine places each local root's own shard into its
   // output concurrently with the kernel (no SM bandwidth spent on it)
@@ -542,6 +545,8 @@ int fc_comm_init(int rank, int nranks, int device, size_t scratch_bytes, fc_comm
   c->nranks = nranks;
   c->device = device;
   c->nlocal = 1;
+  c->local[0] = rank;
+  c->is_local[rank] = true;
   setup_layout(c, scratch_bytes);
   int st;
   if (cudaSetDevice(device) != cudaSuccess || (st = alloc_workspace(c, &c->ws[rank])) != 0 ||
@@ -557,6 +562,44 @@ int fc_comm_init(int rank, int nranks, int device, size_t scratch_bytes, fc_comm
   return FC_SUCCESS;
 }
 
+int fc_comm_init_ranks(const int* ranks, int nlocal, int nranks, int device,
+                       size_t scratch_bytes, fc_comm_t** out) {
+  if (!out || !ranks || nlocal < 1 || nranks < 1 || nranks > FC_MAXR || nlocal > nranks)
+    return FC_ERR_INVALID_ARG;
+  *out = nullptr;
+  fc_comm* c = new fc_comm();
+  c->nranks = nranks;
+  c->device = device;
+  c->nlocal = nlocal;
+  c->rank = ranks[0];
+  for (int i = 0; i < nlocal; ++i) {
+    if (ranks[i] < 0 || ranks[i] >= nranks || c->is_local[ranks[i]]) {
+      delete c;
+      return FC_ERR_INVALID_ARG;
+    }
+    c->local[i] = ranks[i];
+    c->is_local[ranks[i]] = true;
+  }
+  c->virt = nlocal == nranks ? 1 : 0;
+  c->connected = c->virt;
+  setup_layout(c, scratch_bytes);
+  int st = cudaSetDevice(device) == cudaSuccess ? 0 : FC_ERR_CUDA;
+  for (int i = 0; i < nlocal && st == 0; ++i) {
+    st = alloc_workspace(c, &c->ws[c->local[i]]);
+    if (st == 0) c->own[c->local[i]] = true;
+  }
+  if (st == 0) st = default_ctas(c);
+  if (st != 0) {
+    fprintf(stderr, "fc_comm_init_ranks: %s\n", c->err.c_str());
+    for (int r = 0; r < FC_MAXR; ++r)
+      if (c->own[r]) cudaFree(c->ws[r]);
+    delete c;
+    return st;
+  }
+  *out = c;
+  return FC_SUCCESS;
+}
+
 int fc_comm_init_virtual(int nranks, int device, size_t scratch_bytes, fc_comm_t** out) {
   if (!out || nranks < 1 || nranks > FC_MAXR) return FC_ERR_INVALID_ARG;
   *out = nullptr;
@@ -565,6 +608,10 @@ int fc_comm_init_virtual(int nranks, int device, size_t scratch_bytes, fc_comm_t
   c->device = device;
   c->virt = 1;
   c->nlocal = nranks;
+  for (int r = 0; r < nranks; ++r) {
+    c->local[r] = r;
+    c->is_local[r] = true;
+  }
   c->connected = 1;
   setup_layout(c, scratch_bytes);
   int st = cudaSetDevice(device) == cudaSuccess ? 0 : FC_ERR_CUDA;
@@ -586,20 +633,23 @@ int fc_comm_init_virtual(int nranks, int device, size_t scratch_bytes, fc_comm_t
 
 int fc_comm_export(fc_comm_t* c, void* handle) {
   if (!c || !handle || c->virt) return FC_ERR_INVALID_ARG;
-  CommBlob b;
-  memset(&b, 0, sizeof(b));
-  b.magic = kCommMagic;
-  b.rank = c->rank;
-  b.nranks = c->nranks;
-  b.ws_bytes = c->ws_bytes;
-  b.flags_off = c->flags_off;
-  b.flags_words = c->flags_words;
-  b.scratch_off = c->scratch_off;
-  b.scratch_bytes = c->scratch_bytes;
   FC_CUDA(c, cudaSetDevice(c->device));
-  FC_CUDA(c, cudaIpcGetMemHandle(&b.handle, c->ws[c->rank]));
-  memset(handle, 0, kHandleBytes);
-  memcpy(handle, &b, sizeof(b));
+  for (int i = 0; i < c->nlocal; ++i) {  // one blob per local rank
+    CommBlob b;
+    memset(&b, 0, sizeof(b));
+    b.magic = kCommMagic;
+    b.rank = c->local[i];
+    b.nranks = c->nranks;
+    b.ws_bytes = c->ws_bytes;
+    b.flags_off = c->flags_off;
+    b.flags_words = c->flags_words;
+    b.scratch_off = c->scratch_off;
+    b.scratch_bytes = c->scratch_bytes;
+    FC_CUDA(c, cudaIpcGetMemHandle(&b.handle, c->ws[c->local[i]]));
+    char* dst = (char*)handle + (size_t)i * kHandleBytes;
+    memset(dst, 0, kHandleBytes);
+    memcpy(dst, &b, sizeof(b));
+  }
   return FC_SUCCESS;
 }
 
@@ -615,7 +665,7 @@ int fc_comm_connect(fc_comm_t* c, const void* handles) {
         b.scratch_off != c->scratch_off || b.scratch_bytes != c->scratch_bytes)
       return fail(c, FC_ERR_INVALID_ARG,
                   "rank %d workspace layout differs (scratch_bytes must match on all ranks)", r);
-    if (r == c->rank) continue;
+    if (c->is_local[r]) continue;
     char* base = nullptr;
     int st = open_mapping(c, b.handle, &base);
     if (st) return st;
@@ -722,7 +772,7 @@ int fc_comm_check(fc_comm_t* c, int* device_error) {
   FC_CUDA(c, cudaDeviceSynchronize());
   int worst = 0;
   for (int i = 0; i < c->nlocal; ++i) {
-    const int r = c->virt ? i : c->rank;
+    const int r = c->local[i];
     FcCtl ctl;
     FC_CUDA(c, cudaMemcpy(&ctl, c->ws[r], sizeof(ctl), cudaMemcpyDeviceToHost));
     if (ctl.error && !worst) {
@@ -763,39 +813,51 @@ int fc_comm_destroy(fc_comm_t* c) {
 
 const char* fc_last_error(const fc_comm_t* c) { return c ? c->err.c_str() : "null communicator"; }
 
-int fc_buffer_export(fc_comm_t* c, const void* ptr, size_t bytes, void* handle) {
-  if (!c || !ptr || !handle) return FC_ERR_INVALID_ARG;
-  BufBlob b;
-  memset(&b, 0, sizeof(b));
-  b.magic = kBufMagic;
-  b.rank = c->rank;
-  b.bytes = bytes;
-  if (!c->virt) {
-    FC_CUDA(c, cudaSetDevice(c->device));
-    PFN_getRange fn = get_range_fn();
-    if (!fn) return fail(c, FC_ERR_CUDA, "cuMemGetAddressRange entry point unavailable");
-    CUdeviceptr base = 0;
-    size_t size = 0;
-    if (fn(&base, &size, (CUdeviceptr)ptr) != CUDA_SUCCESS)
-      return fail(c, FC_ERR_INVALID_ARG, "pointer %p is not device memory", ptr);
-    if ((uintptr_t)ptr + bytes > (uintptr_t)base + size)
-      return fail(c, FC_ERR_INVALID_ARG, "buffer exceeds its allocation");
-    b.offset = (uintptr_t)ptr - (uintptr_t)base;
-    FC_CUDA(c, cudaIpcGetMemHandle(&b.handle, (void*)base));
+int fc_buffer_export_multi(fc_comm_t* c, const void* const* ptrs, size_t bytes, void* handles) {
+  if (!c || !ptrs || !handles) return FC_ERR_INVALID_ARG;
+  for (int i = 0; i < c->nlocal; ++i) {
+    BufBlob b;
+    memset(&b, 0, sizeof(b));
+    b.magic = kBufMagic;
+    b.rank = c->local[i];
+    b.bytes = bytes;
+    if (!c->virt) {
+      FC_CUDA(c, cudaSetDevice(c->device));
+      PFN_getRange fn = get_range_fn();
+      if (!fn) return fail(c, FC_ERR_CUDA, "cuMemGetAddressRange entry point unavailable");
+      CUdeviceptr base = 0;
+      size_t size = 0;
+      if (fn(&base, &size, (CUdeviceptr)ptrs[i]) != CUDA_SUCCESS)
+        return fail(c, FC_ERR_INVALID_ARG, "pointer %p is not device memory", ptrs[i]);
+      if ((uintptr_t)ptrs[i] + bytes > (uintptr_t)base + size)
+        return fail(c, FC_ERR_INVALID_ARG, "buffer exceeds its allocation");
+      b.offset = (uintptr_t)ptrs[i] - (uintptr_t)base;
+      FC_CUDA(c, cudaIpcGetMemHandle(&b.handle, (void*)base));
+    }
+    char* dst = (char*)handles + (size_t)i * kHandleBytes;
+    memset(dst, 0, kHandleBytes);
+    memcpy(dst, &b, sizeof(b));
   }
-  memset(handle, 0, kHandleBytes);
-  memcpy(handle, &b, sizeof(b));
   return FC_SUCCESS;
 }
 
-int fc_buffer_register(fc_comm_t* c, const void* ptr, size_t bytes, const void* handles) {
-  if (!c || !ptr) return FC_ERR_INVALID_ARG;
+int fc_buffer_export(fc_comm_t* c, const void* ptr, size_t bytes, void* handle) {
+  if (c && c->nlocal != 1) return fail(c, FC_ERR_INVALID_ARG, "use fc_buffer_export_multi");
+  return fc_buffer_export_multi(c, &ptr, bytes, handle);
+}
+
+// Register one output buffer per local rank (ptrs[0..nlocal)); `handles`
+// holds one blob per rank of the communicator, in rank order.  Remote ranks'
+// buffers are opened via IPC; local ranks use the pointers passed per call.
+int fc_buffer_register_multi(fc_comm_t* c, const void* const* ptrs, size_t bytes,
+                             const void* handles) {
+  if (!c || !ptrs) return FC_ERR_INVALID_ARG;
   if (c->virt) return FC_SUCCESS;  // all ranks' buffers are local pointers
   if (!handles) return FC_ERR_INVALID_ARG;
   FC_CUDA(c, cudaSetDevice(c->device));
   Reg reg;
   memset(&reg, 0, sizeof(reg));
-  reg.lo = (uintptr_t)ptr;
+  reg.lo = (uintptr_t)ptrs[0];
   reg.hi = reg.lo + bytes;
   for (int r = 0; r < c->nranks; ++r) {
     BufBlob b;
@@ -805,10 +867,7 @@ int fc_buffer_register(fc_comm_t* c, const void* ptr, size_t bytes, const void* 
     if (b.bytes != bytes)
       return fail(c, FC_ERR_INVALID_ARG, "rank %d registered %llu bytes, this rank %zu", r,
                   (unsigned long long)b.bytes, bytes);
-    if (r == c->rank) {
-      reg.peer[r] = (char*)ptr;
-      continue;
-    }
+    if (c->is_local[r]) continue;
     char* base = nullptr;
     int st = open_mapping(c, b.handle, &base);
     if (st) return st;
@@ -821,6 +880,12 @@ int fc_buffer_register(fc_comm_t* c, const void* ptr, size_t bytes, const void* 
     }
   c->regs.push_back(reg);
   return FC_SUCCESS;
+}
+
+int fc_buffer_register(fc_comm_t* c, const void* ptr, size_t bytes, const void* handles) {
+  if (c && c->nlocal != 1 && !c->virt)
+    return fail(c, FC_ERR_INVALID_ARG, "use fc_buffer_register_multi");
+  return fc_buffer_register_multi(c, &ptr, bytes, handles);
 }
 
 int fc_buffer_deregister(fc_comm_t* c, const void* ptr) {
@@ -889,7 +954,7 @@ int fc_plan_load(fc_comm_t* c, int coll, const int32_t* t, size_t nwords) {
   }
   FC_CUDA(c, cudaSetDevice(c->device));
   for (int i = 0; i < c->nlocal; ++i) {
-    const int r = c->virt ? i : c->rank;
+    const int r = c->local[i];
     const int32_t* D = t + FC_HEADER_WORDS + (size_t)r * FC_RANKDESC_WORDS;
     const int rows = std::max(1, D[RD_NACTIVE] + D[RD_NWAIT]);
     p.nact[i] = D[RD_NACTIVE];
@@ -926,17 +991,17 @@ int fc_allreduce_multi(fc_comm_t* c, const void* const* sends, void* const* recv
 }
 int fc_allgather(fc_comm_t* c, const void* send, void* recv, size_t sendcount, int dtype,
                  void* stream) {
-  if (c && c->virt) return fail(c, FC_ERR_INVALID_ARG, "virtual comm: use fc_allgather_multi");
+  if (c && c->nlocal != 1) return fail(c, FC_ERR_INVALID_ARG, "several local ranks: use fc_allgather_multi");
   return run(c, FC_ALLGATHER, &send, &recv, sendcount, dtype, FC_SUM, stream);
 }
 int fc_reduce_scatter(fc_comm_t* c, const void* send, void* recv, size_t recvcount, int dtype,
                       int op, void* stream) {
-  if (c && c->virt) return fail(c, FC_ERR_INVALID_ARG, "virtual comm: use the _multi variant");
+  if (c && c->nlocal != 1) return fail(c, FC_ERR_INVALID_ARG, "several local ranks: use the _multi variant");
   return run(c, FC_REDUCE_SCATTER, &send, &recv, recvcount, dtype, op, stream);
 }
 int fc_allreduce(fc_comm_t* c, const void* send, void* recv, size_t count, int dtype, int op,
                  void* stream) {
-  if (c && c->virt) return fail(c, FC_ERR_INVALID_ARG, "virtual comm: use the _multi variant");
+  if (c && c->nlocal != 1) return fail(c, FC_ERR_INVALID_ARG, "several local ranks: use the _multi variant");
   return run(c, FC_ALLREDUCE, &send, &recv, count, dtype, op, stream);
 }
 

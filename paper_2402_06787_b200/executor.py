@@ -554,6 +554,104 @@ class VirtualComm(_CommBase):
         return outs
 
 
+class MultiRankComm(_CommBase):
+    """Several ranks of one forest per process / GPU (one cooperative grid),
+    connected over NVLink to the ranks of other processes.
+
+    Used to run forests with more ranks than GPUs (e.g. the 8-GPU NVSwitch
+    forest on 4 GPUs, 2 ranks each) through real peer memory.  Collectives
+    take one tensor per local rank, like VirtualComm.
+    """
+
+    def __init__(self, topology, *, local_ranks, world_size, device=None, group=None,
+                 scratch_bytes=VIRTUAL_SCRATCH, schedules=None, validate=True, prune=True,
+                 options=None):
+        import torch.distributed as dist
+
+        doc = _as_doc(topology)
+        self.device = int(os.environ.get("LOCAL_RANK", 0)) if device is None else device
+        self.local_ranks = tuple(local_ranks)
+        self.nranks = world_size
+        self._group = group if group is not None else dist.new_group(backend="gloo")
+        super().__init__(doc, world_size, schedules, validate, prune)
+        comm = ctypes.c_void_p()
+        arr = (ctypes.c_int * len(self.local_ranks))(*self.local_ranks)
+        _lib.check(self._lib.fc_comm_init_ranks(arr, len(self.local_ranks), world_size,
+                                                self.device, int(scratch_bytes),
+                                                ctypes.byref(comm)), None, "fc_comm_init_ranks")
+        self._comm = comm
+        for name, value in (options or {}).items():
+            self.set_option(name, value)
+        hb = self._lib.fc_handle_bytes()
+        mine = ctypes.create_string_buffer(hb * len(self.local_ranks))
+        _lib.check(self._lib.fc_comm_export(self._comm, mine), self._comm, "comm_export")
+        blobs = self._gather_by_rank(mine.raw, hb)
+        _lib.check(self._lib.fc_comm_connect(self._comm, ctypes.create_string_buffer(blobs, len(blobs))),
+                   self._comm, "comm_connect")
+        self._registered = set()
+
+    def _gather_by_rank(self, raw, hb):
+        import torch.distributed as dist
+
+        out = [None] * dist.get_world_size(self._group)
+        dist.all_gather_object(out, (self.local_ranks, raw), group=self._group)
+        per = {}
+        for ranks, blob in out:
+            for i, r in enumerate(ranks):
+                per[r] = blob[i * hb:(i + 1) * hb]
+        return b"".join(per[r] for r in range(self.nranks))
+
+    def _register(self, outs):
+        key = tuple(t.data_ptr() for t in outs) + (outs[0].numel() * outs[0].element_size(),)
+        if key in self._registered:
+            return
+        hb = self._lib.fc_handle_bytes()
+        ptrs = (ctypes.c_void_p * len(outs))(*[t.data_ptr() for t in outs])
+        nbytes = outs[0].numel() * outs[0].element_size()
+        mine = ctypes.create_string_buffer(hb * len(outs))
+        _lib.check(self._lib.fc_buffer_export_multi(self._comm, ptrs, nbytes, mine), self._comm,
+                   "buffer_export")
+        blobs = self._gather_by_rank(mine.raw, hb)
+        _lib.check(self._lib.fc_buffer_register_multi(self._comm, ptrs, nbytes,
+                                                      ctypes.create_string_buffer(blobs, len(blobs))),
+                   self._comm, "buffer_register")
+        self._registered.add(key)
+
+    def _ptrs(self, ts, name):
+        if len(ts) != len(self.local_ranks):
+            raise InvalidArgument(f"need {len(self.local_ranks)} {name} tensors, got {len(ts)}")
+        for t in ts:
+            self._check_tensor(t, self.device, name)
+        return (ctypes.c_void_p * len(ts))(*[t.data_ptr() for t in ts])
+
+    def _stream(self):
+        return torch.cuda.current_stream(self.device).cuda_stream
+
+    def all_gather(self, outs, inps):
+        self.plan(ALLGATHER)
+        self._register(outs)
+        count, code = _dtype_args(inps[0], inps[0].numel())
+        _lib.check(self._lib.fc_allgather_multi(self._comm, self._ptrs(inps, "input"),
+                                                self._ptrs(outs, "output"), count, code,
+                                                self._stream()), self._comm, "allgather")
+        return outs
+
+    def reduce_scatter(self, outs, inps, op="sum"):
+        self.plan(REDUCE_SCATTER)
+        _lib.check(self._lib.fc_reduce_scatter_multi(
+            self._comm, self._ptrs(inps, "input"), self._ptrs(outs, "output"), outs[0].numel(),
+            DTYPE_CODE[inps[0].dtype], _op_code(op), self._stream()), self._comm, "reduce_scatter")
+        return outs
+
+    def all_reduce(self, bufs, op="sum"):
+        self.plan(ALLREDUCE)
+        self._register(bufs)
+        _lib.check(self._lib.fc_allreduce_multi(
+            self._comm, self._ptrs(bufs, "buffer"), self._ptrs(bufs, "buffer"), bufs[0].numel(),
+            DTYPE_CODE[bufs[0].dtype], _op_code(op), self._stream()), self._comm, "allreduce")
+        return bufs
+
+
 class Executor:
     """§8b surface: ``Executor(schedule_or_path, topology, rank, world, device)``.
 

@@ -70,3 +70,16 @@ def test_randomized_soak(n):
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=1200)
     out = r.stdout + r.stderr
     assert r.returncode == 0 and out.count("STRESS") >= n, out[-4000:]
+
+
+@pytest.mark.parametrize("n", [2, 4])
+def test_eight_rank_forests_over_nvlink(n):
+    """8-rank forests (nvswitch(8), sparse 2x4) with 8/n ranks per GPU."""
+    if _ngpus() < n:
+        pytest.skip(f"needs {n} GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(29900 + n),
+           os.path.join(HERE, "mp", "multirank_worker.py")]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=1200)
+    out = r.stdout + r.stderr
+    assert r.returncode == 0 and out.count(" OK") >= n, out[-4000:]
