@@ -75,6 +75,7 @@ struct fc_comm {
   int copy_mode = 1;
   int dma_root_copy = 0;
   int worker_warps = 8;
+  int pdl = 1;
   int proto = -1;                  // -1 auto, 0 chunk flags, 1 LL128
   long long ll_chunk_max = 64 << 10;
   int ll_worker_warps = 4;
@@ -265,6 +266,7 @@ int run(fc_comm* c, int coll, const void* const* sends, void* const* recvs, size
   P.lag = c->lag;
   P.copy_mode = c->copy_mode;
   P.worker_warps = c->worker_warps;
+  P.pdl = c->pdl;
   P.trace = c->trace;
   P.trace_count = c->trace_count;
   P.trace_cap = c->trace_cap;
@@ -727,6 +729,9 @@ int fc_comm_set_option(fc_comm_t* c, int option, long long v) {
       if (v < 0) return fail(c, FC_ERR_INVALID_ARG, "ll_max < 0");
       c->ll_max = v;
       return FC_SUCCESS;
+    case FC_OPT_PDL:
+      c->pdl = v ? 1 : 0;
+      return FC_SUCCESS;
     case FC_OPT_NVLS_CTAS:
       if (v < 1 || v > 1024) return fail(c, FC_ERR_INVALID_ARG, "nvls_ctas out of range");
       c->nvls_ctas = (int)v;
@@ -761,6 +766,7 @@ int fc_comm_get_option(fc_comm_t* c, int option, long long* v) {
     case FC_OPT_LL_MAX: *v = c->ll_max; return FC_SUCCESS;
     case FC_OPT_LL_CHUNK_MAX: *v = c->ll_chunk_max; return FC_SUCCESS;
     case FC_OPT_NVLS_CTAS: *v = c->nvls_ctas; return FC_SUCCESS;
+    case FC_OPT_PDL: *v = c->pdl; return FC_SUCCESS;
     case FC_OPT_LL_WORKER_WARPS: *v = c->ll_worker_warps; return FC_SUCCESS;
     default: return fail(c, FC_ERR_INVALID_ARG, "unknown option %d", option);
   }

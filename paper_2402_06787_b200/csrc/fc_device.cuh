@@ -874,8 +874,11 @@ __global__ void __launch_bounds__(FC_BLOCK, 1) fc_forest_kernel(const __grid_con
   FcCtl* const ctl = P.ctl[lr];
   const int w = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  if (threadIdx.x == 0) s_epoch = ld_volatile(&ctl->epoch) + 1;
   if (threadIdx.x < FC_WPC * FC_NST) mbar_init(&bars[threadIdx.x], 1);
+  // programmatic dependent launch: the prologue above overlaps the previous
+  // kernel's tail; everything below waits for it to complete (no-op otherwise)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (threadIdx.x == 0) s_epoch = ld_volatile(&ctl->epoch) + 1;
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   __syncthreads();
   const unsigned e = s_epoch;
@@ -950,6 +953,7 @@ __global__ void __launch_bounds__(FC_BLOCK, 1) fc_forest_kernel(const __grid_con
     }
   }
   __syncthreads();
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (threadIdx.x == 0) {
     __threadfence();
     const unsigned prev = atomicAdd(&ctl->done, 1u);

@@ -129,6 +129,7 @@ struct FcParams {
   int root_local_done;  // allgather: own shard already placed in recv (DMA engine)
   int worker_warps;     // warps per worker (1, 2, 4, 8): items in flight per CTA = 8 / this
   int proto;            // 0: chunk flags + fences, 1: LL128 lines (flag in every 128 B)
+  int pdl;              // launch with programmatic stream serialization
   long long ll_unit_bytes;  // LL: staging bytes per unit multiplicity per window
   long long ll_ag_base;     // LL: scratch offset of the broadcast staging region
   FcTraceRec* trace;

@@ -51,10 +51,25 @@ int fc_launch(const FcParams& p, int reduce_dtype, int cooperative, void* stream
   if (a) return a;
   cudaError_t err;
   const int smem = smem_for(p.proto);
-  if (cooperative)
+  if (cooperative) {
     err = cudaLaunchCooperativeKernel(fn, grid, block, args, smem, (cudaStream_t)stream);
-  else
+  } else if (p.pdl) {
+    // programmatic dependent launch: overlap this launch with the tail of
+    // the previous kernel in the stream (the kernel waits in its prologue)
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = (cudaStream_t)stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    err = cudaLaunchKernelExC(&cfg, fn, args);
+  } else {
     err = cudaLaunchKernel(fn, grid, block, args, smem, (cudaStream_t)stream);
+  }
   return (int)err;
 }
 

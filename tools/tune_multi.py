@@ -29,6 +29,7 @@ def main():
     ap.add_argument("--dma", default="0")
     ap.add_argument("--ww", default="4")
     ap.add_argument("--proto", default="-1")
+    ap.add_argument("--pdl", default="1")
     args = ap.parse_args()
     local = int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
@@ -58,6 +59,8 @@ def main():
                     args.ctas.split(","), args.chunks.split(","), args.ipw.split(","),
                     args.lag.split(","), args.mode.split(","), args.dma.split(","),
                     args.ww.split(","), args.proto.split(",")):
+              for pdl in args.pdl.split(","):
+                comm.set_option("pdl", int(pdl))
                 comm.set_option("proto", int(proto))
                 comm.set_option("worker_warps", int(ww))
                 comm.set_option("ll_worker_warps", int(ww))
@@ -71,7 +74,7 @@ def main():
                 ms = timed(fn, 10, 3, dist)
                 info = comm.last_call_info()
                 if rank == 0:
-                    print(f"{coll:15s} {mib:6d}MiB ctas={ctas:>4s} chunk={int(ch)//1024:5d}K ipw={ipw} lag={lag:>3s} ww={ww} p={info['proto']} "
+                    print(f"{coll:15s} {mib:6d}MiB ctas={ctas:>4s} chunk={int(ch)//1024:5d}K ipw={ipw} lag={lag:>3s} ww={ww} p={info["proto"]} pdl={pdl} "
                           f"n={info['nchunks']:5d} L={info['launches']} ms={ms:8.4f} "
                           f"algbw={gbs(M, ms):8.1f} frac_T*={tstar*1e3/ms:6.3f}", flush=True)
     comm.check()
