@@ -452,12 +452,44 @@ def sweep_multi(comm, dist, n, dev, args):
         rec("allreduce", M, ms, nm, "bfloat16")
         comm.deregister(buf)
     comm.check()
+    try:
+        res["nvls"] = nvls_points(dist, dev, n, args)
+    except Exception as exc:
+        res["nvls_error"] = f"{type(exc).__name__}: {exc}"[:300]
     if n == 8:
         try:
             res["sparse_stress"] = sparse_stress(dist, dev, args)
         except Exception as exc:
             res["sparse_stress_error"] = f"{type(exc).__name__}: {exc}"[:300]
     return res
+
+
+def nvls_points(dist, dev, n, args):
+    """Allreduce of the forest pruned for a multicast/aggregation NVSwitch
+    (schedule.py:237-306), executed by the NVLS engine (multimem)."""
+    import torch
+
+    from paper_2402_06787_b200 import ForestCollComm
+    from paper_2402_06787_b200.topology import nvswitch_doc
+
+    c = ForestCollComm(nvswitch_doc(n, multicast=True), rank=dist.get_rank(), world_size=n,
+                       device=dev.index, scratch_bytes=64 << 20, nvls_bytes=1100 << 20)
+    if not c.nvls_enabled:
+        c.close()
+        return {"skipped": "no NVSwitch multicast support"}
+    out = []
+    for mib in (25, 1000):
+        M = mib * MIB
+        buf = c.nvls_empty(M // 2, torch.bfloat16)
+        buf.normal_()
+        ms = timed(lambda: c.all_reduce(buf), max(5, args.steps), 3, dist)
+        t = c.t_star("allreduce", M)
+        out.append({"collective": "allreduce", "engine": c.last_call_info()["proto"],
+                    "M_bytes": M, "dtype": "bfloat16", "ms": round(ms, 4),
+                    "algbw_GBps": round(gbs(M, ms), 2), "frac_of_t_star": round(t * 1e3 / ms, 4)})
+    c.check()
+    c.close()
+    return out
 
 
 def sparse_stress(dist, dev, args):
