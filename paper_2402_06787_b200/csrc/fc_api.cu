@@ -139,7 +139,10 @@ size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 int alloc_workspace(fc_comm* c, char** out) {
   FC_CUDA(c, cudaMalloc((void**)out, c->ws_bytes));
-  FC_CUDA(c, cudaMemset(*out, 0, c->scratch_off));
+  FC_CUDA(c, cudaMemset(*out, 0, c->scratch_off));  // control block + flags
+  // LL128 staging lives in its own zeroed region: a line's flag word only ever
+  // holds 0 or an epoch of this communicator, so a stale line can never match
+  FC_CUDA(c, cudaMemset(*out + c->scratch_off + c->scratch_bytes, 0, c->scratch_bytes));
   return FC_SUCCESS;
 }
 
@@ -149,7 +152,7 @@ int setup_layout(fc_comm* c, size_t scratch_bytes) {
                    2 * FC_MAXR;  // + NVLS entry/exit barrier words
   c->scratch_off = align_up(c->flags_off + c->flags_words * 4, 4096);
   c->scratch_bytes = align_up(scratch_bytes, 4096);
-  c->ws_bytes = c->scratch_off + c->scratch_bytes;
+  c->ws_bytes = c->scratch_off + 2 * c->scratch_bytes;  // reduction scratch + LL128 staging
   return FC_SUCCESS;
 }
 
@@ -302,11 +305,12 @@ int run(fc_comm* c, int coll, const void* const* sends, void* const* recvs, size
     const long long need = ag_base + (long long)pl.max_ag_slot_units * llu + 256LL * pl.max_ag_slots;
     const long long moved = (coll == FC_REDUCE_SCATTER) ? total * es : S * es * N;
     const bool want = c->proto == 1 || moved <= c->ll_max;
-    if (aligned && want && need <= (long long)c->scratch_bytes) {
+    if (aligned && want && need <= (long long)c->scratch_bytes) {  // LL region = scratch_bytes
       proto = 1;
       n = std::min<long long>(chunks_for(c->ll_chunk_max, c->ll_worker_warps), kMaxC);
       W = n;
       P.ll_unit_bytes = llu;
+      P.ll_region_off = (long long)c->scratch_bytes;
       P.ll_ag_base = ag_base;
       P.worker_warps = c->ll_worker_warps;
     } else if (c->proto == 1) {

@@ -762,7 +762,8 @@ __device__ void run_item_ll(const FcParams& P, int me, FcCtl* ctl, const int* T,
   const int g = lane >> 3, gl = lane & 7;
   const long long slot_ofs = -lw * 128LL;  // line l of the window at slot + (l - lw)*128
   auto slot_ptr = [&](int rank, long long region, int slot, int prefix) -> char* {
-    return P.scratch[rank] + region + P.ll_unit_bytes * prefix + 256LL * slot + slot_ofs;
+    return P.scratch[rank] + P.ll_region_off + region + P.ll_unit_bytes * prefix + 256LL * slot +
+           slot_ofs;
   };
   const bool polls = (kind == FC_K_AG_FWD || kind == FC_K_WAIT_AG);
   const char* my_ag = polls ? slot_ptr(me, P.ll_ag_base, __ldg(T + TW_AG_MYSLOT),

@@ -131,7 +131,8 @@ struct FcParams {
   int proto;            // 0: chunk flags + fences, 1: LL128 lines (flag in every 128 B)
   int pdl;              // launch with programmatic stream serialization
   long long ll_unit_bytes;  // LL: staging bytes per unit multiplicity per window
-  long long ll_ag_base;     // LL: scratch offset of the broadcast staging region
+  long long ll_ag_base;     // LL: offset of the broadcast staging within the LL region
+  long long ll_region_off;  // LL: offset of the (zeroed, dedicated) LL region from scratch
   FcTraceRec* trace;
   unsigned* trace_count;
   unsigned trace_cap;

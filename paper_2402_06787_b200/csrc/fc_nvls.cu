@@ -117,7 +117,7 @@ __global__ void __launch_bounds__(FC_NVLS_THREADS) fc_nvls_kernel(const __grid_c
     len = len < 0 ? 0 : (len > P.shard_bytes ? P.shard_bytes : len);
     const long long nv = len / 16;
     const long long stride = (long long)gridDim.x * blockDim.x;
-    constexpr int U = 4;
+    constexpr int U = 8;
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += stride * U) {
       uint4 v[U];
       if (P.mode == 0) {
