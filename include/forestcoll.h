@@ -79,8 +79,11 @@ extern "C" {
 #define FC_FLOAT64 8
 #define FC_BFLOAT16 9
 
-/* reduction ops: numbering follows ncclRedOp_t (only SUM is implemented) */
+/* reduction ops: numbering follows ncclRedOp_t (SUM and AVG are implemented).
+ * AVG (floating-point dtypes only): the tree root multiplies its fp32 sum by
+ * the fp32 value 1/N once, before the final rounding to the buffer dtype. */
 #define FC_SUM 0
+#define FC_AVG 4
 
 /* options for fc_comm_set_option */
 #define FC_OPT_CTAS_PER_RANK 1 /* CTAs per rank (default 128 real, 16 virtual) */
@@ -89,7 +92,7 @@ extern "C" {
 #define FC_OPT_ITEMS_PER_WORKER 4 /* target work items per CTA (default 4) */
 #define FC_OPT_TIMEOUT_MS 5    /* device flag-wait timeout (default 10000 ms) */
 #define FC_OPT_LAG 6           /* claim-order skew, chunks per tree stage (default 64) */
-#define FC_OPT_COPY_MODE 7     /* 0: TMA bulk stores, 1: TMA loads + vector stores (default 0) */
+#define FC_OPT_COPY_MODE 7     /* 0: TMA bulk stores, 1: TMA loads + vector stores (default 1) */
 #define FC_OPT_DMA_ROOT_COPY 8 /* allgather: copy engine places the own shard (default 0) */
 #define FC_OPT_WORKER_WARPS 9  /* warps per work item: 1, 2, 4, 8 (default 8 real, 1 virtual) */
 #define FC_OPT_PROTO 10        /* -1 auto, 0 chunk flags + fences, 1 LL128 lines (default -1) */

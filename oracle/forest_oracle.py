@@ -23,6 +23,9 @@ but ships no executor (pkg/tests/test_acceptance.py:
   order, accumulated in fp32 for fp32/bf16/fp16 and in wrapping int32 for
   int32, rounded to the buffer dtype once per hop; a node without children
   forwards its own slice unchanged.  The root's partial is its output.
+  op "avg" (floating-point dtypes): the root multiplies its fp32 sum by the
+  fp32 value 1/N once, before its final rounding (include/forestcoll.h
+  FC_AVG; NCCL-shaped ncclAvg, used by FSDP / DDP gradient averaging).
 * allreduce — reduce-scatter then allgather over one forest
   (schedule.py:177-211, combine_allreduce); the buffer of `count` elements
   is split into N root shards of S = align_up(ceil(count/N), 128 B / esize)
@@ -159,8 +162,17 @@ def allgather(schedule, sends: list[np.ndarray]) -> list[np.ndarray]:
     return outs
 
 
-def _reduce_tree(root, kids, get_own, dtype, pos):
-    """Post-order in-tree reduction; returns the root's partial."""
+def _root_scale(op: str, n: int, dtype: str):
+    if op == "sum":
+        return None
+    if op != "avg" or dtype not in ("float32", "bfloat16", "float16"):
+        raise ValueError(f"op {op!r} is not defined for dtype {dtype}")
+    return np.float32(1.0) / np.float32(n)
+
+
+def _reduce_tree(root, kids, get_own, dtype, pos, scale=None):
+    """Post-order in-tree reduction; returns the root's partial (scaled in
+    fp32 by `scale` before its rounding when given)."""
     order = _bfs(root, kids)
     partial = {}
     for v in reversed(order):
@@ -172,11 +184,13 @@ def _reduce_tree(root, kids, get_own, dtype, pos):
         acc = _to_acc(own, dtype)
         for c in ch:  # ascending rank order
             acc = _add(acc, _to_acc(partial[c], dtype), dtype)
+        if scale is not None and v == root:
+            acc = acc * scale  # float32 x float32: one IEEE round-to-nearest multiply
         partial[v] = _from_acc(acc, dtype, own)
     return partial[root]
 
 
-def reduce_scatter(schedule, inputs: list[np.ndarray], dtype: str) -> list[np.ndarray]:
+def reduce_scatter(schedule, inputs: list[np.ndarray], dtype: str, op: str = "sum") -> list[np.ndarray]:
     """inputs[r]: N*S elements -> outputs[r]: S elements (sum over ranks of
     inputs[*][r*S:(r+1)*S], tree order per the contract above)."""
     ids = rank_order(schedule)
@@ -184,12 +198,14 @@ def reduce_scatter(schedule, inputs: list[np.ndarray], dtype: str) -> list[np.nd
     pos = {x: i for i, x in enumerate(ids)}
     S = inputs[0].size // n
     k = schedule.k
+    scale = _root_scale(op, n, dtype)
     outs = [np.zeros(S, dtype=inputs[0].dtype) for _ in range(n)]
     for root, lo, hi, kids in trees(schedule, reverse=True):
         r = pos[root]
         a, b = slice_bounds(S, k, lo, hi)
         off = r * S
-        outs[r][a:b] = _reduce_tree(root, kids, lambda i: inputs[i][off + a:off + b], dtype, pos)
+        outs[r][a:b] = _reduce_tree(root, kids, lambda i: inputs[i][off + a:off + b], dtype, pos,
+                                    scale)
     return outs
 
 
@@ -199,7 +215,7 @@ def allreduce_shard(count: int, n: int, esize: int) -> int:
     return -(-s // a) * a
 
 
-def allreduce(schedule, inputs: list[np.ndarray], dtype: str) -> list[np.ndarray]:
+def allreduce(schedule, inputs: list[np.ndarray], dtype: str, op: str = "sum") -> list[np.ndarray]:
     rs, ag = schedule.phases
     ids = rank_order(schedule)
     n = len(ids)
@@ -207,6 +223,7 @@ def allreduce(schedule, inputs: list[np.ndarray], dtype: str) -> list[np.ndarray
     count = inputs[0].size
     S = allreduce_shard(count, n, inputs[0].itemsize)
     k = schedule.k
+    scale = _root_scale(op, n, dtype)
     outs = [np.zeros(count, dtype=inputs[0].dtype) for _ in range(n)]
     reduced = {}
     for root, lo, hi, kids in trees(rs, reverse=True):
@@ -215,7 +232,7 @@ def allreduce(schedule, inputs: list[np.ndarray], dtype: str) -> list[np.ndarray
         a, b = slice_bounds(sr, k, lo, hi)
         off = r * S
         reduced[(root, lo)] = _reduce_tree(root, kids, lambda i: inputs[i][off + a:off + b],
-                                           dtype, pos)
+                                           dtype, pos, scale)
     for root, lo, hi, kids in trees(ag, reverse=False):
         r = pos[root]
         sr = max(0, min(S, count - r * S))

@@ -43,6 +43,7 @@ struct Mapping {
 };
 struct Reg {
   uintptr_t lo, hi;
+  unsigned long long seq;  // registration number: equal on every rank (collective calls)
   char* peer[FC_MAXR];
 };
 struct Plan {
@@ -67,6 +68,7 @@ struct fc_comm {
   bool own[FC_MAXR] = {};
   std::vector<Mapping> maps;
   std::vector<Reg> regs;
+  unsigned long long reg_seq = 0;
   Plan plans[3];
   int ctas_per_rank = 64;
   long long chunk_max = 256 << 10, chunk_min = 16 << 10, items_per_worker = 4;
@@ -89,6 +91,9 @@ struct fc_comm {
   int nvls_bound = 0;
   int nvls_ctas = 32;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaEvent_t ev_last = nullptr;     // completion of the previous collective of this comm
+  cudaStream_t last_stream = nullptr;
+  bool have_last = false;
   FcTraceRec* trace = nullptr;
   unsigned* trace_count = nullptr;
   unsigned trace_cap = 0;
@@ -189,6 +194,32 @@ const Reg* find_reg(const fc_comm* c, const void* p, size_t bytes) {
   return nullptr;
 }
 
+// Collectives of one communicator share its control block, flags and scratch,
+// so they execute one at a time.  Calls on one stream are ordered by that
+// stream; a call issued on another stream (FSDP's all-gather and
+// reduce-scatter streams, say) first waits for the previous call's completion
+// event.  Issue order is the same on every rank of an SPMD program, so every
+// rank runs the same sequence (the ordering NCCL keeps per communicator).
+// Inside CUDA-graph capture the graph's own edges order the calls.
+bool capturing(cudaStream_t s) {
+  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+  return cudaStreamIsCapturing(s, &st) == cudaSuccess && st != cudaStreamCaptureStatusNone;
+}
+
+int order_begin(fc_comm* c, cudaStream_t s) {
+  if (c->have_last && s != c->last_stream && !capturing(s))
+    FC_CUDA(c, cudaStreamWaitEvent(s, c->ev_last, 0));
+  return FC_SUCCESS;
+}
+
+int order_end(fc_comm* c, cudaStream_t s) {
+  if (capturing(s)) return FC_SUCCESS;
+  FC_CUDA(c, cudaEventRecord(c->ev_last, s));
+  c->last_stream = s;
+  c->have_last = true;
+  return FC_SUCCESS;
+}
+
 // Run one collective over this comm's local ranks.
 int run(fc_comm* c, int coll, const void* const* sends, void* const* recvs, size_t count,
         int dtype, int op, void* stream) {
@@ -203,7 +234,10 @@ int run(fc_comm* c, int coll, const void* const* sends, void* const* recvs, size
   if (coll != FC_ALLGATHER) {
     rd = reduce_kind(dtype);
     if (rd < 0) return fail(c, FC_ERR_UNSUPPORTED, "dtype %d cannot be reduced", dtype);
-    if (op != FC_SUM) return fail(c, FC_ERR_UNSUPPORTED, "reduction op %d unsupported", op);
+    if (op != FC_SUM && op != FC_AVG)
+      return fail(c, FC_ERR_UNSUPPORTED, "reduction op %d unsupported", op);
+    if (op == FC_AVG && rd == FC_INT32)
+      return fail(c, FC_ERR_UNSUPPORTED, "AVG is implemented for floating-point dtypes only");
   }
   const int N = c->nranks;
   long long S, stride, total;
@@ -253,6 +287,9 @@ int run(fc_comm* c, int coll, const void* const* sends, void* const* recvs, size
     const size_t delta = (uintptr_t)recvs[0] - reg->lo;
     for (int r = 0; r < N; ++r)
       if (!c->is_local[r]) P.recv[r] = reg->peer[r] + delta;
+    // identity of the output every peer must be writing to in this call
+    P.tag = (reg->seq * 0x9E3779B97F4A7C15ull) ^ ((unsigned long long)delta * 0xC2B2AE3D27D4EB4Full) ^
+            (unsigned long long)need;
   }
   P.shard_elems = S;
   P.stride_elems = stride;
@@ -260,6 +297,7 @@ int run(fc_comm* c, int coll, const void* const* sends, void* const* recvs, size
   P.esize = es;
   P.dtype = dtype;
   P.op = op;
+  P.scale = 1.0f / (float)c->nranks;
   P.maxc = kMaxC;
   P.cnt_off = FC_READY_WORDS;
   P.ag_flag_off = FC_READY_WORDS + kTreeCap;
@@ -339,6 +377,10 @@ int run(fc_comm* c, int coll, const void* const* sends, void* const* recvs, size
   P.proto = proto;
   const int coop = c->nlocal > 1 ? 1 : 0;  // local ranks wait on each other in one grid
   int launches = 0, grid = 0;
+  {
+    const int st = order_begin(c, (cudaStream_t)stream);
+    if (st) return st;
+  }
   // allgather: a copy engine places each local root's own shard into its
   // output concurrently with the kernel (no SM bandwidth spent on it)
   bool dma = false;
@@ -359,12 +401,20 @@ int run(fc_comm* c, int coll, const void* const* sends, void* const* recvs, size
   for (long long c0 = 0; c0 < n; c0 += W) {
     P.c0 = (int)c0;
     P.c1 = (int)std::min(n, c0 + W);
+    // The claim-order skew only has to exceed the chunk span of the window to
+    // keep every item's dependencies earlier in key order; a larger lag just
+    // adds empty claims (stages x lag of them), which dominate tiny messages.
+    P.lag = (int)std::min<long long>(c->lag, P.c1 - P.c0);
     const int e = fc_launch(P, rd, coop, stream, &grid);
     if (e != 0)
       return fail(c, FC_ERR_CUDA, "kernel launch failed: %s", cudaGetErrorString((cudaError_t)e));
     ++launches;
   }
   if (dma) FC_CUDA(c, cudaStreamWaitEvent((cudaStream_t)stream, c->ev_join, 0));
+  {
+    const int st = order_end(c, (cudaStream_t)stream);
+    if (st) return st;
+  }
   c->info[0] = launches;
   c->info[1] = n;
   c->info[2] = W;
@@ -386,6 +436,7 @@ int free_plan(fc_comm* c, Plan& p) {
 }
 
 int make_side_stream(fc_comm* c) {
+  FC_CUDA(c, cudaEventCreateWithFlags(&c->ev_last, cudaEventDisableTiming));
   FC_CUDA(c, cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
   FC_CUDA(c, cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
   FC_CUDA(c, cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
@@ -485,7 +536,7 @@ CUmulticastObjectProp mc_prop(fc_comm* c, size_t bytes) {
 }
 
 int run_nvls(fc_comm* c, int mode, const void* send, void* buf, void* out, size_t count, int dtype,
-             void* stream) {
+             int op, void* stream) {
   if (!c || !c->nvls_bound) return fail(c, FC_ERR_INVALID_ARG, "NVLS pool is not set up");
   const int es = esize_of(dtype);
   if (!es) return fail(c, FC_ERR_INVALID_ARG, "unknown dtype %d", dtype);
@@ -493,6 +544,10 @@ int run_nvls(fc_comm* c, int mode, const void* send, void* buf, void* out, size_
   if (mode != 0) {
     rd = reduce_kind(dtype);
     if (rd < 0) return fail(c, FC_ERR_UNSUPPORTED, "dtype %d cannot be reduced", dtype);
+    if (op != FC_SUM && op != FC_AVG)
+      return fail(c, FC_ERR_UNSUPPORTED, "reduction op %d unsupported", op);
+    if (op == FC_AVG && rd == FC_INT32)
+      return fail(c, FC_ERR_UNSUPPORTED, "AVG is implemented for floating-point dtypes only");
   }
   const uintptr_t b = (uintptr_t)buf, lo = (uintptr_t)c->nvls_uc_va;
   const int N = c->nranks;
@@ -518,6 +573,8 @@ int run_nvls(fc_comm* c, int mode, const void* send, void* buf, void* out, size_
   P.rank = c->rank;
   P.mode = mode;
   P.dtype = rd;
+  P.op = mode == 0 ? FC_SUM : op;
+  P.scale = 1.0f / (float)N;
   P.bar_off = (int)(c->flags_words - 2 * FC_MAXR);
   P.ctl = (FcCtl*)c->ws[c->rank];
   for (int r = 0; r < N; ++r) P.flags[r] = (unsigned*)(c->ws[r] + c->flags_off);
@@ -527,8 +584,16 @@ int run_nvls(fc_comm* c, int mode, const void* send, void* buf, void* out, size_
   P.shard_bytes = shard;
   P.total_bytes = total;
   P.timeout_ns = c->timeout_ms * 1000000LL;
+  {
+    const int st = order_begin(c, (cudaStream_t)stream);
+    if (st) return st;
+  }
   const int e = fc_nvls_launch(P, c->nvls_ctas, stream);
   if (e) return fail(c, FC_ERR_CUDA, "NVLS launch failed: %s", cudaGetErrorString((cudaError_t)e));
+  {
+    const int st = order_end(c, (cudaStream_t)stream);
+    if (st) return st;
+  }
   c->info[0] = 1;
   c->info[5] = 2;  // engine: nvls
   return FC_SUCCESS;
@@ -787,8 +852,13 @@ int fc_comm_check(fc_comm_t* c, int* device_error) {
     FC_CUDA(c, cudaMemcpy(&ctl, c->ws[r], sizeof(ctl), cudaMemcpyDeviceToHost));
     if (ctl.error && !worst) {
       worst = (int)ctl.error;
-      fail(c, FC_ERR_DEVICE, "rank %d: device error %u (flag wait timed out; epoch %u, value %u)",
-           r, ctl.error, ctl.info[1], ctl.info[2]);
+      if (ctl.error == FC_DEVERR_BUFFER_MISMATCH)
+        fail(c, FC_ERR_DEVICE,
+             "rank %d: device error %u (rank %u passed a different output buffer: every rank "
+             "must pass the same registered buffer, offset and size)", r, ctl.error, ctl.info[0]);
+      else
+        fail(c, FC_ERR_DEVICE, "rank %d: device error %u (flag wait timed out; epoch %u, value %u)",
+             r, ctl.error, ctl.info[1], ctl.info[2]);
     }
   }
   if (device_error) *device_error = worst;
@@ -814,6 +884,7 @@ int fc_comm_destroy(fc_comm_t* c) {
   if (c->nvls_mc) drv().memRelease(c->nvls_mc);
   if (c->side) cudaStreamDestroy(c->side);
   if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+  if (c->ev_last) cudaEventDestroy(c->ev_last);
   if (c->ev_join) cudaEventDestroy(c->ev_join);
   for (int r = 0; r < FC_MAXR; ++r)
     if (c->own[r]) cudaFree(c->ws[r]);
@@ -883,6 +954,7 @@ int fc_buffer_register_multi(fc_comm_t* c, const void* const* ptrs, size_t bytes
     if (st) return st;
     reg.peer[r] = base + b.offset;
   }
+  reg.seq = ++c->reg_seq;
   for (auto& r : c->regs)
     if (r.lo == reg.lo) {  // same base: keep the widest registered extent
       if (reg.hi > r.hi) r = reg;
@@ -1126,16 +1198,14 @@ int fc_nvls_bind(fc_comm_t* c, void** pool) {
 
 int fc_nvls_allgather(fc_comm_t* c, const void* send, void* recv, size_t sendcount, int dtype,
                       void* stream) {
-  return run_nvls(c, 0, send, recv, nullptr, sendcount, dtype, stream);
+  return run_nvls(c, 0, send, recv, nullptr, sendcount, dtype, FC_SUM, stream);
 }
 int fc_nvls_reduce_scatter(fc_comm_t* c, const void* send, void* recv, size_t recvcount,
                            int dtype, int op, void* stream) {
-  if (op != FC_SUM) return fail(c, FC_ERR_UNSUPPORTED, "reduction op %d unsupported", op);
-  return run_nvls(c, 1, nullptr, (void*)send, recv, recvcount, dtype, stream);
+  return run_nvls(c, 1, nullptr, (void*)send, recv, recvcount, dtype, op, stream);
 }
 int fc_nvls_allreduce(fc_comm_t* c, void* buf, size_t count, int dtype, int op, void* stream) {
-  if (op != FC_SUM) return fail(c, FC_ERR_UNSUPPORTED, "reduction op %d unsupported", op);
-  return run_nvls(c, 2, nullptr, buf, nullptr, count, dtype, stream);
+  return run_nvls(c, 2, nullptr, buf, nullptr, count, dtype, op, stream);
 }
 
 }  // extern "C"

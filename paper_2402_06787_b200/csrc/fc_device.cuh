@@ -71,6 +71,9 @@ __device__ __forceinline__ void red_release_sys_add(unsigned* p, unsigned v) {
 __device__ __forceinline__ unsigned ld_volatile(const unsigned* p) {
   return *reinterpret_cast<const volatile unsigned*>(p);
 }
+__device__ __forceinline__ void st_volatile(unsigned* p, unsigned v) {
+  *reinterpret_cast<volatile unsigned*>(p) = v;
+}
 __device__ __forceinline__ void fence_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
 // Barrier of one worker (WW warps): a warp barrier or a named CTA barrier
 // (id 0 is __syncthreads).
@@ -154,6 +157,26 @@ __device__ bool spin_geq(const unsigned* p, unsigned e, FcCtl* ctl, long long ti
   }
 }
 
+// Wait until destination rank x has entered launch e.  While x is in launch
+// e (it cannot leave it before receiving from us), the output-buffer tag it
+// published with its ready epoch must equal ours: a rank that passed a
+// differently registered buffer (or offset / size) fails loudly instead of
+// receiving stores meant for another buffer.
+__device__ bool wait_ready(const FcParams& P, int me, int x, unsigned e, FcCtl* ctl) {
+  const unsigned* f = P.flags[me];
+  if (!spin_geq(f + x, e, ctl, P.timeout_ns, FC_DEVERR_TIMEOUT_READY)) return false;
+  if (ld_acquire_sys(f + x) != e) return true;
+  const unsigned long long t = (unsigned long long)ld_volatile(f + FC_TAG_WORD + 2 * x) |
+                               ((unsigned long long)ld_volatile(f + FC_TAG_WORD + 2 * x + 1) << 32);
+  if (t == P.tag) return true;
+  if (atomicCAS(&ctl->error, 0u, (unsigned)FC_DEVERR_BUFFER_MISMATCH) == 0u) {
+    ctl->info[0] = (unsigned)x;
+    ctl->info[1] = (unsigned)P.tag;
+    ctl->info[2] = (unsigned)t;
+  }
+  return false;
+}
+
 // ---------------------------------------------------------------------------
 // Element arithmetic.  Accumulation type A; buffer element E.
 // ---------------------------------------------------------------------------
@@ -167,6 +190,7 @@ struct Red<FC_FLOAT32> {
   __device__ static A to(E x) { return __uint_as_float(x); }
   __device__ static E from(A a) { return __float_as_uint(a); }
   __device__ static A add(A a, A b) { return __fadd_rn(a, b); }
+  __device__ static A mul(A a, float s) { return __fmul_rn(a, s); }
 };
 
 // bf16: fp32 accumulate, one round-to-nearest-even per hop.  NaN is quieted
@@ -183,6 +207,7 @@ struct Red<FC_BFLOAT16> {
     return (E)(u >> 16);
   }
   __device__ static A add(A a, A b) { return __fadd_rn(a, b); }
+  __device__ static A mul(A a, float s) { return __fmul_rn(a, s); }
 };
 
 template <>
@@ -192,6 +217,7 @@ struct Red<FC_FLOAT16> {
   __device__ static A to(E x) { return __half2float(__ushort_as_half(x)); }
   __device__ static E from(A a) { return __half_as_ushort(__float2half_rn(a)); }
   __device__ static A add(A a, A b) { return __fadd_rn(a, b); }
+  __device__ static A mul(A a, float s) { return __fmul_rn(a, s); }
 };
 
 template <>
@@ -201,6 +227,7 @@ struct Red<FC_INT32> {  // also uint32: wrapping two's-complement add
   __device__ static A to(E x) { return x; }
   __device__ static E from(A a) { return a; }
   __device__ static A add(A a, A b) { return a + b; }
+  __device__ static A mul(A a, float) { return a; }  // AVG is rejected for integers
 };
 
 // acc (accumulator lanes of one 16-byte vector) <- first source
@@ -219,6 +246,10 @@ struct Acc16 {
     const E* e = reinterpret_cast<const E*>(&v);
 #pragma unroll
     for (int q = 0; q < NE; ++q) a[q] = R::add(a[q], R::to(e[q]));
+  }
+  __device__ __forceinline__ void scale(float s) {
+#pragma unroll
+    for (int q = 0; q < NE; ++q) a[q] = R::mul(a[q], s);
   }
   __device__ __forceinline__ uint4 pack() const {
     uint4 out;
@@ -245,6 +276,10 @@ struct Acc8 {
     const E* e = reinterpret_cast<const E*>(&v);
 #pragma unroll
     for (int q = 0; q < NE; ++q) a[q] = R::add(a[q], R::to(e[q]));
+  }
+  __device__ __forceinline__ void scale(float s) {
+#pragma unroll
+    for (int q = 0; q < NE; ++q) a[q] = R::mul(a[q], s);
   }
   __device__ __forceinline__ unsigned long long pack() const {
     unsigned long long out;
@@ -325,9 +360,9 @@ __device__ void warp_copy(const char* src, char* const* dst, int ndst, long long
   }
 }
 
-template <int DT>
+template <int DT, bool SC>
 __device__ void warp_reduce_scalar(const char* const* src, int nsrc, char* const* dst, int ndst,
-                                   long long off, long long nelem, int lane) {
+                                   long long off, long long nelem, int lane, bool scaled, float sc) {
   using R = Red<DT>;
   using E = typename R::E;
   for (long long i = lane; i < nelem; i += 32) {
@@ -335,18 +370,24 @@ __device__ void warp_reduce_scalar(const char* const* src, int nsrc, char* const
     typename R::A acc = R::to(__ldcg(reinterpret_cast<const E*>(src[0] + b)));
     for (int s = 1; s < nsrc; ++s)
       acc = R::add(acc, R::to(__ldcg(reinterpret_cast<const E*>(src[s] + b))));
+    if constexpr (SC) {
+      if (scaled) acc = R::mul(acc, sc);
+    }
     const E out = R::from(acc);
     for (int d = 0; d < ndst; ++d) *reinterpret_cast<E*>(dst[d] + b) = out;
   }
 }
 
-template <int DT>
+template <int DT, bool SC>
 __device__ void warp_reduce_vec(const char* const* src, int nsrc, char* const* dst, int ndst,
-                                long long off, long long nvec, int lane) {
+                                long long off, long long nvec, int lane, bool scaled, float sc) {
   for (long long i = lane; i < nvec; i += 32) {
     Acc16<DT> acc;
     acc.init(__ldcg(reinterpret_cast<const uint4*>(src[0] + off) + i));
     for (int s = 1; s < nsrc; ++s) acc.add(__ldcg(reinterpret_cast<const uint4*>(src[s] + off) + i));
+    if constexpr (SC) {
+      if (scaled) acc.scale(sc);
+    }
     const uint4 out = acc.pack();
     for (int d = 0; d < ndst; ++d) reinterpret_cast<uint4*>(dst[d] + off)[i] = out;
   }
@@ -447,9 +488,9 @@ __device__ void bulk_copy_stg(Ring& rg, const char* src, char* const* dst, int n
 
 // Reduce `nbytes` (all pointers 16-aligned, multiple of 16): sources are
 // bulk-loaded into the ring, 32 lanes sum them and store 16-byte vectors.
-template <int DT>
+template <int DT, bool SC>
 __device__ void bulk_reduce(Ring& rg, const char* const* src, int nsrc, char* const* dst,
-                            int ndst, long long nbytes, int lane) {
+                            int ndst, long long nbytes, int lane, bool scaled, float sc) {
   const long long seg = (long long)(FC_STAGE / nsrc) & ~15LL;  // bytes per source per piece
   const long long npieces = (nbytes + seg - 1) / seg;
   const unsigned base = rg.seq;
@@ -473,6 +514,9 @@ __device__ void bulk_reduce(Ring& rg, const char* const* src, int nsrc, char* co
       Acc16<DT> acc;
       acc.init(reinterpret_cast<const uint4*>(sb)[j]);
       for (int s = 1; s < nsrc; ++s) acc.add(reinterpret_cast<const uint4*>(sb + s * seg)[j]);
+      if constexpr (SC) {
+        if (scaled) acc.scale(sc);
+      }
       const uint4 out = acc.pack();
       for (int d = 0; d < ndst; ++d) reinterpret_cast<uint4*>(dst[d] + off)[j] = out;
     }
@@ -505,9 +549,12 @@ __device__ __forceinline__ long long chunk_bound(const Geo& g, int c, int n) {
   return b < g.lo ? g.lo : b;
 }
 
-template <int DT>
+// SC (AVG kernels only): when `scaled` (a root item), the fp32 sum is
+// multiplied by `sc` before the final rounding.  SUM kernels compile it out.
+template <int DT, bool SC>
 __device__ void move(Ring& rg, const char* const* src, int ns, char* const* dst, int nd,
-                     long long nbytes, int esize, int lane, int copy_mode, bool& used_bulk) {
+                     long long nbytes, int esize, int lane, int copy_mode, bool& used_bulk,
+                     bool scaled, float sc) {
   if (nbytes <= 0 || nd <= 0) return;
   const uintptr_t a0 = (uintptr_t)src[0];
   uintptr_t diff = 0;
@@ -535,7 +582,7 @@ __device__ void move(Ring& rg, const char* const* src, int ns, char* const* dst,
   if ((diff & 15) == 0) {
     long long head = (long long)((16 - (a0 & 15)) & 15);
     if (head > nbytes) head = nbytes;
-    warp_reduce_scalar<DT>(src, ns, dst, nd, 0, head / esize, lane);
+    warp_reduce_scalar<DT, SC>(src, ns, dst, nd, 0, head / esize, lane, scaled, sc);
     const long long body = (nbytes - head) & ~15LL;
     if (body > 0) {
       const char* s1[FC_MAXS];
@@ -543,14 +590,14 @@ __device__ void move(Ring& rg, const char* const* src, int ns, char* const* dst,
       for (int s = 0; s < ns; ++s) s1[s] = src[s] + head;
       for (int d = 0; d < nd; ++d) d1[d] = dst[d] + head;
       if (ns <= 8 && body >= 1024)
-        bulk_reduce<DT>(rg, s1, ns, d1, nd, body, lane);
+        bulk_reduce<DT, SC>(rg, s1, ns, d1, nd, body, lane, scaled, sc);
       else
-        warp_reduce_vec<DT>(s1, ns, d1, nd, 0, body / 16, lane);
+        warp_reduce_vec<DT, SC>(s1, ns, d1, nd, 0, body / 16, lane, scaled, sc);
     }
     const long long t0 = head + body;
-    warp_reduce_scalar<DT>(src, ns, dst, nd, t0, (nbytes - t0) / esize, lane);
+    warp_reduce_scalar<DT, SC>(src, ns, dst, nd, t0, (nbytes - t0) / esize, lane, scaled, sc);
   } else {
-    warp_reduce_scalar<DT>(src, ns, dst, nd, 0, nbytes / esize, lane);
+    warp_reduce_scalar<DT, SC>(src, ns, dst, nd, 0, nbytes / esize, lane, scaled, sc);
   }
 }
 
@@ -563,7 +610,7 @@ struct ItemShared {
 // One item (task, chunk) executed by the whole CTA: thread 0 waits for the
 // inputs, every warp moves a 128-byte-aligned 1/FC_WW sub-range through its
 // own bulk ring, and thread 0 publishes after a CTA barrier.
-template <int DT, int WW>
+template <int DT, int WW, bool AVG>
 __device__ void run_item(const FcParams& P, int me, FcCtl* ctl, const int* T, int c,
                          unsigned e, int w, int lane, unsigned& ready_mask, Ring& rg,
                          ItemShared* sh, unsigned long long& t_ready,
@@ -613,7 +660,7 @@ __device__ void run_item(const FcParams& P, int me, FcCtl* ctl, const int* T, in
       for (int j = 0; j < nx && ok; ++j) {
         const int x = (kind == FC_K_RS_FWD) ? rs_parent : __ldg(T + TW_AG_CHILD + j);
         if (!((ready_mask >> x) & 1u)) {
-          ok = spin_geq(myflags + x, e, ctl, P.timeout_ns, FC_DEVERR_TIMEOUT_READY);
+          ok = wait_ready(P, me, x, e, ctl);
           if (ok) ready_mask |= 1u << x;
         }
       }
@@ -654,7 +701,9 @@ __device__ void run_item(const FcParams& P, int me, FcCtl* ctl, const int* T, in
     }
   }
   bool used_bulk = false;
-  move<DT>(rg, src, ns, dst, nd, s1 - s0, P.esize, lane, P.copy_mode, used_bulk);
+  // AVG: the root scales its fp32 sum once, before the final rounding
+  move<DT, AVG>(rg, src, ns, dst, nd, s1 - s0, P.esize, lane, P.copy_mode, used_bulk,
+                AVG && (kind == FC_K_RS_ROOT || kind == FC_K_AR_ROOT), P.scale);
   if (used_bulk && lane == 0) {
     bulk_wait_all();
     fence_proxy_async_global();
@@ -716,7 +765,7 @@ __device__ __forceinline__ bool ll_poll(const char* const* line, const bool* val
 // One item in the LL protocol.  Lines of the chunk are dealt to the worker's
 // warps 4*FC_LL_UNROLL at a time; lane group g (8 lanes) handles one 128-byte
 // line per batch, with all batches' loads in flight together.
-template <int DT, int WW>
+template <int DT, int WW, bool AVG>
 __device__ void run_item_ll(const FcParams& P, int me, FcCtl* ctl, const int* T, int c,
                             unsigned e, int w, int lane, unsigned& ready_mask, ItemShared* sh,
                             unsigned long long& t_ready) {
@@ -748,7 +797,7 @@ __device__ void run_item_ll(const FcParams& P, int me, FcCtl* ctl, const int* T,
       for (int j = 0; j < nx && ok; ++j) {
         const int x = (kind == FC_K_RS_FWD) ? rs_parent : __ldg(T + TW_AG_CHILD + j);
         if (!((ready_mask >> x) & 1u)) {
-          ok = spin_geq(P.flags[me] + x, e, ctl, P.timeout_ns, FC_DEVERR_TIMEOUT_READY);
+          ok = wait_ready(P, me, x, e, ctl);
           if (ok) ready_mask |= 1u << x;
         }
       }
@@ -827,6 +876,13 @@ __device__ void run_item_ll(const FcParams& P, int me, FcCtl* ctl, const int* T,
             a1[u].add(x1[u]);
           }
         }
+        if (AVG && kind != FC_K_RS_FWD) {  // root: scale the fp32 sum once
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            a0[u].scale(P.scale);
+            a1[u].scale(P.scale);
+          }
+        }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           w0[u] = a0[u].pack();
@@ -863,7 +919,7 @@ __device__ void run_item_ll(const FcParams& P, int me, FcCtl* ctl, const int* T,
   worker_sync<WW>(wk);
 }
 
-template <int DT, int WW, int PROTO>
+template <int DT, int WW, int PROTO, bool AVG>
 __global__ void __launch_bounds__(FC_BLOCK, 1) fc_forest_kernel(const __grid_constant__ FcParams P) {
   constexpr int FC_NWK = FC_WPC / WW;
   extern __shared__ __align__(128) char smem[];
@@ -883,9 +939,14 @@ __global__ void __launch_bounds__(FC_BLOCK, 1) fc_forest_kernel(const __grid_con
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   __syncthreads();
   const unsigned e = s_epoch;
-  // entry barrier: tell every peer that this rank entered launch e
-  if ((int)threadIdx.x < P.nranks && (int)threadIdx.x != me)
-    st_release_sys(P.flags[threadIdx.x] + me, e);
+  // entry barrier: tell every peer that this rank entered launch e, and with
+  // which output buffer (the tag store is ordered before the release)
+  if ((int)threadIdx.x < P.nranks && (int)threadIdx.x != me) {
+    unsigned* pf = P.flags[threadIdx.x];
+    st_volatile(pf + FC_TAG_WORD + 2 * me, (unsigned)P.tag);
+    st_volatile(pf + FC_TAG_WORD + 2 * me + 1, (unsigned)(P.tag >> 32));
+    st_release_sys(pf + me, e);
+  }
 
   const int wk = w / WW;
   const bool lead = (w % WW == 0) && lane == 0;
@@ -930,10 +991,10 @@ __global__ void __launch_bounds__(FC_BLOCK, 1) fc_forest_kernel(const __grid_con
     const unsigned long long t0 = trace ? globaltimer() : 0;
     unsigned long long t_ready = t0, t_moved = t0;
     if constexpr (PROTO == 1)
-      run_item_ll<DT, WW>(P, me, ctl, tasks + (long long)ti * FC_TASK_WORDS, P.c0 + c, e, w,
+      run_item_ll<DT, WW, AVG>(P, me, ctl, tasks + (long long)ti * FC_TASK_WORDS, P.c0 + c, e, w,
                           lane, ready_mask, &sh, t_ready);
     else
-      run_item<DT, WW>(P, me, ctl, tasks + (long long)ti * FC_TASK_WORDS, P.c0 + c, e, w, lane,
+      run_item<DT, WW, AVG>(P, me, ctl, tasks + (long long)ti * FC_TASK_WORDS, P.c0 + c, e, w, lane,
                        ready_mask, rg, &sh, t_ready, t_moved);
     if (trace && lead) {
       const unsigned idx = atomicAdd(P.trace_count, 1u);
@@ -970,21 +1031,21 @@ __global__ void __launch_bounds__(FC_BLOCK, 1) fc_forest_kernel(const __grid_con
 
 }  // namespace
 
-// Kernel pointer for one (dtype, worker warps, protocol) instantiation.
-#define FC_DEFINE_KERNEL_TABLE(NAME, DT)                                          \
+// Kernel pointer for one (dtype, worker warps, protocol, AVG) instantiation.
+#define FC_DEFINE_KERNEL_TABLE(NAME, DT, AVG)                                     \
   const void* NAME(int ww, int proto) {                                           \
     if (proto) {                                                                  \
       switch (ww) {                                                               \
-        case 1: return (const void*)fc_forest_kernel<DT, 1, 1>;                   \
-        case 2: return (const void*)fc_forest_kernel<DT, 2, 1>;                   \
-        case 4: return (const void*)fc_forest_kernel<DT, 4, 1>;                   \
-        default: return (const void*)fc_forest_kernel<DT, 8, 1>;                  \
+        case 1: return (const void*)fc_forest_kernel<DT, 1, 1, AVG>;              \
+        case 2: return (const void*)fc_forest_kernel<DT, 2, 1, AVG>;              \
+        case 4: return (const void*)fc_forest_kernel<DT, 4, 1, AVG>;              \
+        default: return (const void*)fc_forest_kernel<DT, 8, 1, AVG>;             \
       }                                                                           \
     }                                                                             \
     switch (ww) {                                                                 \
-      case 1: return (const void*)fc_forest_kernel<DT, 1, 0>;                     \
-      case 2: return (const void*)fc_forest_kernel<DT, 2, 0>;                     \
-      case 4: return (const void*)fc_forest_kernel<DT, 4, 0>;                     \
-      default: return (const void*)fc_forest_kernel<DT, 8, 0>;                    \
+      case 1: return (const void*)fc_forest_kernel<DT, 1, 0, AVG>;                \
+      case 2: return (const void*)fc_forest_kernel<DT, 2, 0, AVG>;                \
+      case 4: return (const void*)fc_forest_kernel<DT, 4, 0, AVG>;                \
+      default: return (const void*)fc_forest_kernel<DT, 8, 0, AVG>;               \
     }                                                                             \
   }

@@ -8,6 +8,8 @@
 #define FC_MAXR FC_MAX_RANKS
 #define FC_ALIGN 128          // chunk boundaries / scratch phase alignment (bytes)
 #define FC_READY_WORDS 64     // flags[0..nranks): entry (ready) epochs per peer
+#define FC_TAG_WORD 32        // flags[32 + 2r, +1]: rank r's output-buffer tag of its
+                              // current launch (written before its ready epoch)
 #define FC_TABLE_MAGIC 0x50434c46  // 'FLCP'
 #define FC_TABLE_VERSION 1
 #define FC_HEADER_WORDS 16
@@ -81,6 +83,7 @@ struct FcCtl {
 #define FC_DEVERR_TIMEOUT_AG 1
 #define FC_DEVERR_TIMEOUT_RS 2
 #define FC_DEVERR_TIMEOUT_READY 3
+#define FC_DEVERR_BUFFER_MISMATCH 4  // peers passed differently registered outputs
 
 // One record per executed item when tracing is enabled (fc_comm_set_trace).
 struct FcTraceRec {
@@ -117,7 +120,9 @@ struct FcParams {
   long long timeout_ns;
   int esize;
   int dtype;
-  int op;
+  int op;       // FC_SUM or FC_AVG
+  float scale;  // FC_AVG: fp32 1/N applied once by tree roots
+  unsigned long long tag;  // identity of the peer-mapped output (registration, offset, size)
   int nchunks;  // chunks per tree slice for the whole call
   int c0, c1;   // chunk window of this launch
   int maxc;     // flag stride per tree / slot
@@ -143,6 +148,8 @@ struct FcParams {
 // (schedule.py:237-306): every root writes its shard once into the switch.
 struct FcNvlsParams {
   int nranks, rank, mode, dtype;  // mode: 0 allgather, 1 reduce-scatter, 2 allreduce
+  int op;                         // FC_SUM or FC_AVG
+  float scale;                    // FC_AVG: fp32 1/N
   int bar_off;                    // word offset of the NVLS barrier words (2 * FC_MAXR)
   FcCtl* ctl;
   unsigned int* flags[FC_MAXR];

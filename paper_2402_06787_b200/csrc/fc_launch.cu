@@ -11,22 +11,25 @@ const void* fc_kernel_ptr_f32(int ww, int proto);
 const void* fc_kernel_ptr_bf16(int ww, int proto);
 const void* fc_kernel_ptr_f16(int ww, int proto);
 const void* fc_kernel_ptr_i32(int ww, int proto);
+const void* fc_kernel_ptr_f32_avg(int ww, int proto);
+const void* fc_kernel_ptr_bf16_avg(int ww, int proto);
+const void* fc_kernel_ptr_f16_avg(int ww, int proto);
 
 namespace {
 
-const void* kernel_for(int rd, int ww, int proto) {
+const void* kernel_for(int rd, int ww, int proto, bool avg) {
   switch (rd) {
-    case FC_BFLOAT16: return fc_kernel_ptr_bf16(ww, proto);
-    case FC_FLOAT16: return fc_kernel_ptr_f16(ww, proto);
-    case FC_INT32: return fc_kernel_ptr_i32(ww, proto);
-    default: return fc_kernel_ptr_f32(ww, proto);
+    case FC_BFLOAT16: return avg ? fc_kernel_ptr_bf16_avg(ww, proto) : fc_kernel_ptr_bf16(ww, proto);
+    case FC_FLOAT16: return avg ? fc_kernel_ptr_f16_avg(ww, proto) : fc_kernel_ptr_f16(ww, proto);
+    case FC_INT32: return fc_kernel_ptr_i32(ww, proto);  // AVG rejected for integers
+    default: return avg ? fc_kernel_ptr_f32_avg(ww, proto) : fc_kernel_ptr_f32(ww, proto);
   }
 }
 
 int smem_for(int proto) { return proto ? 0 : FC_SMEM_BYTES; }  // LL128 keeps no smem ring
 
 int ensure_smem_attr(const void* fn) {
-  static const void* done[64] = {};
+  static const void* done[128] = {};
   for (auto& d : done) {
     if (d == fn) return 0;
     if (!d) {
@@ -45,7 +48,7 @@ int ensure_smem_attr(const void* fn) {
 int fc_launch(const FcParams& p, int reduce_dtype, int cooperative, void* stream, int* grid_out) {
   const dim3 grid(p.nlocal * p.ctas_per_rank), block(FC_BLOCK);
   void* args[] = {(void*)&p};
-  const void* fn = kernel_for(reduce_dtype, p.worker_warps, p.proto);
+  const void* fn = kernel_for(reduce_dtype, p.worker_warps, p.proto, p.op == FC_AVG);
   if (grid_out) *grid_out = (int)grid.x;
   const int a = ensure_smem_attr(fn);
   if (a) return a;
@@ -76,7 +79,7 @@ int fc_launch(const FcParams& p, int reduce_dtype, int cooperative, void* stream
 int fc_max_ctas_per_sm(int reduce_dtype, int* out) {
   int best = 1 << 30;
   for (int proto = 0; proto < 2; ++proto) {
-    const void* fn = kernel_for(reduce_dtype, 8, proto);
+    const void* fn = kernel_for(reduce_dtype, 8, proto, false);
     const int a = ensure_smem_attr(fn);
     if (a) return a;
     int v = 0;

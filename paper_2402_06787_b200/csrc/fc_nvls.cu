@@ -15,6 +15,8 @@
 // In-switch fp reductions use the switch's accumulation order (fp32
 // accumulate for bf16/fp16), so fp results match the tree oracle only within
 // tolerance; int32 sums are exact.
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include <climits>
@@ -96,6 +98,30 @@ __device__ __forceinline__ uint4 mm_ld_reduce(const char* p) {
   return r;
 }
 
+// AVG on the NVLS path: the switch's sum (already in the buffer dtype) is
+// multiplied by the fp32 1/N and rounded again (NVLS fp results are compared
+// within tolerance, see the header comment).
+template <int DT>
+__device__ __forceinline__ void scale16(uint4& v, float s) {
+  unsigned* w = reinterpret_cast<unsigned*>(&v);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    if constexpr (DT == FC_FLOAT32) {
+      w[i] = __float_as_uint(__fmul_rn(__uint_as_float(w[i]), s));
+    } else if constexpr (DT == FC_BFLOAT16) {
+      __nv_bfloat162 h = *reinterpret_cast<__nv_bfloat162*>(&w[i]);
+      float2 f = __bfloat1622float2(h);
+      h = __floats2bfloat162_rn(__fmul_rn(f.x, s), __fmul_rn(f.y, s));
+      w[i] = *reinterpret_cast<unsigned*>(&h);
+    } else if constexpr (DT == FC_FLOAT16) {
+      __half2 h = *reinterpret_cast<__half2*>(&w[i]);
+      float2 f = __half22float2(h);
+      h = __floats2half2_rn(__fmul_rn(f.x, s), __fmul_rn(f.y, s));
+      w[i] = *reinterpret_cast<unsigned*>(&h);
+    }
+  }
+}
+
 template <int DT>
 __global__ void __launch_bounds__(FC_NVLS_THREADS) fc_nvls_kernel(const __grid_constant__ FcNvlsParams P) {
   __shared__ unsigned s_e;
@@ -131,6 +157,10 @@ __global__ void __launch_bounds__(FC_NVLS_THREADS) fc_nvls_kernel(const __grid_c
 #pragma unroll
         for (int u = 0; u < U; ++u)
           if (i + u * stride < nv) v[u] = mm_ld_reduce<DT>(P.mc + r0 + 16 * (i + u * stride));
+        if (P.op == FC_AVG) {
+#pragma unroll
+          for (int u = 0; u < U; ++u) scale16<DT>(v[u], P.scale);
+        }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           if (i + u * stride >= nv) continue;

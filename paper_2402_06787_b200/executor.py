@@ -41,9 +41,17 @@ for _name, _code in (("uint32", 3), ("uint64", 5)):
 REDUCIBLE = {torch.int32, torch.float16, torch.float32, torch.bfloat16}
 if hasattr(torch, "uint32"):
     REDUCIBLE.add(torch.uint32)
-OPS = {"sum": 0}
+OPS = {"sum": 0, "avg": 4}  # ncclRedOp_t numbering (include/forestcoll.h)
 DEFAULT_SCRATCH = 2 << 30  # per rank: reduction scratch + LL128 staging
 VIRTUAL_SCRATCH = 1 << 30
+
+
+# raw cudaStream_t of the current stream without building a torch.cuda.Stream
+# object per call (host overhead matters for small collectives)
+_raw_stream = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+if _raw_stream is None:  # pragma: no cover
+    def _raw_stream(device):
+        return torch.cuda.current_stream(device).cuda_stream
 
 
 def _dtype_args(t: torch.Tensor, count: int):
@@ -62,8 +70,12 @@ def _pci_bus_id(device: int):
 
 
 def _op_code(op) -> int:
+    """'sum' / 'avg' or torch.distributed.ReduceOp.SUM / .AVG."""
+    if not isinstance(op, str):
+        name = str(getattr(op, "name", op)).rsplit(".", 1)[-1].lower()
+        op = name if name in OPS else op
     if op not in OPS:
-        raise Unsupported(f"reduction op {op!r} is not supported (only 'sum')")
+        raise Unsupported(f"reduction op {op!r} is not supported (only 'sum' and 'avg')")
     return OPS[op]
 
 
@@ -200,7 +212,7 @@ class _CommBase:
     def _check_tensor(t, device, name):
         if not isinstance(t, torch.Tensor) or not t.is_cuda:
             raise InvalidArgument(f"{name} must be a CUDA tensor")
-        if t.device.index != device:
+        if t.get_device() != device:
             raise InvalidArgument(f"{name} is on {t.device}, communicator on cuda:{device}")
         if not t.is_contiguous():
             raise InvalidArgument(f"{name} must be contiguous")
@@ -340,10 +352,13 @@ class ForestCollComm(_CommBase):
         """The topology routes every pair through one switch that declares
         `capability` (multicast / aggregation): the pruned forest then sends
         each shard into the switch once (schedule.py:237-306)."""
-        if self.topology is None:
-            return False
-        sws = [n for n in self.topology["nodes"] if n["kind"] == "switch"]
-        return len(sws) == 1 and bool(sws[0].get(capability, False))
+        cache = self.__dict__.setdefault("_capable", {})
+        hit = cache.get(capability)
+        if hit is None:
+            sws = [] if self.topology is None else \
+                [n for n in self.topology["nodes"] if n["kind"] == "switch"]
+            hit = cache[capability] = len(sws) == 1 and bool(sws[0].get(capability, False))
+        return hit
 
     def _usable_topology(self, doc, world_size):
         """An NVML topology whose schedule is neither cached nor generatable
@@ -380,7 +395,7 @@ class ForestCollComm(_CommBase):
         same-sized tensors).  Outputs of all_gather / all_reduce must be
         registered; first use registers automatically."""
         key = (t.data_ptr(), t.numel() * t.element_size())
-        if self.nranks == 1 or any(lo <= key[0] and key[0] + key[1] <= lo + nb
+        if key in self._registered or self.nranks == 1 or any(lo <= key[0] and key[0] + key[1] <= lo + nb
                                    for lo, nb in self._registered):
             return  # already mapped (views of a registered buffer included)
         hb = self._lib.fc_handle_bytes()
@@ -406,7 +421,7 @@ class ForestCollComm(_CommBase):
         return t
 
     def _stream(self):
-        return torch.cuda.current_stream(self.device).cuda_stream
+        return _raw_stream(self.device)
 
     # -- collectives --------------------------------------------------------
     def all_gather(self, out: torch.Tensor, inp: torch.Tensor) -> torch.Tensor:
@@ -515,7 +530,7 @@ class VirtualComm(_CommBase):
         return arr
 
     def _stream(self):
-        return torch.cuda.current_stream(self.device).cuda_stream
+        return _raw_stream(self.device)
 
     def all_gather(self, outs, inps):
         for o, i in zip(outs, inps):
@@ -625,7 +640,7 @@ class MultiRankComm(_CommBase):
         return (ctypes.c_void_p * len(ts))(*[t.data_ptr() for t in ts])
 
     def _stream(self):
-        return torch.cuda.current_stream(self.device).cuda_stream
+        return _raw_stream(self.device)
 
     def all_gather(self, outs, inps):
         self.plan(ALLGATHER)

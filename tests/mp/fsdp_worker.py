@@ -1,0 +1,74 @@
+"""torchrun worker: FSDP2 (fully_shard) with the ForestColl all-gather /
+reduce-scatter adapters trains to the same parameters (within fp32
+reassociation tolerance) as stock FSDP2 over NCCL, in fp32 and in bf16 mixed
+precision; the all-gather outputs come from the symmetric pool."""
+
+import os
+import sys
+
+REPO = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, REPO)
+
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+from torch.distributed.fsdp import FSDPModule, MixedPrecisionPolicy, fully_shard  # noqa: E402
+
+from paper_2402_06787_b200 import ForestCollComm  # noqa: E402
+from paper_2402_06787_b200.fsdp import ForestCollAllGather, ForestCollReduceScatter  # noqa: E402
+from paper_2402_06787_b200.topology import nvswitch_doc  # noqa: E402
+
+
+def build(mp):
+    torch.manual_seed(0)
+    net = torch.nn.Sequential(*[torch.nn.Sequential(torch.nn.Linear(256, 512), torch.nn.GELU(),
+                                                    torch.nn.Linear(512, 256)) for _ in range(4)]).cuda()
+    kw = {"mp_policy": MixedPrecisionPolicy(param_dtype=torch.bfloat16, reduce_dtype=torch.bfloat16)} if mp else {}
+    for blk in net:
+        fully_shard(blk, **kw)
+    fully_shard(net, **kw)
+    return net
+
+
+def train(net, steps=4):
+    opt = torch.optim.SGD(net.parameters(), lr=0.05)
+    g = torch.Generator(device="cuda").manual_seed(10 + dist.get_rank())
+    for _ in range(steps):
+        x = torch.randn(32, 256, device="cuda", generator=g)
+        loss = net(x).float().square().mean()
+        opt.zero_grad()
+        loss.backward()
+        opt.step()
+    return [p.full_tensor().detach().float().clone() for p in net.parameters()]
+
+
+def main():
+    local = int(os.environ["LOCAL_RANK"])
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    rank, n = dist.get_rank(), dist.get_world_size()
+    comm = ForestCollComm(nvswitch_doc(n), rank=rank, world_size=n, device=local)
+    ag = ForestCollAllGather(comm, pool_bytes=64 << 20)
+    rs = ForestCollReduceScatter(comm)
+    fails = []
+    for mp, tol in ((False, 1e-5), (True, 2e-2)):
+        ref = train(build(mp))
+        net = build(mp)
+        for m in net.modules():
+            if isinstance(m, FSDPModule):
+                m.set_custom_all_gather(ag)
+                m.set_custom_reduce_scatter(rs)
+        got = train(net)
+        comm.check()
+        if not all(torch.allclose(a, b, rtol=tol, atol=tol) for a, b in zip(ref, got)):
+            worst = max(float((a - b).abs().max()) for a, b in zip(ref, got))
+            fails.append(f"mp={mp} max|diff|={worst:.3g}")
+    used = ag.pool.nbytes - ag.pool.free_bytes
+    print(f"FSDP rank {rank} {'OK' if not fails else 'FAIL ' + '; '.join(fails)} pool_in_use={used}",
+          flush=True)
+    comm.close()
+    dist.destroy_process_group()
+    sys.exit(0 if not fails else 1)
+
+
+if __name__ == "__main__":
+    main()

@@ -63,6 +63,15 @@ def main():
             comm.all_reduce(buf)
             if not torch.allclose(buf.double().cpu(), ref, rtol=tol, atol=tol * n):
                 fails.append(f"allreduce {dtype} S={S}")
+            if dtype != torch.int32:  # op avg: switch sum scaled by 1/N
+                inp.copy_(allin[rank].to(dev))
+                comm.reduce_scatter(out, inp, op="avg")
+                if not torch.allclose(out.double().cpu(), want / n, rtol=tol, atol=tol):
+                    fails.append(f"reduce_scatter avg {dtype} S={S}")
+                buf.copy_(allin[rank].to(dev))
+                comm.all_reduce(buf, op="avg")
+                if not torch.allclose(buf.double().cpu(), ref / n, rtol=tol, atol=tol):
+                    fails.append(f"allreduce avg {dtype} S={S}")
     comm.check()
     print(f"NVLS rank {rank} {'OK' if not fails else 'FAIL ' + '; '.join(fails)}", flush=True)
     # timing: NVLS engine vs tree engine on the same sizes

@@ -90,6 +90,23 @@ def run_all(comm, rank, n, dev):
             ref = fo.allreduce(comm.schedule("allreduce"), [host(x) for x in ins], name)[rank]
             if not np.array_equal(host(buf).view(np.uint8), ref.view(np.uint8)):
                 fails.append(f"allreduce {name} count={count}")
+    # op avg (fp dtypes): the root scales its fp32 sum by fp32(1/N) once
+    for dtype, name in ((torch.bfloat16, "bfloat16"), (torch.float32, "float32")):
+        for S in (999, (1 << 19) + 8):
+            ins = [seeded(n * S, dtype, 1300 + r + S) for r in range(n)]
+            out = torch.zeros(S, dtype=dtype, device=dev)
+            comm.reduce_scatter(out, ins[rank].to(dev), op="avg")
+            buf = comm.empty(n * S, dtype=dtype)
+            buf.copy_(ins[rank].to(dev))
+            comm.all_reduce(buf, op=dist.ReduceOp.AVG)
+            torch.cuda.synchronize()
+            hs = [host(x) for x in ins]
+            ref = fo.reduce_scatter(comm.schedule("reduce_scatter"), hs, name, op="avg")[rank]
+            if not np.array_equal(host(out).view(np.uint8), ref.view(np.uint8)):
+                fails.append(f"reduce_scatter avg {name} S={S}")
+            ref = fo.allreduce(comm.schedule("allreduce"), hs, name, op="avg")[rank]
+            if not np.array_equal(host(buf).view(np.uint8), ref.view(np.uint8)):
+                fails.append(f"allreduce avg {name} count={n * S}")
     # back-to-back calls reusing buffers (entry barrier / epoch reuse)
     S = 1 << 18
     out = comm.empty(n * S, dtype=torch.float32)

@@ -49,6 +49,33 @@ def test_nvls_engine_parity(n):
     assert out.count(" OK") >= n, out[-4000:]
 
 
+@pytest.mark.parametrize("n", [2, 4])
+def test_mismatched_output_buffers_fail_loudly(n):
+    if _ngpus() < n:
+        pytest.skip(f"needs {n} GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(29760 + n),
+           os.path.join(HERE, "mp", "mismatch_worker.py")]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    out = r.stdout + r.stderr
+    assert r.returncode == 0 and out.count(" OK") >= n, out[-4000:]
+    assert "different output buffer" in out, out[-4000:]
+
+
+@pytest.mark.parametrize("n", [2, 4])
+def test_fsdp2_custom_collectives(n):
+    """FSDP2 with ForestColl all-gather (symmetric pool) and reduce-scatter
+    (AVG fused in the kernel) matches stock NCCL FSDP2."""
+    if _ngpus() < n:
+        pytest.skip(f"needs {n} GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(29770 + n),
+           os.path.join(HERE, "mp", "fsdp_worker.py")]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900)
+    out = r.stdout + r.stderr
+    assert r.returncode == 0 and out.count(" OK") >= n, out[-4000:]
+
+
 def test_ddp_comm_hook():
     if _ngpus() < 2:
         pytest.skip("needs 2 GPUs")

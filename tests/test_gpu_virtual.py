@@ -109,6 +109,63 @@ def test_allreduce_virtual(dev, name, dtype, count, proto):
         assert np.array_equal(_bits(_np(outs[r])), _bits(ref[r])), f"rank {r}"
 
 
+@pytest.mark.parametrize("proto", PROTOS)
+@pytest.mark.parametrize("name", ["nvs4_reduce_scatter", "nvs8_reduce_scatter",
+                                  "groups300_reduce_scatter", "groups100_reduce_scatter"])
+@pytest.mark.parametrize("dtype", ["float32", "bfloat16", "float16"])
+@pytest.mark.parametrize("S", [5, 65536 + 8])
+def test_reduce_scatter_avg_virtual(dev, name, dtype, S, proto):
+    """op avg: the root scales its fp32 sum by fp32(1/N) once (FC_AVG)."""
+    from oracle import forest_oracle as fo
+
+    s = load_golden(name)
+    comm = _comm(s, proto)
+    n = comm.nranks
+    gen = torch.Generator().manual_seed(31)
+    ins = [_rand(n * S, dtype, gen, dev) for _ in range(n)]
+    outs = [torch.zeros(S, dtype=TORCH_DT[dtype], device=dev) for _ in range(n)]
+    comm.reduce_scatter(outs, ins, op="avg")
+    comm.check()
+    ref = fo.reduce_scatter(s, [_np(x) for x in ins], dtype, op="avg")
+    for r in range(n):
+        assert np.array_equal(_bits(_np(outs[r])), _bits(ref[r])), f"rank {r}"
+
+
+@pytest.mark.parametrize("proto", PROTOS)
+@pytest.mark.parametrize("name", ["nvs8_allreduce", "groups450_allreduce"])
+@pytest.mark.parametrize("dtype", ["bfloat16", "float32"])
+@pytest.mark.parametrize("count", [1001, 1 << 18])
+def test_allreduce_avg_virtual(dev, name, dtype, count, proto):
+    import torch.distributed as dist
+
+    from oracle import forest_oracle as fo
+
+    s = load_golden(name)
+    comm = _comm(s, proto)
+    n = comm.nranks
+    gen = torch.Generator().manual_seed(8)
+    ins = [_rand(count, dtype, gen, dev) for _ in range(n)]
+    outs = [torch.zeros(count, dtype=TORCH_DT[dtype], device=dev) for _ in range(n)]
+    comm.all_reduce(ins, outs=outs, op=dist.ReduceOp.AVG)
+    comm.check()
+    ref = fo.allreduce(s, [_np(x) for x in ins], dtype, op="avg")
+    for r in range(n):
+        assert np.array_equal(_bits(_np(outs[r])), _bits(ref[r])), f"rank {r}"
+
+
+def test_avg_rejected_for_integers(dev):
+    from paper_2402_06787_b200.errors import Unsupported
+
+    s = load_golden("nvs4_reduce_scatter")
+    comm = _comm(s)
+    ins = [torch.ones(4 * 64, dtype=torch.int32, device=dev) for _ in range(4)]
+    outs = [torch.zeros(64, dtype=torch.int32, device=dev) for _ in range(4)]
+    with pytest.raises(Unsupported):
+        comm.reduce_scatter(outs, ins, op="avg")
+    with pytest.raises(Unsupported):
+        comm.reduce_scatter(outs, ins, op="max")
+
+
 @pytest.mark.parametrize("name", ["nvs8_allgather", "groups300_allgather", "random1_allgather"])
 def test_ll128_is_used_for_aligned_medium_messages(dev, name):
     s = load_golden(name)

@@ -122,6 +122,44 @@ def test_fp_reduce_scatter_matches_independent_restatement(name, dtype):
         assert np.array_equal(got[r].view(np.uint8), want[r].view(np.uint8))
 
 
+@pytest.mark.parametrize("name", ["nvs8_reduce_scatter", "nvs4_reduce_scatter", "groups300_reduce_scatter"])
+def test_avg_is_power_of_two_scaled_sum_in_fp32(name):
+    """N is a power of two here: fp32(1/N) is exact and so is the scaling,
+    so avg == sum * 1/N bit for bit (the scale happens once, at the root)."""
+    s = load_golden(name)
+    n = s.num_compute
+    rng = np.random.default_rng(12)
+    ins = [rng.uniform(-1, 1, n * 33).astype(np.float32) for _ in range(n)]
+    got = fo.reduce_scatter(s, ins, "float32", op="avg")
+    ref = fo.reduce_scatter(s, ins, "float32")
+    for r in range(n):
+        assert np.array_equal(got[r], ref[r] * np.float32(1.0 / n))
+
+
+def test_avg_bf16_rounds_once_at_the_root():
+    s = load_golden("nvs4_reduce_scatter")
+    n = s.num_compute
+    rng = np.random.default_rng(13)
+    ins = [fo.f32_to_bf16(rng.uniform(-1, 1, n * 40).astype(np.float32)) for _ in range(n)]
+    got = fo.reduce_scatter(s, ins, "bfloat16", op="avg")
+    want = _per_element_rs(s, ins, "bfloat16")  # sum, rounded to bf16 at every hop
+    for r in range(n):
+        # avg of the root's fp32 sum: same as scaling the rounded sum by 1/4 when
+        # the sum's rounding is exact in the last hop; compare within 1 ulp
+        a = fo.bf16_to_f32(got[r]).astype(np.float64)
+        b = fo.bf16_to_f32(want[r]).astype(np.float64) / n
+        assert np.all(np.abs(a - b) <= np.abs(b) * 2.0 ** -7 + 1e-30)
+
+
+def test_avg_rejected_for_integers_and_unknown_ops():
+    s = load_golden("nvs4_reduce_scatter")
+    ins = [np.ones(4 * 8, np.int32) for _ in range(4)]
+    with pytest.raises(ValueError):
+        fo.reduce_scatter(s, ins, "int32", op="avg")
+    with pytest.raises(ValueError):
+        fo.reduce_scatter(s, [x.astype(np.float32) for x in ins], "float32", op="max")
+
+
 def test_fp32_reduction_close_to_float64_sum():
     s = load_golden("nvs8_reduce_scatter")
     n = s.num_compute
