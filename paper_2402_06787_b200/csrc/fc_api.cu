@@ -91,7 +91,7 @@ struct fc_comm {
   int nvls_bound = 0;
   int nvls_ctas = 32;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-  cudaEvent_t ev_last = nullptr;     // completion of the previous collective of this comm
+  cudaEvent_t ev_last = nullptr;     // cross-stream ordering of this comm's collectives
   cudaStream_t last_stream = nullptr;
   bool have_last = false;
   FcTraceRec* trace = nullptr;
@@ -196,25 +196,30 @@ const Reg* find_reg(const fc_comm* c, const void* p, size_t bytes) {
 
 // Collectives of one communicator share its control block, flags and scratch,
 // so they execute one at a time.  Calls on one stream are ordered by that
-// stream; a call issued on another stream (FSDP's all-gather and
-// reduce-scatter streams, say) first waits for the previous call's completion
-// event.  Issue order is the same on every rank of an SPMD program, so every
-// rank runs the same sequence (the ordering NCCL keeps per communicator).
-// Inside CUDA-graph capture the graph's own edges order the calls.
+// stream (and keep programmatic dependent launch between them: nothing is
+// enqueued between two calls).  A call issued on another stream (FSDP's
+// all-gather and reduce-scatter streams, say) first waits for an event
+// recorded at that moment on the previous call's stream.  Issue order is the
+// same on every rank of an SPMD program, so every rank runs the same sequence
+// (the ordering NCCL keeps per communicator).  Inside CUDA-graph capture the
+// graph's own edges order the calls.
 bool capturing(cudaStream_t s) {
   cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
   return cudaStreamIsCapturing(s, &st) == cudaSuccess && st != cudaStreamCaptureStatusNone;
 }
 
 int order_begin(fc_comm* c, cudaStream_t s) {
-  if (c->have_last && s != c->last_stream && !capturing(s))
-    FC_CUDA(c, cudaStreamWaitEvent(s, c->ev_last, 0));
+  if (c->have_last && s != c->last_stream && !capturing(s) && !capturing(c->last_stream)) {
+    if (cudaEventRecord(c->ev_last, c->last_stream) == cudaSuccess)
+      FC_CUDA(c, cudaStreamWaitEvent(s, c->ev_last, 0));
+    else
+      (void)cudaGetLastError();  // that stream is gone: its work has been retired
+  }
   return FC_SUCCESS;
 }
 
 int order_end(fc_comm* c, cudaStream_t s) {
   if (capturing(s)) return FC_SUCCESS;
-  FC_CUDA(c, cudaEventRecord(c->ev_last, s));
   c->last_stream = s;
   c->have_last = true;
   return FC_SUCCESS;

@@ -71,9 +71,6 @@ __device__ __forceinline__ void red_release_sys_add(unsigned* p, unsigned v) {
 __device__ __forceinline__ unsigned ld_volatile(const unsigned* p) {
   return *reinterpret_cast<const volatile unsigned*>(p);
 }
-__device__ __forceinline__ void st_volatile(unsigned* p, unsigned v) {
-  *reinterpret_cast<volatile unsigned*>(p) = v;
-}
 __device__ __forceinline__ void fence_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
 // Barrier of one worker (WW warps): a warp barrier or a named CTA barrier
 // (id 0 is __syncthreads).
@@ -162,17 +159,46 @@ __device__ bool spin_geq(const unsigned* p, unsigned e, FcCtl* ctl, long long ti
 // published with its ready epoch must equal ours: a rank that passed a
 // differently registered buffer (or offset / size) fails loudly instead of
 // receiving stores meant for another buffer.
+// The ready slot is one 64-bit word: epoch in the low half, the sender's
+// 32-bit tag in the high half, published by one release store.
+__device__ __forceinline__ unsigned long long ld_acquire_sys64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned tag32(const FcParams& P) {
+  return (unsigned)(P.tag ^ (P.tag >> 32));
+}
+
 __device__ bool wait_ready(const FcParams& P, int me, int x, unsigned e, FcCtl* ctl) {
-  const unsigned* f = P.flags[me];
-  if (!spin_geq(f + x, e, ctl, P.timeout_ns, FC_DEVERR_TIMEOUT_READY)) return false;
-  if (ld_acquire_sys(f + x) != e) return true;
-  const unsigned long long t = (unsigned long long)ld_volatile(f + FC_TAG_WORD + 2 * x) |
-                               ((unsigned long long)ld_volatile(f + FC_TAG_WORD + 2 * x + 1) << 32);
-  if (t == P.tag) return true;
+  const unsigned long long* f = reinterpret_cast<const unsigned long long*>(P.flags[me]) + x;
+  unsigned long long v = ld_acquire_sys64(f);
+  if ((int)((unsigned)v - e) < 0) {
+    const unsigned long long t0 = globaltimer();
+    for (unsigned i = 1;; ++i) {
+      v = ld_acquire_sys64(f);
+      if ((int)((unsigned)v - e) >= 0) break;
+      if ((i & 1023u) == 0) {
+        if (ld_volatile(&ctl->error) != 0) return false;
+        if ((long long)(globaltimer() - t0) > P.timeout_ns) {
+          if (atomicCAS(&ctl->error, 0u, (unsigned)FC_DEVERR_TIMEOUT_READY) == 0u) {
+            ctl->info[0] = (unsigned)x;
+            ctl->info[1] = e;
+            ctl->info[2] = (unsigned)v;
+          }
+          return false;
+        }
+      }
+    }
+  }
+  if ((unsigned)v != e || (unsigned)(v >> 32) == tag32(P)) return true;
   if (atomicCAS(&ctl->error, 0u, (unsigned)FC_DEVERR_BUFFER_MISMATCH) == 0u) {
     ctl->info[0] = (unsigned)x;
-    ctl->info[1] = (unsigned)P.tag;
-    ctl->info[2] = (unsigned)t;
+    ctl->info[1] = tag32(P);
+    ctl->info[2] = (unsigned)(v >> 32);
   }
   return false;
 }
@@ -942,10 +968,8 @@ __global__ void __launch_bounds__(FC_BLOCK, 1) fc_forest_kernel(const __grid_con
   // entry barrier: tell every peer that this rank entered launch e, and with
   // which output buffer (the tag store is ordered before the release)
   if ((int)threadIdx.x < P.nranks && (int)threadIdx.x != me) {
-    unsigned* pf = P.flags[threadIdx.x];
-    st_volatile(pf + FC_TAG_WORD + 2 * me, (unsigned)P.tag);
-    st_volatile(pf + FC_TAG_WORD + 2 * me + 1, (unsigned)(P.tag >> 32));
-    st_release_sys(pf + me, e);
+    unsigned long long* pf = reinterpret_cast<unsigned long long*>(P.flags[threadIdx.x]);
+    st_release_sys64(pf + me, ((unsigned long long)tag32(P) << 32) | e);
   }
 
   const int wk = w / WW;

@@ -7,9 +7,8 @@
 
 #define FC_MAXR FC_MAX_RANKS
 #define FC_ALIGN 128          // chunk boundaries / scratch phase alignment (bytes)
-#define FC_READY_WORDS 64     // flags[0..nranks): entry (ready) epochs per peer
-#define FC_TAG_WORD 32        // flags[32 + 2r, +1]: rank r's output-buffer tag of its
-                              // current launch (written before its ready epoch)
+#define FC_READY_WORDS 64     // 64-bit ready slot per peer r at words [2r, 2r+1]:
+                              // entry epoch (low) | output-buffer tag (high)
 #define FC_TABLE_MAGIC 0x50434c46  // 'FLCP'
 #define FC_TABLE_VERSION 1
 #define FC_HEADER_WORDS 16
