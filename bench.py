@@ -412,17 +412,57 @@ def run_multi(args):
     dist.destroy_process_group()
 
 
+def nccl_group(dist, algo):
+    """A separate NCCL communicator with NCCL_ALGO pinned (read at comm init)."""
+    import torch
+
+    old = os.environ.get("NCCL_ALGO")
+    os.environ["NCCL_ALGO"] = algo
+    try:
+        g = dist.new_group(backend="nccl")
+        x = torch.ones(1024, device="cuda")
+        dist.all_reduce(x, group=g)  # create the communicator now, under this NCCL_ALGO
+        torch.cuda.synchronize()
+    finally:
+        if old is None:
+            os.environ.pop("NCCL_ALGO", None)
+        else:
+            os.environ["NCCL_ALGO"] = old
+    return g
+
+
+def steps_for(M, floor):
+    """>= ~25 ms of device time per measurement: short windows let host jitter
+    (GC, page faults) drain the launch queue of small calls."""
+    est = 20e-6 + M / 600e9
+    return max(floor, min(2000, int(25e-3 / est)))
+
+
 def sweep_multi(comm, dist, n, dev, args):
     import torch
 
     res = {"sweep": []}
-    steps, warm = max(5, args.steps), 3
+    warm = 3
+    groups = {"nccl": None}
+    for algo in ("Ring", "NVLS"):  # SURVEY.md §8d: NCCL ring and NVLS beside the default
+        try:
+            groups[f"nccl_{algo.lower()}"] = nccl_group(dist, algo)
+        except Exception as exc:  # noqa: BLE001
+            res[f"nccl_{algo.lower()}_error"] = f"{type(exc).__name__}: {exc}"[:200]
 
-    def rec(coll, M, ms, nccl_ms, dtype):
+    def rec(coll, M, ms, dtype, fn_nccl):
         t = comm.t_star(coll, M)
-        res["sweep"].append({"collective": coll, "M_bytes": M, "dtype": dtype, "ms": round(ms, 4),
-                             "algbw_GBps": round(gbs(M, ms), 2), "frac_of_t_star": round(t * 1e3 / ms, 4),
-                             "nccl_ms": round(nccl_ms, 4), "nccl_algbw_GBps": round(gbs(M, nccl_ms), 2)})
+        r = {"collective": coll, "M_bytes": M, "dtype": dtype, "ms": round(ms, 4),
+             "algbw_GBps": round(gbs(M, ms), 2), "frac_of_t_star": round(t * 1e3 / ms, 4),
+             "proto": comm.last_call_info()["proto"]}
+        for name, g in groups.items():
+            try:
+                nm = timed(lambda: fn_nccl(g), steps_for(M, max(5, args.steps)), warm, dist)
+                r[f"{name}_ms"] = round(nm, 4)
+                r[f"{name}_algbw_GBps"] = round(gbs(M, nm), 2)
+            except Exception as exc:  # noqa: BLE001
+                r[f"{name}_error"] = f"{type(exc).__name__}: {exc}"[:120]
+        res["sweep"].append(r)
 
     for mib in (1, 64, 1024):
         M = mib * MIB
@@ -430,26 +470,25 @@ def sweep_multi(comm, dist, n, dev, args):
         inp = torch.randn(S, device=dev)
         out = comm.empty(n * S, dtype=torch.float32)
         o2 = torch.empty_like(out)
-        ms = timed(lambda: comm.all_gather(out, inp), steps, warm, dist)
-        nm = timed(lambda: dist.all_gather_into_tensor(o2, inp), steps, warm, dist)
-        rec("allgather", S * 4 * n, ms, nm, "float32")
+        ms = timed(lambda: comm.all_gather(out, inp), steps_for(M, max(5, args.steps)), warm, dist)
+        rec("allgather", S * 4 * n, ms, "float32",
+            lambda g: dist.all_gather_into_tensor(o2, inp, group=g))
         comm.deregister(out)
     for mib, dt in ((256, torch.float32), (256, torch.bfloat16)):
         M = mib * MIB
         R = M // n // torch.tensor([], dtype=dt).element_size()
         inp = torch.randn(R * n, device=dev).to(dt)
         out = torch.empty(R, device=dev, dtype=dt)
-        ms = timed(lambda: comm.reduce_scatter(out, inp), steps, warm, dist)
-        nm = timed(lambda: dist.reduce_scatter_tensor(out, inp), steps, warm, dist)
-        rec("reduce_scatter", M, ms, nm, str(dt).split(".")[-1])
+        ms = timed(lambda: comm.reduce_scatter(out, inp), steps_for(M, max(5, args.steps)), warm, dist)
+        rec("reduce_scatter", M, ms, str(dt).split(".")[-1],
+            lambda g: dist.reduce_scatter_tensor(out, inp, group=g))
     for mib in (25, 1024):
         M = mib * MIB
         cnt = M // 2
         buf = comm.empty(cnt, dtype=torch.bfloat16)
         buf.normal_()
-        ms = timed(lambda: comm.all_reduce(buf), steps, warm, dist)
-        nm = timed(lambda: dist.all_reduce(buf), steps, warm, dist)
-        rec("allreduce", M, ms, nm, "bfloat16")
+        ms = timed(lambda: comm.all_reduce(buf), steps_for(M, max(5, args.steps)), warm, dist)
+        rec("allreduce", M, ms, "bfloat16", lambda g: dist.all_reduce(buf, group=g))
         comm.deregister(buf)
     comm.check()
     try:
@@ -482,7 +521,7 @@ def nvls_points(dist, dev, n, args):
         M = mib * MIB
         buf = c.nvls_empty(M // 2, torch.bfloat16)
         buf.normal_()
-        ms = timed(lambda: c.all_reduce(buf), max(5, args.steps), 3, dist)
+        ms = timed(lambda: c.all_reduce(buf), steps_for(M, max(5, args.steps)), 3, dist)
         t = c.t_star("allreduce", M)
         out.append({"collective": "allreduce", "engine": c.last_call_info()["proto"],
                     "M_bytes": M, "dtype": "bfloat16", "ms": round(ms, 4),

@@ -57,12 +57,13 @@ def bf16_to_f32(u16: np.ndarray) -> np.ndarray:
 
 
 def f32_to_bf16(f32: np.ndarray) -> np.ndarray:
-    """Round-to-nearest-even; NaN quieted by setting bit 6 (fc_kernel.cu Red<BF16>)."""
+    """IEEE round-to-nearest-even (denormals kept); every NaN becomes the
+    canonical 0x7FFF.  This is sm_100's cvt.rn.bf16x2.f32, which the kernel
+    uses (csrc/fc_device.cuh Red<FC_BFLOAT16>; measured by tools/cvt_probe.cu)."""
     u = np.ascontiguousarray(f32, dtype=np.float32).view(np.uint32)
     nan = (u & np.uint32(0x7FFFFFFF)) > np.uint32(0x7F800000)
     rounded = (u + np.uint32(0x7FFF) + ((u >> np.uint32(16)) & np.uint32(1))) >> np.uint32(16)
-    quiet = (u >> np.uint32(16)) | np.uint32(0x40)
-    return np.where(nan, quiet, rounded).astype(np.uint16)
+    return np.where(nan, np.uint32(0x7FFF), rounded).astype(np.uint16)
 
 
 def _to_acc(x: np.ndarray, dtype: str) -> np.ndarray:

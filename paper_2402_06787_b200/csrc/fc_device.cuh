@@ -219,18 +219,24 @@ struct Red<FC_FLOAT32> {
   __device__ static A mul(A a, float s) { return __fmul_rn(a, s); }
 };
 
-// bf16: fp32 accumulate, one round-to-nearest-even per hop.  NaN is quieted
-// the same way as oracle/forest_oracle.py::f32_to_bf16.
+// bf16: fp32 accumulate, one round-to-nearest-even per hop with the hardware
+// converter (cvt.rn.bf16x2.f32: denormals kept, NaN -> canonical 0x7FFF, as
+// oracle/forest_oracle.py::f32_to_bf16).
 template <>
 struct Red<FC_BFLOAT16> {
   using E = unsigned short;
   using A = float;
   __device__ static A to(E x) { return __uint_as_float(((unsigned)x) << 16); }
   __device__ static E from(A a) {
-    unsigned u = __float_as_uint(a);
-    if ((u & 0x7fffffffu) > 0x7f800000u) return (E)((u >> 16) | 0x40u);
-    u += 0x7fffu + ((u >> 16) & 1u);
-    return (E)(u >> 16);
+    unsigned short r;
+    asm("cvt.rn.bf16.f32 %0, %1;" : "=h"(r) : "f"(a));
+    return r;
+  }
+  // two elements at once: lo -> bits 0..15, hi -> bits 16..31
+  __device__ static unsigned from2(A lo, A hi) {
+    unsigned r;
+    asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+    return r;
   }
   __device__ static A add(A a, A b) { return __fadd_rn(a, b); }
   __device__ static A mul(A a, float s) { return __fmul_rn(a, s); }
@@ -242,6 +248,11 @@ struct Red<FC_FLOAT16> {
   using A = float;
   __device__ static A to(E x) { return __half2float(__ushort_as_half(x)); }
   __device__ static E from(A a) { return __half_as_ushort(__float2half_rn(a)); }
+  __device__ static unsigned from2(A lo, A hi) {
+    unsigned r;
+    asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+    return r;
+  }
   __device__ static A add(A a, A b) { return __fadd_rn(a, b); }
   __device__ static A mul(A a, float s) { return __fmul_rn(a, s); }
 };
@@ -279,9 +290,15 @@ struct Acc16 {
   }
   __device__ __forceinline__ uint4 pack() const {
     uint4 out;
-    E* e = reinterpret_cast<E*>(&out);
+    if constexpr (sizeof(E) == 2) {
+      unsigned* w = reinterpret_cast<unsigned*>(&out);
 #pragma unroll
-    for (int q = 0; q < NE; ++q) e[q] = R::from(a[q]);
+      for (int q = 0; q < NE / 2; ++q) w[q] = R::from2(a[2 * q], a[2 * q + 1]);
+    } else {
+      E* e = reinterpret_cast<E*>(&out);
+#pragma unroll
+      for (int q = 0; q < NE; ++q) e[q] = R::from(a[q]);
+    }
     return out;
   }
 };
@@ -309,9 +326,15 @@ struct Acc8 {
   }
   __device__ __forceinline__ unsigned long long pack() const {
     unsigned long long out;
-    E* e = reinterpret_cast<E*>(&out);
+    if constexpr (sizeof(E) == 2) {
+      unsigned* w = reinterpret_cast<unsigned*>(&out);
 #pragma unroll
-    for (int q = 0; q < NE; ++q) e[q] = R::from(a[q]);
+      for (int q = 0; q < NE / 2; ++q) w[q] = R::from2(a[2 * q], a[2 * q + 1]);
+    } else {
+      E* e = reinterpret_cast<E*>(&out);
+#pragma unroll
+      for (int q = 0; q < NE; ++q) e[q] = R::from(a[q]);
+    }
     return out;
   }
 };

@@ -22,7 +22,16 @@ def test_bf16_rounding_matches_torch():
     ref = torch.from_numpy(x).to(torch.bfloat16).view(torch.int16).numpy().view(np.uint16)
     finite = ~np.isnan(x)
     assert np.array_equal(ours[finite], ref[finite])
-    assert np.isnan(fo.bf16_to_f32(ours[~finite])).all()
+    assert (ours[~finite] == 0x7FFF).all()  # canonical NaN, as cvt.rn.bf16x2.f32 on sm_100
+
+
+def test_bf16_rounding_matches_sm100_cvt_vectors():
+    """Pinned outputs of cvt.rn.bf16x2.f32 measured on a B200 (tools/cvt_probe.cu)."""
+    pairs = {0x7fc00000: 0x7fff, 0xffc00000: 0x7fff, 0x7f800001: 0x7fff, 0xff812345: 0x7fff,
+             0x7fa5a5a5: 0x7fff, 0x7f800000: 0x7f80, 0x3f808000: 0x3f80, 0x3f818000: 0x3f82,
+             0x00000001: 0x0000, 0x807fffff: 0x8080, 0x7f7fffff: 0x7f80, 0x3f80ffff: 0x3f81}
+    x = np.array(list(pairs), dtype=np.uint32).view(np.float32)
+    assert fo.f32_to_bf16(x).tolist() == list(pairs.values())
 
 
 @pytest.mark.parametrize("name", golden_names("allgather"))

@@ -58,6 +58,7 @@ def main():
         f = lambda: comm.all_gather(out, inp)  # noqa: E731
         g = lambda: dist.all_gather_into_tensor(o2, inp)  # noqa: E731
         e1 = timed(f, 200, 20, dist) * 1e3
+        e1b = timed(f, 2000, 20, dist) * 1e3
         h1 = host_us(f)
         try:
             g1 = graph_us(f)
@@ -76,7 +77,7 @@ def main():
                 print("nccl graph capture failed:", exc, flush=True)
         ok = torch.equal(out, ref) and torch.equal(o2, ref)
         if rank == 0:
-            print(f"AG {S*4*n:9d} B  forest: eager {e1:6.1f} host {h1:5.1f} graph {g1:6.1f} us"
+            print(f"AG {S*4*n:9d} B  forest: eager {e1:6.1f} (x2000 {e1b:6.1f}) host {h1:5.1f} graph {g1:6.1f} us"
                   f" | nccl: eager {e2:6.1f} host {h2:5.1f} graph {g2:6.1f} us  ok={ok}", flush=True)
     comm.check()
     comm.close()

@@ -17,28 +17,11 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
 import torch.distributed as dist  # noqa: E402
 
-from bench import gbs, timed  # noqa: E402
+from bench import gbs, nccl_group, steps_for, timed  # noqa: E402
 from paper_2402_06787_b200 import ForestCollComm  # noqa: E402
 from paper_2402_06787_b200.topology import nvswitch_doc  # noqa: E402
 
 KIB, MIB = 1 << 10, 1 << 20
-
-
-def nccl_group(algo):
-    """A separate NCCL communicator with NCCL_ALGO pinned (read at comm init)."""
-    old = os.environ.get("NCCL_ALGO")
-    os.environ["NCCL_ALGO"] = algo
-    try:
-        g = dist.new_group(backend="nccl")
-        x = torch.ones(1024, device="cuda")
-        dist.all_reduce(x, group=g)           # force communicator creation now
-        torch.cuda.synchronize()
-    finally:
-        if old is None:
-            os.environ.pop("NCCL_ALGO", None)
-        else:
-            os.environ["NCCL_ALGO"] = old
-    return g
 
 
 def main():
@@ -60,7 +43,7 @@ def main():
     groups = {"nccl": None}
     for algo in ("Ring", "NVLS"):
         try:
-            groups[f"nccl_{algo.lower()}"] = nccl_group(algo)
+            groups[f"nccl_{algo.lower()}"] = nccl_group(dist, algo)
         except Exception as exc:  # noqa: BLE001
             if rank == 0:
                 print(f"# NCCL_ALGO={algo} unavailable: {exc}", flush=True)
@@ -75,13 +58,13 @@ def main():
         if rank == 0:
             print(json.dumps(r), flush=True)
 
-    def steps_for(M):
-        return max(5, min(200, int(args.iters * (256 * MIB) / max(M, 1)))) if M < 256 * MIB else args.iters
+    def steps(M):
+        return steps_for(M, args.iters)
 
     def run_nccl(coll, M, dtype, fn):
         for name, g in groups.items():
             try:
-                ms = timed(lambda: fn(g), steps_for(M), 3, dist)
+                ms = timed(lambda: fn(g), steps(M), 3, dist)
                 emit(coll, M, name, ms, dtype)
             except Exception as exc:  # noqa: BLE001
                 if rank == 0:
@@ -94,7 +77,7 @@ def main():
         Mb = S * 4 * n
         inp = torch.randn(S, device=dev)
         out = comm.empty(n * S)
-        ms = timed(lambda: comm.all_gather(out, inp), steps_for(Mb), 3, dist)
+        ms = timed(lambda: comm.all_gather(out, inp), steps(Mb), 3, dist)
         emit("allgather", Mb, "forestcoll", ms, "float32", proto=comm.last_call_info()["proto"])
         ref = out.clone()
         comm.deregister(out)
@@ -102,7 +85,7 @@ def main():
         if nv.nvls_enabled and Mb <= args.nvls_max_mib * MIB:
             nv._nvls_next = 0
             o3 = nv.nvls_empty(n * S)
-            ms = timed(lambda: nv.all_gather(o3, inp), steps_for(Mb), 3, dist)
+            ms = timed(lambda: nv.all_gather(o3, inp), steps(Mb), 3, dist)
             assert torch.equal(o3, ref), "NVLS allgather mismatch"
             emit("allgather", Mb, "forestcoll_nvls", ms, "float32")
             del o3
@@ -122,13 +105,13 @@ def main():
             R = M // n // es
             inp = torch.randn(R * n, device=dev).to(dt)
             out = torch.empty(R, device=dev, dtype=dt)
-            ms = timed(lambda: comm.reduce_scatter(out, inp), steps_for(M), 3, dist)
+            ms = timed(lambda: comm.reduce_scatter(out, inp), steps(M), 3, dist)
             emit("reduce_scatter", M, "forestcoll", ms, str(dt)[6:], proto=comm.last_call_info()["proto"])
             if nv.nvls_enabled and M <= args.nvls_max_mib * MIB:
                 nv._nvls_next = 0
                 i3 = nv.nvls_empty(R * n, dt)
                 i3.copy_(inp)
-                ms = timed(lambda: nv.reduce_scatter(out, i3), steps_for(M), 3, dist)
+                ms = timed(lambda: nv.reduce_scatter(out, i3), steps(M), 3, dist)
                 emit("reduce_scatter", M, "forestcoll_nvls", ms, str(dt)[6:])
                 del i3
             run_nccl("reduce_scatter", M, str(dt)[6:],
@@ -141,14 +124,14 @@ def main():
         M = mib * MIB
         buf = comm.empty(M // 2, dtype=torch.bfloat16)
         buf.normal_()
-        ms = timed(lambda: comm.all_reduce(buf), steps_for(M), 3, dist)
+        ms = timed(lambda: comm.all_reduce(buf), steps(M), 3, dist)
         emit("allreduce", M, "forestcoll", ms, "bfloat16", proto=comm.last_call_info()["proto"])
         comm.deregister(buf)
         if nv.nvls_enabled and M <= args.nvls_max_mib * MIB:
             nv._nvls_next = 0
             b3 = nv.nvls_empty(M // 2, torch.bfloat16)
             b3.normal_()
-            ms = timed(lambda: nv.all_reduce(b3), steps_for(M), 3, dist)
+            ms = timed(lambda: nv.all_reduce(b3), steps(M), 3, dist)
             emit("allreduce", M, "forestcoll_nvls", ms, "bfloat16")
             del b3
         run_nccl("allreduce", M, "bfloat16", lambda g: dist.all_reduce(buf, group=g))

@@ -30,6 +30,9 @@ def main():
     ap.add_argument("--ww", default="4")
     ap.add_argument("--proto", default="-1")
     ap.add_argument("--pdl", default="1")
+    ap.add_argument("--chunk-min", default="16384")
+    ap.add_argument("--dtype", default="float32")
+    ap.add_argument("--iters", type=int, default=10)
     args = ap.parse_args()
     local = int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
@@ -46,9 +49,10 @@ def main():
                 out = comm.empty(n * S, dtype=torch.float32)
                 fn = lambda: comm.all_gather(out, inp)  # noqa: E731
             elif coll == "reduce_scatter":
-                R = M // n // 4
-                inp = torch.randn(R * n, device=dev)
-                out = torch.empty(R, device=dev)
+                dt = getattr(torch, args.dtype)
+                R = M // n // torch.tensor([], dtype=dt).element_size()
+                inp = torch.randn(R * n, device=dev).to(dt)
+                out = torch.empty(R, device=dev, dtype=dt)
                 fn = lambda: comm.reduce_scatter(out, inp)  # noqa: E731
             else:
                 buf = comm.empty(M // 2, dtype=torch.bfloat16)
@@ -59,7 +63,8 @@ def main():
                     args.ctas.split(","), args.chunks.split(","), args.ipw.split(","),
                     args.lag.split(","), args.mode.split(","), args.dma.split(","),
                     args.ww.split(","), args.proto.split(",")):
-              for pdl in args.pdl.split(","):
+              for pdl, cmin in itertools.product(args.pdl.split(","), args.chunk_min.split(",")):
+                comm.set_option("chunk_min", int(cmin))
                 comm.set_option("pdl", int(pdl))
                 comm.set_option("proto", int(proto))
                 comm.set_option("worker_warps", int(ww))
@@ -71,10 +76,10 @@ def main():
                 comm.set_option("chunk_max", int(ch))
                 comm.set_option("ll_chunk_max", int(ch))
                 comm.set_option("items_per_worker", int(ipw))
-                ms = timed(fn, 10, 3, dist)
+                ms = timed(fn, args.iters, 3, dist)
                 info = comm.last_call_info()
                 if rank == 0:
-                    print(f"{coll:15s} {mib:6d}MiB ctas={ctas:>4s} chunk={int(ch)//1024:5d}K ipw={ipw} lag={lag:>3s} ww={ww} p={info["proto"]} pdl={pdl} "
+                    print(f"{coll:15s} {mib:6d}MiB ctas={ctas:>4s} chunk={int(ch)//1024:5d}K ipw={ipw} lag={lag:>3s} ww={ww} p={info["proto"]} pdl={pdl} cmin={int(cmin)//1024}K "
                           f"n={info['nchunks']:5d} L={info['launches']} ms={ms:8.4f} "
                           f"algbw={gbs(M, ms):8.1f} frac_T*={tstar*1e3/ms:6.3f}", flush=True)
     comm.check()
