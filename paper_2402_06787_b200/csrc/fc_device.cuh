@@ -1013,9 +1013,14 @@ __global__ void __launch_bounds__(FC_BLOCK, 1) fc_forest_kernel(const __grid_con
   const long long total = nA + (PROTO ? 0 : nwait);  // simple: one completion wait per leaf
   unsigned ready_mask = 1u << me;
   FcTraceRec* const trace = P.trace;
+  // The lead claims one item ahead: the atomic's round trip overlaps the
+  // current item, and the final (empty) claim costs nothing at the tail.  A
+  // pre-claimed item is never smaller in key than the one in hand, so the
+  // smallest unfinished item is always being worked on (progress argument).
+  unsigned next = lead ? atomicAdd(&ctl->claim, 1u) : 0u;
   for (;;) {
     if (lead) {
-      int v = (int)atomicAdd(&ctl->claim, 1u);
+      int v = (int)next;
       if (ld_volatile(&ctl->error) != 0) v = INT_MAX;
       sh.item = v;
     }
@@ -1023,6 +1028,7 @@ __global__ void __launch_bounds__(FC_BLOCK, 1) fc_forest_kernel(const __grid_con
     const long long item = sh.item;
     worker_sync<WW>(wk);  // sh.item is rewritten by the next claim
     if (item >= total) break;
+    if (lead) next = atomicAdd(&ctl->claim, 1u);
     int c, ti;
     if (item < nA) {
       const long long d = item / nitem;
@@ -1063,13 +1069,14 @@ __global__ void __launch_bounds__(FC_BLOCK, 1) fc_forest_kernel(const __grid_con
   }
   __syncthreads();
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  // The last CTA of this rank re-arms the counters and publishes the epoch.
+  // No fences: every CTA's claims returned before its `done` increment, and
+  // the next launch reads these words only after this grid has completed.
   if (threadIdx.x == 0) {
-    __threadfence();
     const unsigned prev = atomicAdd(&ctl->done, 1u);
     if (prev == (unsigned)P.ctas_per_rank - 1u) {
       ctl->claim = 0;
       ctl->done = 0;
-      __threadfence();
       atomicExch(&ctl->epoch, e);
     }
   }

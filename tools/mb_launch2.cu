@@ -23,11 +23,12 @@ __global__ void __launch_bounds__(256, 1) k_spin(const __grid_constant__ Par<W> 
 }
 
 template <int W, int PDL>
-void run(cudaStream_t s, long long spin_ns) {
+void run(cudaStream_t s, long long spin_ns, int smem = 0) {
   Par<W> p{}; p.spin_ns = spin_ns;
   auto launch = [&]() {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(128); cfg.blockDim = dim3(256); cfg.stream = s;
+    cfg.dynamicSmemBytes = smem;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     at[0].val.programmaticStreamSerializationAllowed = 1;
@@ -53,8 +54,8 @@ void run(cudaStream_t s, long long spin_ns) {
   for (int i = 0; i < R / 200; ++i) CK(cudaGraphLaunch(ge, s));
   CK(cudaEventRecord(b, s)); CK(cudaEventSynchronize(b));
   float ms_g; CK(cudaEventElapsedTime(&ms_g, a, b));
-  printf("params %5zu B pdl=%d spin %5lld ns: eager %.2f us/launch (gap %.2f), graph %.2f (gap %.2f)\n",
-         sizeof(Par<W>), PDL, spin_ns, ms_e * 1e3 / R, ms_e * 1e3 / R - spin_ns * 1e-3,
+  printf("smem %6d params %5zu B pdl=%d spin %5lld ns: eager %.2f us/launch (gap %.2f), graph %.2f (gap %.2f)\n",
+         smem, sizeof(Par<W>), PDL, spin_ns, ms_e * 1e3 / R, ms_e * 1e3 / R - spin_ns * 1e-3,
          ms_g * 1e3 / R, ms_g * 1e3 / R - spin_ns * 1e-3);
   CK(cudaGraphExecDestroy(ge)); CK(cudaGraphDestroy(g));
 }
@@ -62,10 +63,12 @@ void run(cudaStream_t s, long long spin_ns) {
 int main() {
   CK(cudaSetDevice(0));
   cudaStream_t s; CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  CK(cudaFuncSetAttribute((const void*)k_spin<150, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 << 10));
+  CK(cudaFuncSetAttribute((const void*)k_spin<150, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 << 10));
   for (long long ns : {2000LL, 10000LL}) {
     run<1, 0>(s, ns); run<1, 1>(s, ns);
     run<150, 0>(s, ns); run<150, 1>(s, ns);
-    run<500, 0>(s, ns); run<500, 1>(s, ns);
+    run<150, 0>(s, ns, 200 << 10); run<150, 1>(s, ns, 200 << 10);
   }
   return 0;
 }
