@@ -348,12 +348,15 @@ int run(fc_comm* c, int coll, const void* const* sends, void* const* recvs, size
     const long long need = ag_base + (long long)pl.max_ag_slot_units * llu + 256LL * pl.max_ag_slots;
     const long long moved = (coll == FC_REDUCE_SCATTER) ? total * es : S * es * N;
     const bool want = c->proto == 1 || moved <= c->ll_max;
-    if (aligned && want && need <= (long long)c->scratch_bytes) {  // LL region = scratch_bytes
+    // the LL region (scratch_bytes) is two halves used by alternate epochs
+    const long long half = (long long)(c->scratch_bytes / 2) / 4096 * 4096;
+    if (aligned && want && need <= half) {
       proto = 1;
       n = std::min<long long>(chunks_for(c->ll_chunk_max, c->ll_worker_warps), kMaxC);
       W = n;
       P.ll_unit_bytes = llu;
       P.ll_region_off = (long long)c->scratch_bytes;
+      P.ll_half = half;
       P.ll_ag_base = ag_base;
       P.worker_warps = c->ll_worker_warps;
     } else if (c->proto == 1) {

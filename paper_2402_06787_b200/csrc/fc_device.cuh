@@ -838,30 +838,20 @@ __device__ void run_item_ll(const FcParams& P, int me, FcCtl* ctl, const int* T,
   const bool leader = (wl == 0 && lane == 0);
   const unsigned long long flag = (unsigned long long)e;
 
-  // entry barrier only (no chunk flags in LL): destinations must have entered
-  if (leader) {
-    bool ok = true;
-    if (kind != FC_K_WAIT_AG && kind != FC_K_RS_ROOT) {
-      const int nx = (kind == FC_K_RS_FWD) ? 1 : n_ag;
-      for (int j = 0; j < nx && ok; ++j) {
-        const int x = (kind == FC_K_RS_FWD) ? rs_parent : __ldg(T + TW_AG_CHILD + j);
-        if (!((ready_mask >> x) & 1u)) {
-          ok = wait_ready(P, me, x, e, ctl);
-          if (ok) ready_mask |= 1u << x;
-        }
-      }
-    }
-    sh->ok = ok ? 1 : 0;
-    if (P.trace) t_ready = globaltimer();
-  }
-  worker_sync<WW>(wk);
-  if (!sh->ok) return;
+  // No entry wait.  LL stores only ever land in peers' staging, never in user
+  // buffers, and staging alternates between two halves by epoch parity.  A
+  // rank in launch e has finished e-1, which needed every rank's data (every
+  // rank roots a non-empty tree, or feeds one that reaches every rank), so
+  // every rank has finished e-2, the last user of this half.  Lines left there
+  // carry epoch e-2, never e.
+  (void)ready_mask;
+  if (P.trace && leader) t_ready = globaltimer();
 
   const int g = lane >> 3, gl = lane & 7;
   const long long slot_ofs = -lw * 128LL;  // line l of the window at slot + (l - lw)*128
+  const long long ll_off = P.ll_region_off + (long long)(e & 1u) * P.ll_half;
   auto slot_ptr = [&](int rank, long long region, int slot, int prefix) -> char* {
-    return P.scratch[rank] + P.ll_region_off + region + P.ll_unit_bytes * prefix + 256LL * slot +
-           slot_ofs;
+    return P.scratch[rank] + ll_off + region + P.ll_unit_bytes * prefix + 256LL * slot + slot_ofs;
   };
   const bool polls = (kind == FC_K_AG_FWD || kind == FC_K_WAIT_AG);
   const char* my_ag = polls ? slot_ptr(me, P.ll_ag_base, __ldg(T + TW_AG_MYSLOT),

@@ -137,6 +137,7 @@ struct FcParams {
   long long ll_unit_bytes;  // LL: staging bytes per unit multiplicity per window
   long long ll_ag_base;     // LL: offset of the broadcast staging within the LL region
   long long ll_region_off;  // LL: offset of the (zeroed, dedicated) LL region from scratch
+  long long ll_half;        // LL: the region's two halves alternate by launch-epoch parity
   FcTraceRec* trace;
   unsigned* trace_count;
   unsigned trace_cap;

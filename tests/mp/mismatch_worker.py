@@ -1,6 +1,8 @@
 """torchrun worker: ranks that pass differently registered output buffers to
 one allgather get a loud device error (FC_DEVERR_BUFFER_MISMATCH), not
-silently misplaced data.  Prints `MISMATCH rank r OK|FAIL`."""
+silently misplaced data.  Only the chunk-flag protocol stores straight into
+peers' output buffers (LL128 stores land in the library's staging), so the
+check is exercised with that protocol.  Prints `MISMATCH rank r OK|FAIL`."""
 
 import os
 import sys
@@ -23,7 +25,7 @@ def main():
     dist.init_process_group("nccl", device_id=dev)
     rank, n = dist.get_rank(), dist.get_world_size()
     comm = ForestCollComm(nvswitch_doc(n), rank=rank, world_size=n, device=local,
-                          options={"timeout_ms": 3000})
+                          options={"timeout_ms": 3000, "proto": 0})
     S = 4096
     inp = torch.full((S,), float(rank), device=dev)
     a = comm.empty(n * S)
