@@ -106,6 +106,7 @@ class _CommBase:
         self._prune = prune
         self._schedules = dict(schedules or {})
         self._plans = {}
+        self._capable = {}  # switch capability -> bool (cached: checked on every call)
         self._comm = None
         self._lib = _lib.load()
         if topology_doc is not None and len(compute_ids(topology_doc)) != nranks:
@@ -352,12 +353,11 @@ class ForestCollComm(_CommBase):
         """The topology routes every pair through one switch that declares
         `capability` (multicast / aggregation): the pruned forest then sends
         each shard into the switch once (schedule.py:237-306)."""
-        cache = self.__dict__.setdefault("_capable", {})
-        hit = cache.get(capability)
+        hit = self._capable.get(capability)
         if hit is None:
             sws = [] if self.topology is None else \
                 [n for n in self.topology["nodes"] if n["kind"] == "switch"]
-            hit = cache[capability] = len(sws) == 1 and bool(sws[0].get(capability, False))
+            hit = self._capable[capability] = len(sws) == 1 and bool(sws[0].get(capability, False))
         return hit
 
     def _usable_topology(self, doc, world_size):
