@@ -40,6 +40,16 @@
  * void*; calls are stream-ordered and asynchronous; a communicator is not
  * re-entrant across host threads and all calls on one communicator must be
  * issued in the same order on every rank (NCCL semantics).
+ *
+ * Ordering: the collectives of one communicator execute one at a time in
+ * issue order, also when issued on different streams (a call on a new stream
+ * waits for an event recorded on the previous call's stream at issue time).
+ * Outside CUDA-graph capture no further synchronisation is needed.
+ *
+ * Output buffers: every rank must pass the same registered buffer (same
+ * registration, offset and size).  Each launch publishes a tag of its output
+ * with its entry epoch; a mismatch is a device error (FC_ERR_DEVICE from
+ * fc_comm_check) rather than misplaced peer stores.
  */
 #ifndef FORESTCOLL_H_
 #define FORESTCOLL_H_
@@ -60,7 +70,7 @@ extern "C" {
 #define FC_ERR_UNSUPPORTED 3
 #define FC_ERR_NOT_REGISTERED 4
 #define FC_ERR_PLAN 5
-#define FC_ERR_DEVICE 6 /* device-side failure (flag wait timed out) */
+#define FC_ERR_DEVICE 6 /* device-side failure: flag wait timed out, or peers passed different outputs */
 
 /* collectives (plan slots) */
 #define FC_ALLGATHER 0
