@@ -175,23 +175,33 @@ def _check_group(comm, group):
 
 
 class ForestCollAllGather(_AllGatherBase):
-    """FSDP2 ``AllGather``: outputs come from a ``SymmetricPool``.  When the
-    pool is full, the output is a fresh tensor registered with the peers.
-    That registration is collective and the pool state is identical on every
-    rank, so every rank takes the same path."""
+    """FSDP2 ``AllGather``: outputs come from ``SymmetricPool`` segments.
+    When no segment has room, a new segment of at least ``pool_bytes`` is
+    registered.  Registration is collective, and the pool state is identical
+    on every rank, so every rank grows at the same call.  Segments are reused
+    and never leak per-call buffers."""
 
     def __init__(self, comm, pool_bytes: int = 1 << 30, pool: SymmetricPool | None = None):
         self.comm = comm
-        self.pool = pool if pool is not None else SymmetricPool(comm, pool_bytes)
+        self.pool_bytes = int(pool_bytes)
+        self.pools = [pool if pool is not None else SymmetricPool(comm, self.pool_bytes)]
+
+    @property
+    def pool(self) -> SymmetricPool:
+        return self.pools[0]
 
     def allocate(self, size, *, dtype: torch.dtype, device: torch.device) -> torch.Tensor:
         numel = 1
         for s in size:
             numel *= int(s)
-        t = self.pool.empty(numel, dtype)
-        if t is None:
-            t = torch.empty(numel, dtype=dtype, device=device)
-            self.comm.register(t)
+        for p in self.pools:
+            t = p.empty(numel, dtype)
+            if t is not None:
+                break
+        else:
+            es = torch.tensor([], dtype=dtype).element_size()
+            self.pools.append(SymmetricPool(self.comm, max(self.pool_bytes, 2 * numel * es)))
+            t = self.pools[-1].empty(numel, dtype)
         return t.view(*[int(s) for s in size])
 
     def __call__(self, output_tensor, input_tensor, group=None, async_op: bool = False):

@@ -47,7 +47,8 @@ def main():
     dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     rank, n = dist.get_rank(), dist.get_world_size()
     comm = ForestCollComm(nvswitch_doc(n), rank=rank, world_size=n, device=local)
-    ag = ForestCollAllGather(comm, pool_bytes=64 << 20)
+    # a small first segment: the pool must grow (collectively) during training
+    ag = ForestCollAllGather(comm, pool_bytes=1 << 20)
     rs = ForestCollReduceScatter(comm)
     fails = []
     for mp, tol in ((False, 1e-5), (True, 2e-2)):
@@ -62,9 +63,11 @@ def main():
         if not all(torch.allclose(a, b, rtol=tol, atol=tol) for a, b in zip(ref, got)):
             worst = max(float((a - b).abs().max()) for a, b in zip(ref, got))
             fails.append(f"mp={mp} max|diff|={worst:.3g}")
-    used = ag.pool.nbytes - ag.pool.free_bytes
-    print(f"FSDP rank {rank} {'OK' if not fails else 'FAIL ' + '; '.join(fails)} pool_in_use={used}",
-          flush=True)
+    if len(ag.pools) < 2:
+        fails.append("pool never grew")
+    used = sum(p.nbytes - p.free_bytes for p in ag.pools)
+    print(f"FSDP rank {rank} {'OK' if not fails else 'FAIL ' + '; '.join(fails)} "
+          f"segments={len(ag.pools)} in_use={used}", flush=True)
     comm.close()
     dist.destroy_process_group()
     sys.exit(0 if not fails else 1)

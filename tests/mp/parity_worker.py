@@ -107,6 +107,36 @@ def run_all(comm, rank, n, dev):
             ref = fo.allreduce(comm.schedule("allreduce"), hs, name, op="avg")[rank]
             if not np.array_equal(host(buf).view(np.uint8), ref.view(np.uint8)):
                 fails.append(f"allreduce avg {name} count={n * S}")
+    # CUDA graph: capture an allgather + allreduce once, replay with new inputs
+    S = 5000
+    gin = torch.empty(S, device=dev)
+    gout = comm.empty(n * S, dtype=torch.float32)
+    gbuf = comm.empty(n * S, dtype=torch.float32)
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        comm.all_gather(gout, gin)
+        comm.all_reduce(gbuf)
+    torch.cuda.current_stream().wait_stream(side)
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        comm.all_gather(gout, gin)
+        comm.all_reduce(gbuf)
+    for rep in range(3):
+        sends = [seeded(S, torch.float32, 8100 + 10 * rep + r) for r in range(n)]
+        ins = [seeded(n * S, torch.float32, 8500 + 10 * rep + r) for r in range(n)]
+        gin.copy_(sends[rank].to(dev))
+        gbuf.copy_(ins[rank].to(dev))
+        dist.barrier()
+        graph.replay()
+        torch.cuda.synchronize()
+        ref = fo.allgather(comm.schedule("allgather"), [host(x) for x in sends])[rank]
+        if not np.array_equal(host(gout).view(np.uint8), ref.view(np.uint8)):
+            fails.append(f"graph replay {rep} allgather")
+        ref = fo.allreduce(comm.schedule("allreduce"), [host(x) for x in ins], "float32")[rank]
+        if not np.array_equal(host(gbuf).view(np.uint8), ref.view(np.uint8)):
+            fails.append(f"graph replay {rep} allreduce")
     # back-to-back calls reusing buffers (entry barrier / epoch reuse)
     S = 1 << 18
     out = comm.empty(n * S, dtype=torch.float32)
