@@ -111,6 +111,7 @@ extern "C" {
 #define FC_OPT_LL_WORKER_WARPS 13 /* warps per work item, LL128 (default 4 real, 1 virtual) */
 #define FC_OPT_NVLS_CTAS 14    /* CTAs of the NVLS (multicast) kernel (default 32) */
 #define FC_OPT_PDL 15          /* programmatic dependent launch (default 1) */
+#define FC_OPT_CHUNK_TAIL 16   /* chunk flags: last k chunks of a slice halve in size (default 4) */
 
 typedef struct fc_comm fc_comm_t;
 

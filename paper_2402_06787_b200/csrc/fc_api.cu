@@ -82,6 +82,7 @@ struct fc_comm {
   long long ll_chunk_max = 64 << 10;
   int ll_worker_warps = 4;
   long long ll_max = 512LL << 20;  // auto: LL128 when bytes moved per rank <= this (and staging fits)
+  int chunk_tail = 4;              // chunk-flag protocol: halving tail chunks per slice
   cudaStream_t side = nullptr;
   // NVLS pool (multicast object bound to a per-rank physical allocation)
   unsigned long long nvls_mc = 0, nvls_mem = 0;
@@ -366,8 +367,15 @@ int run(fc_comm* c, int coll, const void* const* sends, void* const* recvs, size
   if (proto == 0) {
     n = chunks_for(c->chunk_max, c->worker_warps);
     W = std::min<long long>(n, kMaxC);
-    auto unit_for = [&](long long w) {
-      return (long long)align_up((size_t)((slice_unit * w + n - 1) / n), FC_ALIGN);
+    // shrinking tail chunks (see chunk_bound in fc_device.cuh): only when the
+    // slice has enough chunks that the halved ones stay >= chunk_min-ish
+    int tail = 0;
+    while (tail < c->chunk_tail && (n >> (tail + 1)) >= 8) ++tail;
+    P.tail = tail;
+    const long long wreg = 1LL << tail;
+    const long long fsum = wreg * (n - tail) + wreg - 1;  // chunk_prefix(n, n, tail)
+    auto unit_for = [&](long long w) {  // bytes of the widest window of w chunks, per unit
+      return (long long)align_up((size_t)((slice_unit * w * wreg + fsum - 1) / fsum), FC_ALIGN);
     };
     if (coll != FC_ALLGATHER) {
       auto need = [&](long long w) {
@@ -809,6 +817,10 @@ int fc_comm_set_option(fc_comm_t* c, int option, long long v) {
     case FC_OPT_PDL:
       c->pdl = v ? 1 : 0;
       return FC_SUCCESS;
+    case FC_OPT_CHUNK_TAIL:
+      if (v < 0 || v > 8) return fail(c, FC_ERR_INVALID_ARG, "chunk_tail out of range [0, 8]");
+      c->chunk_tail = (int)v;
+      return FC_SUCCESS;
     case FC_OPT_NVLS_CTAS:
       if (v < 1 || v > 1024) return fail(c, FC_ERR_INVALID_ARG, "nvls_ctas out of range");
       c->nvls_ctas = (int)v;
@@ -844,6 +856,7 @@ int fc_comm_get_option(fc_comm_t* c, int option, long long* v) {
     case FC_OPT_LL_CHUNK_MAX: *v = c->ll_chunk_max; return FC_SUCCESS;
     case FC_OPT_NVLS_CTAS: *v = c->nvls_ctas; return FC_SUCCESS;
     case FC_OPT_PDL: *v = c->pdl; return FC_SUCCESS;
+    case FC_OPT_CHUNK_TAIL: *v = c->chunk_tail; return FC_SUCCESS;
     case FC_OPT_LL_WORKER_WARPS: *v = c->ll_worker_warps; return FC_SUCCESS;
     default: return fail(c, FC_ERR_INVALID_ARG, "unknown option %d", option);
   }

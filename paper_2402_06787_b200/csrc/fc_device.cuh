@@ -590,11 +590,24 @@ struct Geo {
   long long base, lo, hi;
 };
 
-__device__ __forceinline__ long long chunk_bound(const Geo& g, int c, int n) {
+// Chunk c of n covers [bound(c), bound(c+1)).  Regular chunks weigh 2^tail;
+// the last `tail` chunks halve at each step (2^(tail-1) ... 1), so every
+// launch ends on small chunks: the final hops of deep chains and the last
+// claims finish sooner.  fc_api.cu (chunk_prefix) sizes scratch windows with
+// the same weights.
+__device__ __forceinline__ long long chunk_prefix(int c, int n, int tail) {
+  const int reg = n - tail;
+  const long long w = 1LL << tail;
+  if (c <= reg) return w * c;
+  return w * reg + (w - (1LL << (tail - (c - reg))));
+}
+
+__device__ __forceinline__ long long chunk_bound(const Geo& g, int c, int n, int tail) {
   if (c <= 0) return g.lo;
   if (c >= n) return g.hi;
   const long long len = g.hi - g.lo;
-  long long b = (g.lo + len * c / n) & ~(long long)(FC_ALIGN - 1);
+  const long long F = chunk_prefix(n, n, tail);
+  long long b = (g.lo + len * chunk_prefix(c, n, tail) / F) & ~(long long)(FC_ALIGN - 1);
   return b < g.lo ? g.lo : b;
 }
 
@@ -674,9 +687,9 @@ __device__ void run_item(const FcParams& P, int me, FcCtl* ctl, const int* T, in
   g.base = (long long)root * P.stride_elems * es;
   g.lo = g.base + (Sr * __ldg(T + TW_MLO) / P.k) * es;
   g.hi = g.base + (Sr * __ldg(T + TW_MHI) / P.k) * es;
-  const long long b0 = chunk_bound(g, c, P.nchunks);
-  const long long b1 = chunk_bound(g, c + 1, P.nchunks);
-  const long long wbase = chunk_bound(g, P.c0, P.nchunks) & ~(long long)(FC_ALIGN - 1);
+  const long long b0 = chunk_bound(g, c, P.nchunks, P.tail);
+  const long long b1 = chunk_bound(g, c + 1, P.nchunks, P.tail);
+  const long long wbase = chunk_bound(g, P.c0, P.nchunks, P.tail) & ~(long long)(FC_ALIGN - 1);
   const int fi = c - P.c0;
   unsigned* const myflags = P.flags[me];
   const int n_ag = __ldg(T + TW_N_AG_CHILD);

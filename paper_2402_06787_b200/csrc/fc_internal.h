@@ -123,6 +123,7 @@ struct FcParams {
   float scale;  // FC_AVG: fp32 1/N applied once by tree roots
   unsigned long long tag;  // identity of the peer-mapped output (registration, offset, size)
   int nchunks;  // chunks per tree slice for the whole call
+  int tail;     // chunk-flag protocol: the last `tail` chunks halve in size, step by step
   int c0, c1;   // chunk window of this launch
   int maxc;     // flag stride per tree / slot
   int cnt_off;      // word offset of per-tree leaf arrival counters

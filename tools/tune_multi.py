@@ -32,6 +32,7 @@ def main():
     ap.add_argument("--pdl", default="1")
     ap.add_argument("--chunk-min", default="16384")
     ap.add_argument("--dtype", default="float32")
+    ap.add_argument("--tail", default="4")
     ap.add_argument("--iters", type=int, default=10)
     args = ap.parse_args()
     local = int(os.environ["LOCAL_RANK"])
@@ -63,8 +64,10 @@ def main():
                     args.ctas.split(","), args.chunks.split(","), args.ipw.split(","),
                     args.lag.split(","), args.mode.split(","), args.dma.split(","),
                     args.ww.split(","), args.proto.split(",")):
-              for pdl, cmin in itertools.product(args.pdl.split(","), args.chunk_min.split(",")):
+              for pdl, cmin, tail in itertools.product(args.pdl.split(","), args.chunk_min.split(","),
+                                                       args.tail.split(",")):
                 comm.set_option("chunk_min", int(cmin))
+                comm.set_option("chunk_tail", int(tail))
                 comm.set_option("pdl", int(pdl))
                 comm.set_option("proto", int(proto))
                 comm.set_option("worker_warps", int(ww))
@@ -79,7 +82,7 @@ def main():
                 ms = timed(fn, args.iters, 3, dist)
                 info = comm.last_call_info()
                 if rank == 0:
-                    print(f"{coll:15s} {mib:6d}MiB ctas={ctas:>4s} chunk={int(ch)//1024:5d}K ipw={ipw} lag={lag:>3s} ww={ww} p={info["proto"]} pdl={pdl} cmin={int(cmin)//1024}K "
+                    print(f"{coll:15s} {mib:6d}MiB ctas={ctas:>4s} chunk={int(ch)//1024:5d}K ipw={ipw} lag={lag:>3s} ww={ww} p={info["proto"]} pdl={pdl} cmin={int(cmin)//1024}K tail={tail} "
                           f"n={info['nchunks']:5d} L={info['launches']} ms={ms:8.4f} "
                           f"algbw={gbs(M, ms):8.1f} frac_T*={tstar*1e3/ms:6.3f}", flush=True)
     comm.check()

@@ -24,6 +24,7 @@ def main():
     ap.add_argument("--chunks", default="131072,262144,524288")
     ap.add_argument("--proto", default="-1")
     ap.add_argument("--iters", type=int, default=10)
+    ap.add_argument("--tail", default="4")
     args = ap.parse_args()
     local = int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
@@ -48,14 +49,15 @@ def main():
             fn = lambda: comm.reduce_scatter(outs, ins)  # noqa: E731
         t = comm.t_star(args.coll, M)
         for proto in [int(x) for x in args.proto.split(",")]:
-            for ch in [int(x) for x in args.chunks.split(",")]:
+            for ch, tail in [(int(x), int(y)) for x in args.chunks.split(",") for y in args.tail.split(",")]:
+                comm.set_option("chunk_tail", tail)
                 comm.set_option("proto", proto)
                 comm.set_option("chunk_max", ch)
                 comm.set_option("ll_chunk_max", min(ch, 1 << 20))
                 ms = timed(fn, args.iters, 2, dist)
                 info = comm.last_call_info()
                 if p == 0:
-                    print(f"{args.coll} N={N} on {P} GPUs {mib} MiB proto={info['proto']} chunk={ch >> 10}K "
+                    print(f"{args.coll} N={N} on {P} GPUs {mib} MiB proto={info['proto']} chunk={ch >> 10}K tail={tail} "
                           f"n={info['nchunks']} L={info['launches']}: {ms * 1e3:.1f} us "
                           f"algbw {gbs(M, ms):.1f} GB/s (T* frac {t * 1e3 / ms:.3f})", flush=True)
     comm.check()
