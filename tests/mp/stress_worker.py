@@ -56,8 +56,47 @@ def main():
         if not ok:
             fails += 1
             print(f"rank {rank} iter {it} {coll} S={S} proto={proto} MISMATCH", flush=True)
+    # bursts: several collectives queued back to back with no host sync, on two
+    # alternating streams, each into its own output, verified only at the end.
+    # Exercises launch-to-launch reuse of staging / scratch / flags (LL128
+    # has no entry handshake) and the cross-stream ordering of one comm.
+    streams = [torch.cuda.current_stream(), torch.cuda.Stream()]
+    bufs = [comm.empty(n * (1 << 18), dtype=torch.int32) for _ in range(8)]
+    for burst in range(max(1, iters // 20)):
+        pending = []
+        for j in range(8):
+            coll = rng.choice(["allgather", "reduce_scatter", "allreduce"])
+            comm.set_option("proto", rng.choice([-1, 0]))
+            S = rng.choice([3, 256, 4096, 65536 + 8, 1 << 18])
+            g = torch.Generator().manual_seed(100000 + 8 * burst + j)
+            allin = torch.randint(-2**20, 2**20, (n, n * S if coll != "allgather" else S),
+                                  generator=g, dtype=torch.int32)
+            src = allin[rank].to(dev)
+            s = streams[j % 2]
+            s.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(s):
+                if coll == "allgather":
+                    out = bufs[j][: n * S]
+                    comm.all_gather(out, src)
+                    want = allin.reshape(-1)
+                elif coll == "reduce_scatter":
+                    out = torch.empty(S, dtype=torch.int32, device=dev)
+                    comm.reduce_scatter(out, src)
+                    want = allin.sum(0, dtype=torch.int64).to(torch.int32)[rank * S:(rank + 1) * S]
+                else:
+                    out = bufs[j][: n * S]
+                    out.copy_(src)
+                    comm.all_reduce(out)
+                    want = allin.sum(0, dtype=torch.int64).to(torch.int32)
+            pending.append((coll, S, out, want, src))
+        torch.cuda.synchronize()
+        for coll, S, out, want, _ in pending:
+            if not torch.equal(out.cpu(), want):
+                fails += 1
+                print(f"rank {rank} burst {burst} {coll} S={S} MISMATCH", flush=True)
     comm.check()
-    print(f"STRESS rank {rank} {'OK' if not fails else f'FAIL {fails}'} ({iters} calls)", flush=True)
+    print(f"STRESS rank {rank} {'OK' if not fails else f'FAIL {fails}'} ({iters} calls + bursts)",
+          flush=True)
     comm.close()
     dist.destroy_process_group()
     sys.exit(1 if fails else 0)
