@@ -1,3 +1,7 @@
+// Probe: outputs of sm_100's cvt.rn.bf16x2.f32 for NaN, infinity, ties and
+// denormals; these vectors pin oracle/forest_oracle.py::f32_to_bf16
+// (tests/test_oracle.py::test_bf16_rounding_matches_sm100_cvt_vectors).
+//   nvcc -gencode arch=compute_100a,code=sm_100a -o cvt_probe tools/cvt_probe.cu
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
 #include <cstdio>

@@ -1,3 +1,5 @@
+"""Probe NVSwitch multicast support per device (CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED)
+and the multicast granularity, through cuda-python."""
 from cuda.bindings import driver as cu
 import sys
 err, = cu.cuInit(0)

@@ -1,3 +1,7 @@
+"""Host<->device copy bandwidth with pinned memory (H2D, D2H, both at once),
+one GPU or several at once: the bound on bench.py's e2e figure.
+    python tools/pcie_probe.py                      # one GPU
+    for i in 0 1 2 3; do LOCAL_RANK=$i python tools/pcie_probe.py & done; wait"""
 import torch, time, os, sys
 dev = int(os.environ.get("LOCAL_RANK", 0)); torch.cuda.set_device(dev)
 N = 1 << 30
