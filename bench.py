@@ -552,8 +552,9 @@ def sweep_multi(comm, dist, n, dev, args):
 
 
 def nvls_points(dist, dev, n, args):
-    """Allreduce of the forest pruned for a multicast/aggregation NVSwitch
-    (schedule.py:237-306), executed by the NVLS engine (multimem)."""
+    """The forest pruned for a multicast/aggregation NVSwitch
+    (schedule.py:237-306), executed by the NVLS engine: small allgathers as LL
+    over multicast (one switch hop), allreduce with multimem.ld_reduce/st."""
     import torch
 
     from paper_2402_06787_b200 import ForestCollComm
@@ -565,6 +566,17 @@ def nvls_points(dist, dev, n, args):
         c.close()
         return {"skipped": "no NVSwitch multicast support"}
     out = []
+    # small allgathers: LL over multicast (one switch hop), ordinary buffers
+    for kib in (64, 1024):
+        M = kib * 1024
+        S = M // n // 4
+        inp = torch.randn(S, device=dev)
+        o = torch.empty(n * S, device=dev)
+        ms = timed(lambda: c.all_gather(o, inp), steps_for(M, max(5, args.steps)), 3, dist)
+        t = c.t_star("allgather", M)
+        out.append({"collective": "allgather", "engine": c.last_call_info()["proto"],
+                    "M_bytes": M, "dtype": "float32", "ms": round(ms, 4),
+                    "algbw_GBps": round(gbs(M, ms), 2), "frac_of_t_star": round(t * 1e3 / ms, 4)})
     for mib in (25, 1000):
         M = mib * MIB
         buf = c.nvls_empty(M // 2, torch.bfloat16)

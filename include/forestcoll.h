@@ -112,6 +112,8 @@ extern "C" {
 #define FC_OPT_NVLS_CTAS 14    /* CTAs of the NVLS (multicast) kernel (default 32) */
 #define FC_OPT_PDL 15          /* programmatic dependent launch (default 1) */
 #define FC_OPT_CHUNK_TAIL 16   /* chunk flags: last k chunks of a slice halve in size (default 4) */
+#define FC_OPT_NVLS_LL_MAX 17  /* NVLS allgather: LL multicast when output bytes <= this (default max(2 MiB, N x 512 KiB)) */
+#define FC_OPT_NVLS_LL_HALF 18 /* read-only: bytes per LL staging half, reserved x2 at the pool top */
 
 typedef struct fc_comm fc_comm_t;
 
@@ -180,6 +182,9 @@ int fc_nvls_supported(int device);
 int fc_nvls_create(fc_comm_t* comm, size_t bytes, void* handle);
 int fc_nvls_attach(fc_comm_t* comm, const void* handle);
 int fc_nvls_bind(fc_comm_t* comm, void** pool);
+/* allgather: small calls (output <= FC_OPT_NVLS_LL_MAX, 8-byte aligned, staging
+ * fits) use the LL multicast protocol and accept any device buffers; larger
+ * calls need `recv` inside the pool (below the reserved LL staging). */
 int fc_nvls_allgather(fc_comm_t* comm, const void* send, void* recv,
                       size_t sendcount, int dtype, void* stream);
 int fc_nvls_reduce_scatter(fc_comm_t* comm, const void* send, void* recv,

@@ -91,6 +91,9 @@ struct fc_comm {
   size_t nvls_bytes = 0;
   int nvls_bound = 0;
   int nvls_ctas = 32;
+  long long nvls_ll_max = -1;         // NVLS allgather: LL multicast up to this output size
+                                      // (-1: max(2 MiB, N x 512 KiB), measured crossover)
+  long long nvls_ll_half = 0;         // LL staging half (2 halves reserved at the pool top)
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   cudaEvent_t ev_last = nullptr;     // cross-stream ordering of this comm's collectives
   cudaStream_t last_stream = nullptr;
@@ -579,10 +582,18 @@ int run_nvls(fc_comm* c, int mode, const void* send, void* buf, void* out, size_
     total = shard * N;
   }
   if (total == 0) return FC_SUCCESS;
-  if (b < lo || b + (size_t)total > lo + c->nvls_bytes)
-    return fail(c, FC_ERR_NOT_REGISTERED, "buffer %p is not inside the NVLS pool", buf);
-  if ((b - lo) % 16 || shard % 16 || total % 16)
-    return fail(c, FC_ERR_UNSUPPORTED, "NVLS needs 16-byte aligned shards");
+  const size_t usable = c->nvls_bytes - 2 * (size_t)c->nvls_ll_half;  // LL staging on top
+  const long long ll_max =
+      c->nvls_ll_max >= 0 ? c->nvls_ll_max : std::max<long long>(2LL << 20, N * (512LL << 10));
+  if (mode == 0 && total <= ll_max && shard % 8 == 0 && (uintptr_t)send % 8 == 0 &&
+      (uintptr_t)buf % 8 == 0 && 2LL * shard * N <= c->nvls_ll_half)
+    mode = 3;  // LL over multicast: any device buffers
+  if (mode != 3) {
+    if (b < lo || b + (size_t)total > lo + usable)
+      return fail(c, FC_ERR_NOT_REGISTERED, "buffer %p is not inside the NVLS pool", buf);
+    if ((b - lo) % 16 || shard % 16 || total % 16)
+      return fail(c, FC_ERR_UNSUPPORTED, "NVLS needs 16-byte aligned shards");
+  }
   FcNvlsParams P;
   memset(&P, 0, sizeof(P));
   P.nranks = N;
@@ -597,6 +608,12 @@ int run_nvls(fc_comm* c, int mode, const void* send, void* buf, void* out, size_
   P.mc = c->nvls_mc_va + (b - lo);
   P.send = (const char*)send;
   P.out = (char*)out;
+  if (mode == 3) {
+    P.out = (char*)buf;
+    P.mc_stage = c->nvls_mc_va + usable;
+    P.uc_stage = c->nvls_uc_va + usable;
+    P.ll_half = c->nvls_ll_half;
+  }
   P.shard_bytes = shard;
   P.total_bytes = total;
   P.timeout_ns = c->timeout_ms * 1000000LL;
@@ -611,7 +628,7 @@ int run_nvls(fc_comm* c, int mode, const void* send, void* buf, void* out, size_
     if (st) return st;
   }
   c->info[0] = 1;
-  c->info[5] = 2;  // engine: nvls
+  c->info[5] = mode == 3 ? 3 : 2;  // engine: nvls (3: LL multicast)
   return FC_SUCCESS;
 }
 
@@ -821,6 +838,12 @@ int fc_comm_set_option(fc_comm_t* c, int option, long long v) {
       if (v < 0 || v > 8) return fail(c, FC_ERR_INVALID_ARG, "chunk_tail out of range [0, 8]");
       c->chunk_tail = (int)v;
       return FC_SUCCESS;
+    case FC_OPT_NVLS_LL_MAX:
+      if (v < 0) return fail(c, FC_ERR_INVALID_ARG, "nvls_ll_max < 0");
+      c->nvls_ll_max = v;
+      return FC_SUCCESS;
+    case FC_OPT_NVLS_LL_HALF:
+      return fail(c, FC_ERR_INVALID_ARG, "nvls_ll_half is read-only");
     case FC_OPT_NVLS_CTAS:
       if (v < 1 || v > 1024) return fail(c, FC_ERR_INVALID_ARG, "nvls_ctas out of range");
       c->nvls_ctas = (int)v;
@@ -857,6 +880,11 @@ int fc_comm_get_option(fc_comm_t* c, int option, long long* v) {
     case FC_OPT_NVLS_CTAS: *v = c->nvls_ctas; return FC_SUCCESS;
     case FC_OPT_PDL: *v = c->pdl; return FC_SUCCESS;
     case FC_OPT_CHUNK_TAIL: *v = c->chunk_tail; return FC_SUCCESS;
+    case FC_OPT_NVLS_LL_MAX:
+      *v = c->nvls_ll_max >= 0 ? c->nvls_ll_max
+                               : std::max<long long>(2LL << 20, c->nranks * (512LL << 10));
+      return FC_SUCCESS;
+    case FC_OPT_NVLS_LL_HALF: *v = c->nvls_ll_half; return FC_SUCCESS;
     case FC_OPT_LL_WORKER_WARPS: *v = c->ll_worker_warps; return FC_SUCCESS;
     default: return fail(c, FC_ERR_INVALID_ARG, "unknown option %d", option);
   }
@@ -1210,6 +1238,8 @@ int fc_nvls_bind(fc_comm_t* c, void** pool) {
   FC_DRV(c, d.setAccess(mcva, c->nvls_bytes, &acc, 1));
   c->nvls_uc_va = (char*)uc;
   c->nvls_mc_va = (char*)mcva;
+  // LL multicast staging: two halves at the top of the pool (allgather <= nvls_ll_max)
+  c->nvls_ll_half = (long long)(std::min<size_t>(c->nvls_bytes / 8, 16u << 20) / 4096 * 4096);
   FC_CUDA(c, cudaMemset(c->nvls_uc_va, 0, c->nvls_bytes));
   FC_CUDA(c, cudaDeviceSynchronize());
   c->nvls_bound = 1;

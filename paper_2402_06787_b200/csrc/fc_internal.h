@@ -160,6 +160,11 @@ struct FcNvlsParams {
   long long shard_bytes;          // bytes per root shard
   long long total_bytes;          // bytes of the N-shard buffer in the pool
   long long timeout_ns;
+  // mode 3 (allgather, LL over multicast): staging at the top of the pool,
+  // two halves alternating by epoch parity; 16-byte units {d0, e, d1, e}
+  char* mc_stage;                 // multicast VA of the staging region
+  const char* uc_stage;           // this GPU's view of the same region
+  long long ll_half;              // bytes per half
 };
 
 // Kernel entry (fc_kernel.cu).  Returns a cudaError_t value.

@@ -190,11 +190,82 @@ __global__ void __launch_bounds__(FC_NVLS_THREADS) fc_nvls_kernel(const __grid_c
   }
 }
 
+// Allgather of the multicast-pruned forest with an LL protocol: every root
+// stores its shard once into the switch as 16-byte units {d0, e, d1, e} (each
+// 8-byte half pairs data with the launch epoch, NCCL's LL idea); the switch
+// replicates it into every GPU's staging, and receivers poll their local copy
+// until both flags read e.  No entry or exit barrier: staging alternates
+// between two halves by epoch parity (a rank in launch e has finished e-1,
+// which needed every rank's shard, so every rank has finished e-2, the last
+// user of this half).  Output and input may be any device buffers.
+__global__ void __launch_bounds__(FC_NVLS_THREADS) fc_nvls_ll_ag_kernel(const __grid_constant__ FcNvlsParams P) {
+  __shared__ unsigned s_e;
+  FcCtl* ctl = P.ctl;
+  if (threadIdx.x == 0) s_e = *reinterpret_cast<volatile unsigned*>(&ctl->epoch) + 1;
+  __syncthreads();
+  const unsigned e = s_e;
+  const long long half = (long long)(e & 1u) * P.ll_half;
+  const long long slot = 2 * P.shard_bytes;  // staging bytes per root
+  const long long nunits = P.shard_bytes / 8;
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  // 1. own shard: one multicast store per 8 payload bytes; local copy direct
+  const uint2* src = reinterpret_cast<const uint2*>(P.send);
+  uint2* own = reinterpret_cast<uint2*>(P.out + (long long)P.rank * P.shard_bytes);
+  char* mst = P.mc_stage + half + (long long)P.rank * slot;
+  for (long long i = tid; i < nunits; i += stride) {
+    const uint2 v = __ldg(src + i);
+    asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(mst + 16 * i),
+                 "f"(__uint_as_float(v.x)), "f"(__uint_as_float(e)), "f"(__uint_as_float(v.y)),
+                 "f"(__uint_as_float(e))
+                 : "memory");
+    own[i] = v;
+  }
+  // 2. every other root's shard from the local staging copy
+  bool ok = true;
+  const unsigned long long t0 = globaltimer();
+  for (int q = 0; q < P.nranks && ok; ++q) {
+    if (q == P.rank) continue;
+    const char* ust = P.uc_stage + half + (long long)q * slot;
+    uint2* dst = reinterpret_cast<uint2*>(P.out + (long long)q * P.shard_bytes);
+    for (long long i = tid; i < nunits && ok; i += stride) {
+      unsigned a, fa, b, fb;
+      for (unsigned it = 0;; ++it) {
+        asm volatile("ld.volatile.global.v4.u32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(a), "=r"(fa), "=r"(b), "=r"(fb)
+                     : "l"(ust + 16 * i)
+                     : "memory");
+        if (fa == e && fb == e) break;
+        if ((it & 1023u) == 1023u) {
+          if (*reinterpret_cast<volatile unsigned*>(&ctl->error) != 0 ||
+              (long long)(globaltimer() - t0) > P.timeout_ns) {
+            atomicCAS(&ctl->error, 0u, (unsigned)FC_DEVERR_TIMEOUT_AG);
+            ok = false;
+            break;
+          }
+        }
+      }
+      if (ok) dst[i] = make_uint2(a, b);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned prev = atomicAdd(&ctl->done, 1u);
+    if (prev == gridDim.x - 1) {
+      ctl->done = 0;
+      atomicExch(&ctl->epoch, e);
+    }
+  }
+}
+
 }  // namespace
 
 int fc_nvls_launch(const FcNvlsParams& p, int ctas, void* stream) {
   void* args[] = {(void*)&p};
   const void* fn;
+  if (p.mode == 3)
+    return (int)cudaLaunchKernel((const void*)fc_nvls_ll_ag_kernel, dim3(ctas),
+                                 dim3(FC_NVLS_THREADS), args, 0, (cudaStream_t)stream);
   switch (p.dtype) {
     case FC_BFLOAT16: fn = (const void*)fc_nvls_kernel<FC_BFLOAT16>; break;
     case FC_FLOAT16: fn = (const void*)fc_nvls_kernel<FC_FLOAT16>; break;

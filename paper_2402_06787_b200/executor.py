@@ -150,6 +150,8 @@ class _CommBase:
     def set_option(self, name: str, value: int) -> None:
         _lib.check(self._lib.fc_comm_set_option(self._comm, _lib.OPTIONS[name], int(value)),
                    self._comm, f"set_option({name})")
+        if name == "nvls_ll_max":
+            self._nvls_ll_max = int(value)
 
     def get_option(self, name: str) -> int:
         v = ctypes.c_longlong()
@@ -166,7 +168,8 @@ class _CommBase:
         buf = (ctypes.c_longlong * 8)()
         self._lib.fc_last_call_info(self._comm, buf, 8)
         return {"launches": buf[0], "nchunks": buf[1], "window": buf[2], "grid": buf[3],
-                "unit_bytes": buf[4], "proto": {0: "flags", 1: "ll128", 2: "nvls"}[buf[5]]}
+                "unit_bytes": buf[4],
+                "proto": {0: "flags", 1: "ll128", 2: "nvls", 3: "nvls_ll"}[buf[5]]}
 
     # -- tracing ------------------------------------------------------------
     TRACE_DTYPE = np.dtype([("t_start", "<u8"), ("t_end", "<u8"), ("t_wait", "<u4"),
@@ -316,7 +319,10 @@ class ForestCollComm(_CommBase):
         _lib.check(self._lib.fc_nvls_bind(self._comm, ctypes.byref(base)), self._comm, "nvls_bind")
         dist.barrier(group=self._group)
         self._nvls_base = base.value
-        self._nvls_bytes = nbytes
+        # the top 2 x nvls_ll_half bytes hold the LL multicast staging
+        self._nvls_ll_half = self.get_option("nvls_ll_half")
+        self._nvls_ll_max = self.get_option("nvls_ll_max")
+        self._nvls_bytes = nbytes - 2 * self._nvls_ll_half
 
     @property
     def nvls_enabled(self) -> bool:
@@ -342,6 +348,14 @@ class ForestCollComm(_CommBase):
                                            "data": (self._nvls_base + off, False), "version": 3}
         t = torch.as_tensor(holder, device=f"cuda:{self.device}")
         return t.view(dtype)
+
+    def _nvls_ll(self, out: torch.Tensor, inp: torch.Tensor) -> bool:
+        """Small allgather the NVLS engine runs as LL over multicast (any buffers)."""
+        nb = out.numel() * out.element_size()
+        sb = inp.numel() * inp.element_size()
+        return (self.nvls_enabled and nb <= self._nvls_ll_max and sb % 8 == 0
+                and out.data_ptr() % 8 == 0 and inp.data_ptr() % 8 == 0
+                and 2 * nb <= self._nvls_ll_half)
 
     def _in_pool(self, t) -> bool:
         if not self.nvls_enabled:
@@ -431,7 +445,7 @@ class ForestCollComm(_CommBase):
         if out.dtype != inp.dtype or out.numel() != inp.numel() * self.nranks:
             raise InvalidArgument("output must hold world_size x input elements of the same dtype")
         count, code = _dtype_args(inp, inp.numel())
-        if self._in_pool(out) and self._switch_capable("multicast"):
+        if (self._in_pool(out) or self._nvls_ll(out, inp)) and self._switch_capable("multicast"):
             self.schedule(ALLGATHER)
             _lib.check(self._lib.fc_nvls_allgather(self._comm, inp.data_ptr(), out.data_ptr(),
                                                    count, code, self._stream()),

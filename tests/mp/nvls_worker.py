@@ -39,10 +39,26 @@ def main():
         out = comm.nvls_empty(n * S, torch.float32)
         comm.all_gather(out, allin[rank].to(dev))
         torch.cuda.synchronize()
-        if comm.last_call_info()["proto"] != "nvls":
+        if comm.last_call_info()["proto"] not in ("nvls", "nvls_ll"):
             fails.append("allgather did not use NVLS")
         if not torch.equal(out.cpu().view(torch.int32), torch.cat(allin).view(torch.int32)):
             fails.append(f"allgather S={S}")
+    # small allgathers: LL over multicast into ordinary (non-pool) buffers, queued
+    # back to back without a host sync (staging halves alternate by epoch)
+    pend = []
+    for it in range(12):
+        S = [2, 64, 1000, 4096, 65536][it % 5]
+        allin = [torch.randint(0, 2**31 - 1, (S,), generator=g, dtype=torch.int32).view(torch.float32)
+                 for _ in range(n)]
+        out = torch.full((n * S,), -1.0, device=dev)
+        comm.all_gather(out, allin[rank].to(dev))
+        if comm.last_call_info()["proto"] != "nvls_ll":
+            fails.append(f"small allgather S={S} did not use the LL multicast protocol")
+        pend.append((S, out, torch.cat(allin)))
+    torch.cuda.synchronize()
+    for S, out, want in pend:
+        if not torch.equal(out.cpu().view(torch.int32), want.view(torch.int32)):
+            fails.append(f"LL multicast allgather S={S}")
     # reduce-scatter / allreduce
     for dtype, tol in ((torch.int32, 0), (torch.float32, 1e-5), (torch.bfloat16, 2e-2)):
         for S in (64, 1 << 18):
