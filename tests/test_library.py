@@ -82,3 +82,24 @@ def test_product_package_never_imports_the_oracle():
                 with open(os.path.join(root, f)) as fh:
                     src = fh.read()
                 assert not re.search(r"^\s*(from|import)\s+oracle", src, re.M), f
+
+
+def test_python_option_and_op_codes_match_the_header():
+    """Option numbers, reduction-op codes and dtype codes in the ctypes binding
+    and the executor are the ones include/forestcoll.h defines."""
+    from paper_2402_06787_b200 import _lib
+    from paper_2402_06787_b200.executor import DTYPE_CODE, OPS
+
+    with open(HEADER) as f:
+        text = f.read()
+    defs = {k: int(v) for k, v in re.findall(r"^#define (FC_\w+) (\d+)", text, re.M)}
+    opts = {k[len("FC_OPT_"):].lower(): v for k, v in defs.items() if k.startswith("FC_OPT_")}
+    assert opts == _lib.OPTIONS
+    assert OPS == {"sum": defs["FC_SUM"], "avg": defs["FC_AVG"]}
+    names = {"int8": "FC_INT8", "uint8": "FC_UINT8", "int32": "FC_INT32", "int64": "FC_INT64",
+             "float16": "FC_FLOAT16", "float32": "FC_FLOAT32", "float64": "FC_FLOAT64",
+             "bfloat16": "FC_BFLOAT16"}
+    for dt, code in DTYPE_CODE.items():
+        name = str(dt).split(".")[-1]
+        if name in names:
+            assert code == defs[names[name]], name
