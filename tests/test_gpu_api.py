@@ -192,3 +192,23 @@ def test_cuda_graph_capture_and_replay(dev, proto):
             got = ar_out[r].view(torch.int16).cpu().numpy().view(np.uint16)
             assert np.array_equal(got, ref[r]), f"replay {rep} AR rank {r}"
     comm.close()
+
+
+def test_cli_run_subcommand(dev, tmp_path):
+    """`python -m paper_2402_06787_b200 run` times a forest on virtual ranks."""
+    import json
+    import subprocess
+    import sys
+
+    from conftest import REPO
+    from paper_2402_06787_b200.topology import nvswitch_doc
+
+    topo = tmp_path / "nvs4.json"
+    topo.write_text(json.dumps(nvswitch_doc(4)))
+    for coll in ("allgather", "reduce_scatter", "allreduce"):
+        r = subprocess.run([sys.executable, "-m", "paper_2402_06787_b200", "run", "-t", str(topo),
+                            "--collective", coll, "--mib", "4", "--steps", "3"],
+                           cwd=REPO, capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0, r.stderr[-2000:]
+        line = json.loads(r.stdout.strip().splitlines()[-1])
+        assert line["collective"] == coll and line["ranks"] == 4 and line["ms"] > 0
