@@ -114,6 +114,8 @@ extern "C" {
 #define FC_OPT_CHUNK_TAIL 16   /* chunk flags: last k chunks of a slice halve in size (default 4) */
 #define FC_OPT_NVLS_LL_MAX 17  /* NVLS allgather: LL multicast when output bytes <= this (default max(2 MiB, N x 512 KiB)) */
 #define FC_OPT_NVLS_LL_HALF 18 /* read-only: bytes per LL staging half, reserved x2 at the pool top */
+#define FC_OPT_NVLS_LL_RED_MAX 19 /* NVLS allreduce: LL multicast + local tree evaluation up to
+                                     this many bytes (default N x 64 KiB; reduce-scatter: 1/N) */
 
 typedef struct fc_comm fc_comm_t;
 

@@ -53,6 +53,8 @@ struct Plan {
   long long active_total = 0;
   int* d_tasks[FC_MAXR] = {};
   int nact[FC_MAXR] = {}, nwait[FC_MAXR] = {}, lag_max[FC_MAXR] = {};
+  int* d_os = nullptr;  // RS/AR: one-shot forest program (FC_OS_TREE_WORDS per tree)
+  int os_ntrees = 0;
 };
 
 typedef CUresult (*PFN_getRange)(CUdeviceptr*, size_t*, CUdeviceptr);
@@ -94,6 +96,9 @@ struct fc_comm {
   long long nvls_ll_max = -1;         // NVLS allgather: LL multicast up to this output size
                                       // (-1: max(2 MiB, N x 512 KiB), measured crossover)
   long long nvls_ll_half = 0;         // LL staging half (2 halves reserved at the pool top)
+  long long nvls_ll_red_max = -1;     // NVLS allreduce via LL multicast up to this many bytes
+                                      // (-1: N x 64 KiB; reduce-scatter: 1/N of it)
+  int sm_count = 148;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   cudaEvent_t ev_last = nullptr;     // cross-stream ordering of this comm's collectives
   cudaStream_t last_stream = nullptr;
@@ -449,6 +454,10 @@ int free_plan(fc_comm* c, Plan& p) {
       cudaFree(p.d_tasks[i]);
       p.d_tasks[i] = nullptr;
     }
+  if (p.d_os) {
+    cudaFree(p.d_os);
+    p.d_os = nullptr;
+  }
   p.loaded = false;
   (void)c;
   return FC_SUCCESS;
@@ -471,6 +480,7 @@ int default_ctas(fc_comm* c) {
     per_sm = std::min(per_sm, v);
   }
   FC_CUDA(c, cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));
+  c->sm_count = sms;
   const int cap = per_sm * sms / c->nlocal;
   if (cap < 1) return fail(c, FC_ERR_UNSUPPORTED, "device cannot co-schedule %d ranks", c->nlocal);
   c->ctas_per_rank = std::min(c->virt ? std::max(1, 128 / c->nlocal) : 128, cap);
@@ -588,7 +598,20 @@ int run_nvls(fc_comm* c, int mode, const void* send, void* buf, void* out, size_
   if (mode == 0 && total <= ll_max && shard % 8 == 0 && (uintptr_t)send % 8 == 0 &&
       (uintptr_t)buf % 8 == 0 && 2LL * shard * N <= c->nvls_ll_half)
     mode = 3;  // LL over multicast: any device buffers
-  if (mode != 3) {
+  // small reductions: LL multicast of the whole input + local tree evaluation
+  // (needs the forest program of the loaded plan)
+  // Every rank moves its whole input (N x a reduce-scatter's need), and the
+  // local tree evaluation is compute: it pays off only for small buffers
+  // (measured at N=4: allreduce up to 256 KiB, 1.6x the tree engine).
+  const long long red_max =
+      c->nvls_ll_red_max >= 0 ? c->nvls_ll_red_max : (long long)N * (64LL << 10);
+  const Plan& rp = c->plans[mode == 1 ? FC_REDUCE_SCATTER : FC_ALLREDUCE];
+  const long long red_lim = mode == 1 ? red_max / N : red_max;
+  if ((mode == 1 || mode == 2) && rp.loaded && rp.d_os && total <= red_lim && total % 8 == 0 &&
+      shard % 8 == 0 && (uintptr_t)buf % 8 == 0 && (out == nullptr || (uintptr_t)out % 8 == 0) &&
+      2LL * total * N <= c->nvls_ll_half)
+    mode = mode == 1 ? 4 : 5;
+  if (mode < 3) {
     if (b < lo || b + (size_t)total > lo + usable)
       return fail(c, FC_ERR_NOT_REGISTERED, "buffer %p is not inside the NVLS pool", buf);
     if ((b - lo) % 16 || shard % 16 || total % 16)
@@ -608,11 +631,21 @@ int run_nvls(fc_comm* c, int mode, const void* send, void* buf, void* out, size_
   P.mc = c->nvls_mc_va + (b - lo);
   P.send = (const char*)send;
   P.out = (char*)out;
-  if (mode == 3) {
-    P.out = (char*)buf;
+  if (mode >= 3) {
     P.mc_stage = c->nvls_mc_va + usable;
     P.uc_stage = c->nvls_uc_va + usable;
     P.ll_half = c->nvls_ll_half;
+  }
+  if (mode == 3) P.out = (char*)buf;
+  if (mode >= 4) {  // reduce-scatter: send = buf (N shards) -> out; allreduce: buf in place
+    P.send = (const char*)buf;
+    P.out = mode == 4 ? (char*)out : (char*)buf;
+    P.os_trees = rp.d_os;
+    P.os_ntrees = rp.os_ntrees;
+    P.k = rp.k;
+    P.buf_bytes = total;
+    P.count = total / es;
+    P.shard_elems = shard / es;
   }
   P.shard_bytes = shard;
   P.total_bytes = total;
@@ -621,14 +654,15 @@ int run_nvls(fc_comm* c, int mode, const void* send, void* buf, void* out, size_
     const int st = order_begin(c, (cudaStream_t)stream);
     if (st) return st;
   }
-  const int e = fc_nvls_launch(P, c->nvls_ctas, stream);
+  // LL modes poll and (for reductions) evaluate trees: one CTA per SM
+  const int e = fc_nvls_launch(P, mode >= 3 ? c->sm_count : c->nvls_ctas, stream);
   if (e) return fail(c, FC_ERR_CUDA, "NVLS launch failed: %s", cudaGetErrorString((cudaError_t)e));
   {
     const int st = order_end(c, (cudaStream_t)stream);
     if (st) return st;
   }
   c->info[0] = 1;
-  c->info[5] = mode == 3 ? 3 : 2;  // engine: nvls (3: LL multicast)
+  c->info[5] = mode >= 3 ? 3 : 2;  // engine: nvls (3: LL multicast)
   return FC_SUCCESS;
 }
 
@@ -844,6 +878,10 @@ int fc_comm_set_option(fc_comm_t* c, int option, long long v) {
       return FC_SUCCESS;
     case FC_OPT_NVLS_LL_HALF:
       return fail(c, FC_ERR_INVALID_ARG, "nvls_ll_half is read-only");
+    case FC_OPT_NVLS_LL_RED_MAX:
+      if (v < 0) return fail(c, FC_ERR_INVALID_ARG, "nvls_ll_red_max < 0");
+      c->nvls_ll_red_max = v;
+      return FC_SUCCESS;
     case FC_OPT_NVLS_CTAS:
       if (v < 1 || v > 1024) return fail(c, FC_ERR_INVALID_ARG, "nvls_ctas out of range");
       c->nvls_ctas = (int)v;
@@ -885,6 +923,9 @@ int fc_comm_get_option(fc_comm_t* c, int option, long long* v) {
                                : std::max<long long>(2LL << 20, c->nranks * (512LL << 10));
       return FC_SUCCESS;
     case FC_OPT_NVLS_LL_HALF: *v = c->nvls_ll_half; return FC_SUCCESS;
+    case FC_OPT_NVLS_LL_RED_MAX:
+      *v = c->nvls_ll_red_max >= 0 ? c->nvls_ll_red_max : (long long)c->nranks * (64LL << 10);
+      return FC_SUCCESS;
     case FC_OPT_LL_WORKER_WARPS: *v = c->ll_worker_warps; return FC_SUCCESS;
     default: return fail(c, FC_ERR_INVALID_ARG, "unknown option %d", option);
   }
@@ -1101,6 +1142,61 @@ int fc_plan_load(fc_comm_t* c, int coll, const int32_t* t, size_t nwords) {
       free_plan(c, p);
       return fail(c, FC_ERR_CUDA, "plan upload failed: %s", cudaGetErrorString(e));
     }
+  }
+  if (coll != FC_ALLGATHER) {
+    // one-shot program for the NVLS engine: per tree, the in-tree children of
+    // every rank (its RS row's children, ascending) and a post-order
+    std::vector<int32_t> os((size_t)ntrees * FC_OS_TREE_WORDS, 0);
+    std::vector<int> seen(ntrees, 0);
+    for (int r = 0; r < N; ++r) {
+      const int32_t* D = t + FC_HEADER_WORDS + (size_t)r * FC_RANKDESC_WORDS;
+      for (int j = 0; j < D[RD_NACTIVE] + D[RD_NWAIT]; ++j) {
+        const int32_t* T = t + task0 + (size_t)(D[RD_FIRST] + j) * FC_TASK_WORDS;
+        const int kind = T[TW_KIND];
+        if (kind != FC_K_RS_FWD && kind != FC_K_RS_ROOT && kind != FC_K_AR_ROOT) continue;
+        int32_t* o = os.data() + (size_t)T[TW_TREE] * FC_OS_TREE_WORDS;
+        o[OS_ROOT] = T[TW_ROOT];
+        o[OS_MLO] = T[TW_MLO];
+        o[OS_MHI] = T[TW_MHI];
+        o[OS_NCH + r] = T[TW_N_RS_CHILD];
+        for (int q = 0; q < T[TW_N_RS_CHILD]; ++q) {
+          const int ch = T[TW_RS_CHILD + q];
+          if (ch < 0 || ch >= N) return free_plan(c, p), fail(c, FC_ERR_PLAN, "task row: bad reduce child");
+          o[OS_CH + r * FC_MAXR + q] = ch;
+        }
+        ++seen[T[TW_TREE]];
+      }
+    }
+    for (int tr = 0; tr < ntrees; ++tr) {
+      if (seen[tr] != N) return free_plan(c, p), fail(c, FC_ERR_PLAN, "tree %d: %d of %d reduce rows", tr, seen[tr], N);
+      int32_t* o = os.data() + (size_t)tr * FC_OS_TREE_WORDS;
+      // iterative post-order from the root
+      int stack[FC_MAXR], idx[FC_MAXR], sp = 0, np = 0;
+      stack[sp] = o[OS_ROOT];
+      idx[sp++] = 0;
+      while (sp > 0) {
+        const int v = stack[sp - 1];
+        if (idx[sp - 1] < o[OS_NCH + v]) {
+          const int ch = o[OS_CH + v * FC_MAXR + idx[sp - 1]++];
+          if (sp >= FC_MAXR) return free_plan(c, p), fail(c, FC_ERR_PLAN, "tree %d is not a tree", tr);
+          stack[sp] = ch;
+          idx[sp++] = 0;
+        } else {
+          if (np >= N) return free_plan(c, p), fail(c, FC_ERR_PLAN, "tree %d is not a tree", tr);
+          o[OS_POST + np++] = v;
+          --sp;
+        }
+      }
+      if (np != N) return free_plan(c, p), fail(c, FC_ERR_PLAN, "tree %d does not span the ranks", tr);
+      o[OS_NPOST] = np;
+    }
+    cudaError_t e = cudaMalloc((void**)&p.d_os, os.size() * 4);
+    if (e == cudaSuccess) e = cudaMemcpy(p.d_os, os.data(), os.size() * 4, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+      free_plan(c, p);
+      return fail(c, FC_ERR_CUDA, "plan upload failed: %s", cudaGetErrorString(e));
+    }
+    p.os_ntrees = ntrees;
   }
   free_plan(c, c->plans[coll]);
   p.loaded = true;

@@ -1,0 +1,76 @@
+#pragma once
+// Element arithmetic shared by the forest kernels (fc_device.cuh) and the
+// NVLS engine (fc_nvls.cu): accumulation type A, buffer element E, one
+// round-to-nearest-even per hop (the arithmetic contract).
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include "fc_internal.h"
+
+namespace {
+
+// ---------------------------------------------------------------------------
+// Element arithmetic.  Accumulation type A; buffer element E.
+// ---------------------------------------------------------------------------
+template <int DT>
+struct Red;
+
+template <>
+struct Red<FC_FLOAT32> {
+  using E = unsigned;
+  using A = float;
+  __device__ static A to(E x) { return __uint_as_float(x); }
+  __device__ static E from(A a) { return __float_as_uint(a); }
+  __device__ static A add(A a, A b) { return __fadd_rn(a, b); }
+  __device__ static A mul(A a, float s) { return __fmul_rn(a, s); }
+};
+
+// bf16: fp32 accumulate, one round-to-nearest-even per hop with the hardware
+// converter (cvt.rn.bf16x2.f32: denormals kept, NaN -> canonical 0x7FFF, as
+// oracle/forest_oracle.py::f32_to_bf16).
+template <>
+struct Red<FC_BFLOAT16> {
+  using E = unsigned short;
+  using A = float;
+  __device__ static A to(E x) { return __uint_as_float(((unsigned)x) << 16); }
+  __device__ static E from(A a) {
+    unsigned short r;
+    asm("cvt.rn.bf16.f32 %0, %1;" : "=h"(r) : "f"(a));
+    return r;
+  }
+  // two elements at once: lo -> bits 0..15, hi -> bits 16..31
+  __device__ static unsigned from2(A lo, A hi) {
+    unsigned r;
+    asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+    return r;
+  }
+  __device__ static A add(A a, A b) { return __fadd_rn(a, b); }
+  __device__ static A mul(A a, float s) { return __fmul_rn(a, s); }
+};
+
+template <>
+struct Red<FC_FLOAT16> {
+  using E = unsigned short;
+  using A = float;
+  __device__ static A to(E x) { return __half2float(__ushort_as_half(x)); }
+  __device__ static E from(A a) { return __half_as_ushort(__float2half_rn(a)); }
+  __device__ static unsigned from2(A lo, A hi) {
+    unsigned r;
+    asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+    return r;
+  }
+  __device__ static A add(A a, A b) { return __fadd_rn(a, b); }
+  __device__ static A mul(A a, float s) { return __fmul_rn(a, s); }
+};
+
+template <>
+struct Red<FC_INT32> {  // also uint32: wrapping two's-complement add
+  using E = unsigned;
+  using A = unsigned;
+  __device__ static A to(E x) { return x; }
+  __device__ static E from(A a) { return a; }
+  __device__ static A add(A a, A b) { return a + b; }
+  __device__ static A mul(A a, float) { return a; }  // AVG is rejected for integers
+};
+
+}  // namespace

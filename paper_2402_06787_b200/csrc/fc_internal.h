@@ -165,7 +165,21 @@ struct FcNvlsParams {
   char* mc_stage;                 // multicast VA of the staging region
   const char* uc_stage;           // this GPU's view of the same region
   long long ll_half;              // bytes per half
+  // modes 4 (reduce-scatter) / 5 (allreduce), LL over multicast + one-shot
+  const int* os_trees;            // [os_ntrees][FC_OS_TREE_WORDS]
+  int os_ntrees, k;
+  long long buf_bytes;            // bytes of each rank's input buffer
+  long long count;                // AR: elements of the buffer
+  long long shard_elems;          // elements per root shard
 };
+
+// One tree of a reduce-scatter / allreduce forest for the NVLS engine's
+// one-shot LL reduction: every rank holds every rank's input after one
+// multicast hop and evaluates the in-tree locally in the executor's order
+// (post-order; own value + children ascending; one rounding per node).
+#define FC_OS_TREE_WORDS (4 + FC_MAXR + FC_MAXR + FC_MAXR * FC_MAXR)
+enum { OS_ROOT = 0, OS_MLO = 1, OS_MHI = 2, OS_NPOST = 3, OS_POST = 4,
+       OS_NCH = 4 + FC_MAXR, OS_CH = 4 + 2 * FC_MAXR };
 
 // Kernel entry (fc_kernel.cu).  Returns a cudaError_t value.
 int fc_launch(const FcParams& p, int reduce_dtype, int cooperative,

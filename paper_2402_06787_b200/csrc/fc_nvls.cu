@@ -22,6 +22,7 @@
 #include <climits>
 #include <cstdint>
 
+#include "fc_arith.cuh"
 #include "fc_internal.h"
 
 #define FC_NVLS_THREADS 512
@@ -190,6 +191,40 @@ __global__ void __launch_bounds__(FC_NVLS_THREADS) fc_nvls_kernel(const __grid_c
   }
 }
 
+// Load unit `off` of every rank's staging slot at once (independent loads),
+// repeating until every flag reads e.  x[q] gets rank q's 8 payload bytes;
+// the slot of rank `skip` is not read.  Returns false on timeout / error.
+__device__ __forceinline__ bool ll_gather_unit(const char* base, long long slot, long long off,
+                                               int n, int skip, unsigned e, uint2* x, FcCtl* ctl,
+                                               unsigned long long t0, long long timeout_ns) {
+  unsigned pending = 0;
+  for (int q = 0; q < n; ++q)
+    if (q != skip) pending |= 1u << q;
+  for (unsigned it = 0; pending; ++it) {
+    unsigned a[FC_MAXR], fa[FC_MAXR], b[FC_MAXR], fb[FC_MAXR];
+#pragma unroll
+    for (int q = 0; q < FC_MAXR; ++q)
+      if ((pending >> q) & 1u)
+        asm volatile("ld.volatile.global.v4.u32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(a[q]), "=r"(fa[q]), "=r"(b[q]), "=r"(fb[q])
+                     : "l"(base + q * slot + off)
+                     : "memory");
+#pragma unroll
+    for (int q = 0; q < FC_MAXR; ++q)
+      if (((pending >> q) & 1u) && fa[q] == e && fb[q] == e) {
+        x[q] = make_uint2(a[q], b[q]);
+        pending &= ~(1u << q);
+      }
+    if (pending && (it & 255u) == 255u &&
+        (*reinterpret_cast<volatile unsigned*>(&ctl->error) != 0 ||
+         (long long)(globaltimer() - t0) > timeout_ns)) {
+      atomicCAS(&ctl->error, 0u, (unsigned)FC_DEVERR_TIMEOUT_AG);
+      return false;
+    }
+  }
+  return true;
+}
+
 // Allgather of the multicast-pruned forest with an LL protocol: every root
 // stores its shard once into the switch as 16-byte units {d0, e, d1, e} (each
 // 8-byte half pairs data with the launch epoch, NCCL's LL idea); the switch
@@ -221,32 +256,120 @@ __global__ void __launch_bounds__(FC_NVLS_THREADS) fc_nvls_ll_ag_kernel(const __
                  : "memory");
     own[i] = v;
   }
-  // 2. every other root's shard from the local staging copy
-  bool ok = true;
+  // 2. every other root's shard from the local staging copy: one unit index
+  //    at a time, all roots' copies of it loaded together
   const unsigned long long t0 = globaltimer();
-  for (int q = 0; q < P.nranks && ok; ++q) {
-    if (q == P.rank) continue;
-    const char* ust = P.uc_stage + half + (long long)q * slot;
-    uint2* dst = reinterpret_cast<uint2*>(P.out + (long long)q * P.shard_bytes);
-    for (long long i = tid; i < nunits && ok; i += stride) {
-      unsigned a, fa, b, fb;
-      for (unsigned it = 0;; ++it) {
-        asm volatile("ld.volatile.global.v4.u32 {%0,%1,%2,%3}, [%4];"
-                     : "=r"(a), "=r"(fa), "=r"(b), "=r"(fb)
-                     : "l"(ust + 16 * i)
-                     : "memory");
-        if (fa == e && fb == e) break;
-        if ((it & 1023u) == 1023u) {
-          if (*reinterpret_cast<volatile unsigned*>(&ctl->error) != 0 ||
-              (long long)(globaltimer() - t0) > P.timeout_ns) {
-            atomicCAS(&ctl->error, 0u, (unsigned)FC_DEVERR_TIMEOUT_AG);
-            ok = false;
-            break;
-          }
+  const char* ust = P.uc_stage + half;
+  for (long long i = tid; i < nunits; i += stride) {
+    uint2 x[FC_MAXR];
+    if (!ll_gather_unit(ust, slot, 16 * i, P.nranks, P.rank, e, x, ctl, t0, P.timeout_ns)) break;
+    for (int q = 0; q < P.nranks; ++q)
+      if (q != P.rank) reinterpret_cast<uint2*>(P.out + (long long)q * P.shard_bytes)[i] = x[q];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned prev = atomicAdd(&ctl->done, 1u);
+    if (prev == gridDim.x - 1) {
+      ctl->done = 0;
+      atomicExch(&ctl->epoch, e);
+    }
+  }
+}
+
+// Reduce-scatter (mode 4) / allreduce (mode 5) for small buffers: every rank
+// multicasts its whole input once as LL units (same staging scheme as the
+// allgather above), so after one switch hop every GPU holds every rank's
+// input.  Each GPU then evaluates the forest's in-trees locally, in the
+// executor's order: post-order; a node adds its own value and its children's
+// partials in ascending rank order in the accumulation type and rounds once
+// (leaves forward their own value; AVG scales at the root).  The result is
+// bit-identical to the tree engine and the oracle.  Allreduce computes the
+// whole buffer on every GPU; reduce-scatter only the own shard.
+template <int DT>
+__global__ void __launch_bounds__(FC_NVLS_THREADS) fc_nvls_ll_red_kernel(const __grid_constant__ FcNvlsParams P) {
+  using R = Red<DT>;
+  using E = typename R::E;
+  using Acc = typename R::A;
+  constexpr int EPU = 8 / (int)sizeof(E);  // elements per 8-byte payload unit
+  __shared__ unsigned s_e;
+  FcCtl* ctl = P.ctl;
+  if (threadIdx.x == 0) s_e = *reinterpret_cast<volatile unsigned*>(&ctl->epoch) + 1;
+  __syncthreads();
+  const unsigned e = s_e;
+  const long long half = (long long)(e & 1u) * P.ll_half;
+  const long long slot = 2 * P.buf_bytes;
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  // 1. multicast the whole own input
+  const uint2* src = reinterpret_cast<const uint2*>(P.send);
+  char* mst = P.mc_stage + half + (long long)P.rank * slot;
+  const long long nin = P.buf_bytes / 8;
+  for (long long i = tid; i < nin; i += stride) {
+    const uint2 v = __ldg(src + i);
+    asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(mst + 16 * i),
+                 "f"(__uint_as_float(v.x)), "f"(__uint_as_float(e)), "f"(__uint_as_float(v.y)),
+                 "f"(__uint_as_float(e))
+                 : "memory");
+  }
+  // 2. output units: allreduce the whole buffer, reduce-scatter the own shard
+  const long long S = P.shard_elems;
+  const long long u0 = P.mode == 4 ? (long long)P.rank * S * (long long)sizeof(E) / 8 : 0;
+  const long long nout = P.mode == 4 ? S * (long long)sizeof(E) / 8 : nin;
+  const unsigned long long t0 = globaltimer();
+  for (long long u = tid; u < nout; u += stride) {
+    const long long iu = u0 + u;
+    uint2 x[FC_MAXR];
+    // every slot including our own: its arrival proves the input was read
+    if (!ll_gather_unit(P.uc_stage + half, slot, 16 * iu, P.nranks, -1, e, x, ctl, t0,
+                        P.timeout_ns))
+      break;
+    uint2 res;
+    E* re = reinterpret_cast<E*>(&res);
+    for (int m = 0; m < EPU; ++m) {
+      const long long gi = iu * EPU + m;  // element index in every rank's buffer
+      long long r, o, Sr;
+      if (P.mode == 4) {
+        r = P.rank;
+        o = gi - (long long)P.rank * S;
+        Sr = S;
+      } else {
+        r = gi / S;
+        o = gi - r * S;
+        Sr = P.count - r * S;
+        Sr = Sr < S ? Sr : S;
+      }
+      const int* T = nullptr;
+      for (int ti = 0; ti < P.os_ntrees; ++ti) {
+        const int* c = P.os_trees + (long long)ti * FC_OS_TREE_WORDS;
+        if (__ldg(c + OS_ROOT) != (int)r) continue;
+        const long long lo = Sr * __ldg(c + OS_MLO) / P.k, hi = Sr * __ldg(c + OS_MHI) / P.k;
+        if (o >= lo && o < hi) {
+          T = c;
+          break;
         }
       }
-      if (ok) dst[i] = make_uint2(a, b);
+      if (T == nullptr) {  // past the last shard (padding): nothing to reduce
+        re[m] = reinterpret_cast<const E*>(&x[P.rank])[m];
+        continue;
+      }
+      E part[FC_MAXR];
+      const int np = __ldg(T + OS_NPOST), root = __ldg(T + OS_ROOT);
+      for (int a = 0; a < np; ++a) {
+        const int v = __ldg(T + OS_POST + a);
+        const E xv = reinterpret_cast<const E*>(&x[v])[m];
+        const int nc = __ldg(T + OS_NCH + v);
+        if (nc == 0) {
+          part[v] = xv;
+          continue;
+        }
+        Acc acc = R::to(xv);
+        for (int q = 0; q < nc; ++q) acc = R::add(acc, R::to(part[__ldg(T + OS_CH + v * FC_MAXR + q)]));
+        if (P.op == FC_AVG && v == root) acc = R::mul(acc, P.scale);
+        part[v] = R::from(acc);
+      }
+      re[m] = part[root];
     }
+    reinterpret_cast<uint2*>(P.out)[u] = res;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -266,6 +389,16 @@ int fc_nvls_launch(const FcNvlsParams& p, int ctas, void* stream) {
   if (p.mode == 3)
     return (int)cudaLaunchKernel((const void*)fc_nvls_ll_ag_kernel, dim3(ctas),
                                  dim3(FC_NVLS_THREADS), args, 0, (cudaStream_t)stream);
+  if (p.mode >= 4) {
+    switch (p.dtype) {
+      case FC_BFLOAT16: fn = (const void*)fc_nvls_ll_red_kernel<FC_BFLOAT16>; break;
+      case FC_FLOAT16: fn = (const void*)fc_nvls_ll_red_kernel<FC_FLOAT16>; break;
+      case FC_INT32: fn = (const void*)fc_nvls_ll_red_kernel<FC_INT32>; break;
+      default: fn = (const void*)fc_nvls_ll_red_kernel<FC_FLOAT32>; break;
+    }
+    return (int)cudaLaunchKernel(fn, dim3(ctas), dim3(FC_NVLS_THREADS), args, 0,
+                                 (cudaStream_t)stream);
+  }
   switch (p.dtype) {
     case FC_BFLOAT16: fn = (const void*)fc_nvls_kernel<FC_BFLOAT16>; break;
     case FC_FLOAT16: fn = (const void*)fc_nvls_kernel<FC_FLOAT16>; break;

@@ -152,6 +152,8 @@ class _CommBase:
                    self._comm, f"set_option({name})")
         if name == "nvls_ll_max":
             self._nvls_ll_max = int(value)
+        if name == "nvls_ll_red_max":
+            self._nvls_ll_red_max = int(value)
 
     def get_option(self, name: str) -> int:
         v = ctypes.c_longlong()
@@ -322,6 +324,7 @@ class ForestCollComm(_CommBase):
         # the top 2 x nvls_ll_half bytes hold the LL multicast staging
         self._nvls_ll_half = self.get_option("nvls_ll_half")
         self._nvls_ll_max = self.get_option("nvls_ll_max")
+        self._nvls_ll_red_max = self.get_option("nvls_ll_red_max")
         self._nvls_bytes = nbytes - 2 * self._nvls_ll_half
 
     @property
@@ -356,6 +359,18 @@ class ForestCollComm(_CommBase):
         return (self.nvls_enabled and nb <= self._nvls_ll_max and sb % 8 == 0
                 and out.data_ptr() % 8 == 0 and inp.data_ptr() % 8 == 0
                 and 2 * nb <= self._nvls_ll_half)
+
+    def _nvls_ll_red(self, inp: torch.Tensor, out: torch.Tensor) -> bool:
+        """Small reduce-scatter / allreduce the NVLS engine runs as one LL
+        multicast of each input plus a local evaluation of the in-trees."""
+        if not self.nvls_enabled:
+            return False
+        nb = inp.numel() * inp.element_size()
+        lim = self._nvls_ll_red_max if out is inp else self._nvls_ll_red_max // self.nranks
+        return (nb <= lim and nb % 8 == 0
+                and (out.numel() * out.element_size()) % 8 == 0
+                and inp.data_ptr() % 8 == 0 and out.data_ptr() % 8 == 0
+                and 2 * nb * self.nranks <= self._nvls_ll_half)
 
     def _in_pool(self, t) -> bool:
         if not self.nvls_enabled:
@@ -467,8 +482,8 @@ class ForestCollComm(_CommBase):
             raise InvalidArgument("input must hold world_size x output elements of the same dtype")
         if inp.dtype not in REDUCIBLE:
             raise Unsupported(f"dtype {inp.dtype} cannot be reduced")
-        if self._in_pool(inp) and self._switch_capable("aggregation"):
-            self.schedule(REDUCE_SCATTER)
+        if (self._in_pool(inp) or self._nvls_ll_red(inp, out)) and self._switch_capable("aggregation"):
+            self.plan(REDUCE_SCATTER)  # the LL path evaluates the plan's in-trees
             _lib.check(self._lib.fc_nvls_reduce_scatter(
                 self._comm, inp.data_ptr(), out.data_ptr(), out.numel(), DTYPE_CODE[inp.dtype],
                 _op_code(op), self._stream()), self._comm, "nvls_reduce_scatter")
@@ -490,9 +505,9 @@ class ForestCollComm(_CommBase):
             raise InvalidArgument("output must match the buffer")
         if buf.dtype not in REDUCIBLE:
             raise Unsupported(f"dtype {buf.dtype} cannot be reduced")
-        if (out is buf and self._in_pool(buf) and self._switch_capable("multicast")
-                and self._switch_capable("aggregation")):
-            self.schedule(ALLREDUCE)
+        if (out is buf and (self._in_pool(buf) or self._nvls_ll_red(buf, buf))
+                and self._switch_capable("multicast") and self._switch_capable("aggregation")):
+            self.plan(ALLREDUCE)  # the LL path evaluates the plan's in-trees
             _lib.check(self._lib.fc_nvls_allreduce(self._comm, buf.data_ptr(), buf.numel(),
                                                    DTYPE_CODE[buf.dtype], _op_code(op),
                                                    self._stream()), self._comm, "nvls_allreduce")

@@ -12,8 +12,11 @@ import sys
 REPO = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, REPO)
 
+import numpy as np  # noqa: E402
 import torch  # noqa: E402
 import torch.distributed as dist  # noqa: E402
+
+from oracle import forest_oracle as fo  # noqa: E402
 
 from paper_2402_06787_b200 import ForestCollComm  # noqa: E402
 from paper_2402_06787_b200.topology import nvswitch_doc  # noqa: E402
@@ -59,6 +62,37 @@ def main():
     for S, out, want in pend:
         if not torch.equal(out.cpu().view(torch.int32), want.view(torch.int32)):
             fails.append(f"LL multicast allgather S={S}")
+    # small reductions: LL multicast + local in-tree evaluation, bit-exact with
+    # the oracle (the tree engine's arithmetic), ordinary buffers
+    def host(t):
+        return (t.view(torch.int16).cpu().numpy().view(np.uint16) if t.dtype == torch.bfloat16
+                else t.cpu().numpy())
+
+    red_default = comm.get_option("nvls_ll_red_max")
+    comm.set_option("nvls_ll_red_max", 8 << 20)  # route every size below through the LL path
+    for dtype, name in ((torch.float32, "float32"), (torch.bfloat16, "bfloat16"), (torch.int32, "int32")):
+        for S, op in ((16, "sum"), (1000, "sum"), (4096, "avg"), (20000, "sum")):
+            if op == "avg" and dtype == torch.int32:
+                continue
+            allin = [(torch.randint(-1000, 1000, (n * S,), generator=g).to(dtype)
+                      if dtype == torch.int32 else torch.empty(n * S).uniform_(-1, 1, generator=g).to(dtype))
+                     for _ in range(n)]
+            hs = [host(x) for x in allin]
+            out = torch.empty(S, dtype=dtype, device=dev)
+            comm.reduce_scatter(out, allin[rank].to(dev), op=op)
+            if comm.last_call_info()["proto"] != "nvls_ll":
+                fails.append(f"small reduce_scatter {name} S={S} did not use LL multicast")
+            want = fo.reduce_scatter(comm.schedule("reduce_scatter"), hs, name, op=op)[rank]
+            if not np.array_equal(host(out).view(np.uint8), want.view(np.uint8)):
+                fails.append(f"LL reduce_scatter {name} S={S} op={op} not bit-exact")
+            buf = allin[rank].to(dev)
+            comm.all_reduce(buf, op=op)
+            if comm.last_call_info()["proto"] != "nvls_ll":
+                fails.append(f"small allreduce {name} n={n * S} did not use LL multicast")
+            want = fo.allreduce(comm.schedule("allreduce"), hs, name, op=op)[rank]
+            if not np.array_equal(host(buf).view(np.uint8), want.view(np.uint8)):
+                fails.append(f"LL allreduce {name} count={n * S} op={op} not bit-exact")
+    comm.set_option("nvls_ll_red_max", red_default)
     # reduce-scatter / allreduce
     for dtype, tol in ((torch.int32, 0), (torch.float32, 1e-5), (torch.bfloat16, 2e-2)):
         for S in (64, 1 << 18):

@@ -119,6 +119,31 @@ def main():
             del inp, out
     comm.check()
 
+    # --- small reductions (bf16): tree engine vs NVLS LL multicast vs NCCL ---
+    for kib in (64, 256, 1024, 4096):
+        M = kib * KIB
+        R = M // n // 2
+        inp = torch.randn(R * n, device=dev).to(torch.bfloat16)
+        out = torch.empty(R, device=dev, dtype=torch.bfloat16)
+        ms = timed(lambda: comm.reduce_scatter(out, inp), steps(M), 3, dist)
+        emit("reduce_scatter", M, "forestcoll", ms, "bfloat16", proto=comm.last_call_info()["proto"])
+        if nv.nvls_enabled:
+            ms = timed(lambda: nv.reduce_scatter(out, inp), steps(M), 3, dist)
+            emit("reduce_scatter", M, "forestcoll_nvls", ms, "bfloat16", proto=nv.last_call_info()["proto"])
+        run_nccl("reduce_scatter", M, "bfloat16", lambda g: dist.reduce_scatter_tensor(out, inp, group=g))
+        buf = comm.empty(M // 2, dtype=torch.bfloat16)
+        buf.normal_()
+        ms = timed(lambda: comm.all_reduce(buf), steps(M), 3, dist)
+        emit("allreduce", M, "forestcoll", ms, "bfloat16", proto=comm.last_call_info()["proto"])
+        comm.deregister(buf)
+        if nv.nvls_enabled:
+            b2 = torch.randn(M // 2, device=dev).to(torch.bfloat16)
+            ms = timed(lambda: nv.all_reduce(b2), steps(M), 3, dist)
+            emit("allreduce", M, "forestcoll_nvls", ms, "bfloat16", proto=nv.last_call_info()["proto"])
+        b3 = torch.randn(M // 2, device=dev).to(torch.bfloat16)
+        run_nccl("allreduce", M, "bfloat16", lambda g: dist.all_reduce(b3, group=g))
+    comm.check()
+
     # --- allreduce bf16: DDP bucket and 1 GiB ---
     for mib in (25, 1024):
         M = mib * MIB
