@@ -256,15 +256,32 @@ __global__ void __launch_bounds__(FC_NVLS_THREADS) fc_nvls_ll_ag_kernel(const __
                  : "memory");
     own[i] = v;
   }
-  // 2. every other root's shard from the local staging copy: one unit index
-  //    at a time, all roots' copies of it loaded together
+  // 2. every other root's shard from the local staging copy, root by root
+  //    (measured ~1 us faster than gathering all roots' units together)
   const unsigned long long t0 = globaltimer();
-  const char* ust = P.uc_stage + half;
-  for (long long i = tid; i < nunits; i += stride) {
-    uint2 x[FC_MAXR];
-    if (!ll_gather_unit(ust, slot, 16 * i, P.nranks, P.rank, e, x, ctl, t0, P.timeout_ns)) break;
-    for (int q = 0; q < P.nranks; ++q)
-      if (q != P.rank) reinterpret_cast<uint2*>(P.out + (long long)q * P.shard_bytes)[i] = x[q];
+  bool ok = true;
+  for (int q = 0; q < P.nranks && ok; ++q) {
+    if (q == P.rank) continue;
+    const char* us = P.uc_stage + half + (long long)q * slot;
+    uint2* dst = reinterpret_cast<uint2*>(P.out + (long long)q * P.shard_bytes);
+    for (long long i = tid; i < nunits && ok; i += stride) {
+      unsigned a, fa, b, fb;
+      for (unsigned it = 0;; ++it) {
+        asm volatile("ld.volatile.global.v4.u32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(a), "=r"(fa), "=r"(b), "=r"(fb)
+                     : "l"(us + 16 * i)
+                     : "memory");
+        if (fa == e && fb == e) break;
+        if ((it & 1023u) == 1023u &&
+            (*reinterpret_cast<volatile unsigned*>(&ctl->error) != 0 ||
+             (long long)(globaltimer() - t0) > P.timeout_ns)) {
+          atomicCAS(&ctl->error, 0u, (unsigned)FC_DEVERR_TIMEOUT_AG);
+          ok = false;
+          break;
+        }
+      }
+      if (ok) dst[i] = make_uint2(a, b);
+    }
   }
   __syncthreads();
   if (threadIdx.x == 0) {
