@@ -577,6 +577,13 @@ def nvls_points(dist, dev, n, args):
         out.append({"collective": "allgather", "engine": c.last_call_info()["proto"],
                     "M_bytes": M, "dtype": "float32", "ms": round(ms, 4),
                     "algbw_GBps": round(gbs(M, ms), 2), "frac_of_t_star": round(t * 1e3 / ms, 4)})
+    # tiny allreduce: LL multicast of every input + local in-tree evaluation
+    M = 256 * 1024
+    small = torch.randn(M // 2, device=dev).to(torch.bfloat16)
+    ms = timed(lambda: c.all_reduce(small), steps_for(M, max(5, args.steps)), 3, dist)
+    out.append({"collective": "allreduce", "engine": c.last_call_info()["proto"], "M_bytes": M,
+                "dtype": "bfloat16", "ms": round(ms, 4), "algbw_GBps": round(gbs(M, ms), 2),
+                "frac_of_t_star": round(c.t_star("allreduce", M) * 1e3 / ms, 4)})
     for mib in (25, 1000):
         M = mib * MIB
         buf = c.nvls_empty(M // 2, torch.bfloat16)
