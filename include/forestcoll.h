@@ -116,6 +116,9 @@ extern "C" {
 #define FC_OPT_NVLS_LL_HALF 18 /* read-only: bytes per LL staging half, reserved x2 at the pool top */
 #define FC_OPT_NVLS_LL_RED_MAX 19 /* NVLS allreduce: LL multicast + local tree evaluation up to
                                      this many bytes (default N x 64 KiB; reduce-scatter: 1/N) */
+#define FC_OPT_ONESHOT_MAX 20  /* tree engine: one-shot allreduce (peer stores + local tree
+                                  evaluation) up to this many bytes (default 512 KiB,
+                                  reduce-scatter 1/N of it; 0 disables) */
 
 typedef struct fc_comm fc_comm_t;
 

@@ -96,6 +96,8 @@ struct fc_comm {
   long long nvls_ll_max = -1;         // NVLS allgather: LL multicast up to this output size
                                       // (-1: max(2 MiB, N x 512 KiB), measured crossover)
   long long nvls_ll_half = 0;         // LL staging half (2 halves reserved at the pool top)
+  long long oneshot_max = -1;         // tree engine: one-shot allreduce up to this many bytes
+                                      // (-1: 512 KiB; reduce-scatter 1/N of it; 0: off)
   long long nvls_ll_red_max = -1;     // NVLS allreduce via LL multicast up to this many bytes
                                       // (-1: N x 64 KiB; reduce-scatter: 1/N of it)
   int sm_count = 148;
@@ -234,6 +236,50 @@ int order_end(fc_comm* c, cudaStream_t s) {
   return FC_SUCCESS;
 }
 
+// One-shot reduce-scatter / allreduce for small inputs: every rank stores its
+// whole input (LL units) into every rank's LL staging through the peer
+// mappings, then evaluates the forest's in-trees locally in the executor's
+// order (fc_nvls.cu, fc_nvls_ll_red_kernel; bit-identical to the forest
+// kernel).  One hop instead of RS depth + AG depth.
+int run_oneshot(fc_comm* c, int coll, const Plan& pl, const void* send, void* out, long long S,
+                long long total, int es, int rd, int op, long long half, void* stream) {
+  FcNvlsParams P;
+  memset(&P, 0, sizeof(P));
+  P.nranks = c->nranks;
+  P.rank = c->rank;
+  P.mode = coll == FC_REDUCE_SCATTER ? 4 : 5;
+  P.dtype = rd;
+  P.op = op;
+  P.scale = 1.0f / (float)c->nranks;
+  P.ctl = (FcCtl*)c->ws[c->rank];
+  P.send = (const char*)send;
+  P.out = (char*)out;
+  for (int r = 0; r < c->nranks; ++r) P.peer_stage[r] = c->ws[r] + c->scratch_off + c->scratch_bytes;
+  P.uc_stage = P.peer_stage[c->rank];
+  P.ll_half = half;
+  P.os_trees = pl.d_os;
+  P.os_ntrees = pl.os_ntrees;
+  P.k = pl.k;
+  P.buf_bytes = total * es;
+  P.count = total;
+  P.shard_elems = S;
+  P.timeout_ns = c->timeout_ms * 1000000LL;
+  {
+    const int st = order_begin(c, (cudaStream_t)stream);
+    if (st) return st;
+  }
+  const int e = fc_nvls_launch(P, c->sm_count, stream);
+  if (e) return fail(c, FC_ERR_CUDA, "one-shot launch failed: %s", cudaGetErrorString((cudaError_t)e));
+  {
+    const int st = order_end(c, (cudaStream_t)stream);
+    if (st) return st;
+  }
+  c->info[0] = 1;
+  c->info[1] = 1;
+  c->info[5] = 4;  // one-shot
+  return FC_SUCCESS;
+}
+
 // Run one collective over this comm's local ranks.
 int run(fc_comm* c, int coll, const void* const* sends, void* const* recvs, size_t count,
         int dtype, int op, void* stream) {
@@ -271,6 +317,17 @@ int run(fc_comm* c, int coll, const void* const* sends, void* const* recvs, size
   for (int i = 0; i < c->nlocal; ++i)
     if (!sends[i] || !recvs[i]) return fail(c, FC_ERR_INVALID_ARG, "null buffer");
 
+  // small reductions: one-shot (one hop) instead of the forest's two chains
+  if (coll != FC_ALLGATHER && !c->virt && c->nlocal == 1 && pl.d_os && c->oneshot_max != 0) {
+    const long long bytes = total * es;  // per-rank input bytes (AR: buffer; RS: N shards)
+    // measured crossover vs the forest kernel at N=2 and N=4: 512 KiB
+    const long long lim = c->oneshot_max > 0 ? c->oneshot_max : (512LL << 10);
+    const long long half = (long long)(c->scratch_bytes / 2) / 4096 * 4096;
+    if (bytes <= (coll == FC_REDUCE_SCATTER ? lim / N : lim) && bytes % 8 == 0 &&
+        (S * es) % 8 == 0 && (uintptr_t)sends[0] % 8 == 0 && (uintptr_t)recvs[0] % 8 == 0 &&
+        2LL * bytes * N <= half)
+      return run_oneshot(c, coll, pl, sends[0], recvs[0], S, total, es, rd, op, half, stream);
+  }
   FcParams P;
   memset(&P, 0, sizeof(P));
   P.nranks = N;
@@ -882,6 +939,10 @@ int fc_comm_set_option(fc_comm_t* c, int option, long long v) {
       if (v < 0) return fail(c, FC_ERR_INVALID_ARG, "nvls_ll_red_max < 0");
       c->nvls_ll_red_max = v;
       return FC_SUCCESS;
+    case FC_OPT_ONESHOT_MAX:
+      if (v < 0) return fail(c, FC_ERR_INVALID_ARG, "oneshot_max < 0");
+      c->oneshot_max = v;
+      return FC_SUCCESS;
     case FC_OPT_NVLS_CTAS:
       if (v < 1 || v > 1024) return fail(c, FC_ERR_INVALID_ARG, "nvls_ctas out of range");
       c->nvls_ctas = (int)v;
@@ -925,6 +986,9 @@ int fc_comm_get_option(fc_comm_t* c, int option, long long* v) {
     case FC_OPT_NVLS_LL_HALF: *v = c->nvls_ll_half; return FC_SUCCESS;
     case FC_OPT_NVLS_LL_RED_MAX:
       *v = c->nvls_ll_red_max >= 0 ? c->nvls_ll_red_max : (long long)c->nranks * (64LL << 10);
+      return FC_SUCCESS;
+    case FC_OPT_ONESHOT_MAX:
+      *v = c->oneshot_max >= 0 ? c->oneshot_max : (512LL << 10);
       return FC_SUCCESS;
     case FC_OPT_LL_WORKER_WARPS: *v = c->ll_worker_warps; return FC_SUCCESS;
     default: return fail(c, FC_ERR_INVALID_ARG, "unknown option %d", option);

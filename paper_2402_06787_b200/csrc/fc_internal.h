@@ -171,6 +171,9 @@ struct FcNvlsParams {
   long long buf_bytes;            // bytes of each rank's input buffer
   long long count;                // AR: elements of the buffer
   long long shard_elems;          // elements per root shard
+  // one-shot without multicast (tree-engine communicators): mc_stage == null and
+  // each input unit is stored to every rank's staging through its peer mapping
+  char* peer_stage[FC_MAXR];
 };
 
 // One tree of a reduce-scatter / allreduce forest for the NVLS engine's

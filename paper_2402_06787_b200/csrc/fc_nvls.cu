@@ -317,16 +317,28 @@ __global__ void __launch_bounds__(FC_NVLS_THREADS) fc_nvls_ll_red_kernel(const _
   const long long slot = 2 * P.buf_bytes;
   const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const long long stride = (long long)gridDim.x * blockDim.x;
-  // 1. multicast the whole own input
+  // 1. the whole own input to every rank's staging: one multicast store, or
+  //    (no multicast object) one store per rank through the peer mappings
   const uint2* src = reinterpret_cast<const uint2*>(P.send);
-  char* mst = P.mc_stage + half + (long long)P.rank * slot;
   const long long nin = P.buf_bytes / 8;
-  for (long long i = tid; i < nin; i += stride) {
-    const uint2 v = __ldg(src + i);
-    asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(mst + 16 * i),
-                 "f"(__uint_as_float(v.x)), "f"(__uint_as_float(e)), "f"(__uint_as_float(v.y)),
-                 "f"(__uint_as_float(e))
-                 : "memory");
+  const long long mine = half + (long long)P.rank * slot;
+  if (P.mc_stage) {
+    char* mst = P.mc_stage + mine;
+    for (long long i = tid; i < nin; i += stride) {
+      const uint2 v = __ldg(src + i);
+      asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(mst + 16 * i),
+                   "f"(__uint_as_float(v.x)), "f"(__uint_as_float(e)), "f"(__uint_as_float(v.y)),
+                   "f"(__uint_as_float(e))
+                   : "memory");
+    }
+  } else {
+    for (long long i = tid; i < nin; i += stride) {
+      const uint2 v = __ldg(src + i);
+      for (int q = 0; q < P.nranks; ++q)
+        asm volatile("st.volatile.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(P.peer_stage[q] + mine + 16 * i),
+                     "r"(v.x), "r"(e), "r"(v.y), "r"(e)
+                     : "memory");
+    }
   }
   // 2. output units: allreduce the whole buffer, reduce-scatter the own shard
   const long long S = P.shard_elems;

@@ -171,7 +171,7 @@ class _CommBase:
         self._lib.fc_last_call_info(self._comm, buf, 8)
         return {"launches": buf[0], "nchunks": buf[1], "window": buf[2], "grid": buf[3],
                 "unit_bytes": buf[4],
-                "proto": {0: "flags", 1: "ll128", 2: "nvls", 3: "nvls_ll"}[buf[5]]}
+                "proto": {0: "flags", 1: "ll128", 2: "nvls", 3: "nvls_ll", 4: "oneshot"}[buf[5]]}
 
     # -- tracing ------------------------------------------------------------
     TRACE_DTYPE = np.dtype([("t_start", "<u8"), ("t_end", "<u8"), ("t_wait", "<u4"),

@@ -90,6 +90,27 @@ def run_all(comm, rank, n, dev):
             ref = fo.allreduce(comm.schedule("allreduce"), [host(x) for x in ins], name)[rank]
             if not np.array_equal(host(buf).view(np.uint8), ref.view(np.uint8)):
                 fails.append(f"allreduce {name} count={count}")
+    # one-shot path (small reductions: peer stores of every input + local in-tree
+    # evaluation): must be bit-identical to the forest kernel / oracle
+    for dtype, name in ((torch.float32, "float32"), (torch.bfloat16, "bfloat16"), (torch.int32, "int32")):
+        for count in (8 * n, 4096, 16 * 1024):
+            ins = [seeded(count, dtype, 1700 + r + count) for r in range(n)]
+            buf = comm.empty(count, dtype=dtype)
+            buf.copy_(ins[rank].to(dev))
+            comm.all_reduce(buf)
+            if comm.last_call_info()["proto"] != "oneshot":
+                fails.append(f"allreduce {name} count={count} did not take the one-shot path")
+            torch.cuda.synchronize()
+            ref = fo.allreduce(comm.schedule("allreduce"), [host(x) for x in ins], name)[rank]
+            if not np.array_equal(host(buf).view(np.uint8), ref.view(np.uint8)):
+                fails.append(f"one-shot allreduce {name} count={count}")
+            S = count // n
+            out = torch.zeros(S, dtype=dtype, device=dev)
+            comm.reduce_scatter(out, ins[rank].to(dev))
+            torch.cuda.synchronize()
+            ref = fo.reduce_scatter(comm.schedule("reduce_scatter"), [host(x) for x in ins], name)[rank]
+            if not np.array_equal(host(out).view(np.uint8), ref.view(np.uint8)):
+                fails.append(f"one-shot reduce_scatter {name} S={S}")
     # op avg (fp dtypes): the root scales its fp32 sum by fp32(1/N) once
     for dtype, name in ((torch.bfloat16, "bfloat16"), (torch.float32, "float32")):
         for S in (999, (1 << 19) + 8):
