@@ -332,12 +332,21 @@ __global__ void __launch_bounds__(FC_NVLS_THREADS) fc_nvls_ll_red_kernel(const _
                    : "memory");
     }
   } else {
-    for (long long i = tid; i < nin; i += stride) {
-      const uint2 v = __ldg(src + i);
-      for (int q = 0; q < P.nranks; ++q)
-        asm volatile("st.volatile.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(P.peer_stage[q] + mine + 16 * i),
-                     "r"(v.x), "r"(e), "r"(v.y), "r"(e)
-                     : "memory");
+    constexpr int U1 = 4;  // loads in flight per thread
+    for (long long i0 = tid; i0 < nin; i0 += stride * U1) {
+      uint2 v[U1];
+#pragma unroll
+      for (int k = 0; k < U1; ++k)
+        if (i0 + k * stride < nin) v[k] = __ldg(src + i0 + k * stride);
+      for (int q = 0; q < P.nranks; ++q) {
+        char* dq = P.peer_stage[q] + mine;
+#pragma unroll
+        for (int k = 0; k < U1; ++k)
+          if (i0 + k * stride < nin)
+            asm volatile("st.volatile.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(dq + 16 * (i0 + k * stride)),
+                         "r"(v[k].x), "r"(e), "r"(v[k].y), "r"(e)
+                         : "memory");
+      }
     }
   }
   // 2. output units: allreduce the whole buffer, reduce-scatter the own shard
@@ -348,12 +357,93 @@ __global__ void __launch_bounds__(FC_NVLS_THREADS) fc_nvls_ll_red_kernel(const _
   for (long long u = tid; u < nout; u += stride) {
     const long long iu = u0 + u;
     uint2 x[FC_MAXR];
-    // every slot including our own: its arrival proves the input was read
-    if (!ll_gather_unit(P.uc_stage + half, slot, 16 * iu, P.nranks, -1, e, x, ctl, t0,
-                        P.timeout_ns))
-      break;
+    // every slot including our own (its arrival proves the input was read),
+    // one rank at a time: a single poll in flight per thread keeps the
+    // staging reads from competing with the arriving stores
+    bool ok = true;
+    for (int q = 0; q < P.nranks && ok; ++q) {
+      const char* pq = P.uc_stage + half + (long long)q * slot + 16 * iu;
+      unsigned a, fa, b, fb;
+      for (unsigned it = 0;; ++it) {
+        asm volatile("ld.volatile.global.v4.u32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(a), "=r"(fa), "=r"(b), "=r"(fb)
+                     : "l"(pq)
+                     : "memory");
+        if (fa == e && fb == e) break;
+        if ((it & 1023u) == 1023u &&
+            (*reinterpret_cast<volatile unsigned*>(&ctl->error) != 0 ||
+             (long long)(globaltimer() - t0) > P.timeout_ns)) {
+          atomicCAS(&ctl->error, 0u, (unsigned)FC_DEVERR_TIMEOUT_RS);
+          ok = false;
+          break;
+        }
+      }
+      x[q] = make_uint2(a, b);
+    }
+    if (!ok) break;
     uint2 res;
     E* re = reinterpret_cast<E*>(&res);
+    // the tree of the unit's first element; if its last element is in the same
+    // slice (almost always), evaluate the tree once for all EPU lanes
+    const int* T0 = nullptr;
+    {
+      const long long g0 = iu * EPU, g1 = g0 + EPU - 1;
+      long long r0, o0, o1, Sr;
+      if (P.mode == 4) {
+        r0 = P.rank;
+        o0 = g0 - (long long)P.rank * S;
+        o1 = o0 + EPU - 1;
+        Sr = S;
+      } else {
+        r0 = g0 / S;
+        o0 = g0 - r0 * S;
+        o1 = g1 - r0 * S;
+        Sr = P.count - r0 * S;
+        Sr = Sr < S ? Sr : S;
+      }
+      for (int ti = 0; ti < P.os_ntrees && o1 < Sr; ++ti) {
+        const int* c = P.os_trees + (long long)ti * FC_OS_TREE_WORDS;
+        if (__ldg(c + OS_ROOT) != (int)r0) continue;
+        const long long lo = Sr * __ldg(c + OS_MLO) / P.k, hi = Sr * __ldg(c + OS_MHI) / P.k;
+        if (o0 >= lo && o1 < hi) {
+          T0 = c;
+          break;
+        }
+      }
+    }
+    if (T0 != nullptr) {
+      uint2 part[FC_MAXR];
+      const int np = __ldg(T0 + OS_NPOST), root = __ldg(T0 + OS_ROOT);
+      for (int a = 0; a < np; ++a) {
+        const int v = __ldg(T0 + OS_POST + a);
+        const int nc = __ldg(T0 + OS_NCH + v);
+        if (nc == 0) {
+          part[v] = x[v];
+          continue;
+        }
+        const E* xv = reinterpret_cast<const E*>(&x[v]);
+        Acc acc[EPU];
+#pragma unroll
+        for (int m = 0; m < EPU; ++m) acc[m] = R::to(xv[m]);
+        for (int q = 0; q < nc; ++q) {
+          const uint2 pc = part[__ldg(T0 + OS_CH + v * FC_MAXR + q)];
+          const E* pe = reinterpret_cast<const E*>(&pc);
+#pragma unroll
+          for (int m = 0; m < EPU; ++m) acc[m] = R::add(acc[m], R::to(pe[m]));
+        }
+        if (P.op == FC_AVG && v == root) {
+#pragma unroll
+          for (int m = 0; m < EPU; ++m) acc[m] = R::mul(acc[m], P.scale);
+        }
+        uint2 o;
+        E* oe = reinterpret_cast<E*>(&o);
+#pragma unroll
+        for (int m = 0; m < EPU; ++m) oe[m] = R::from(acc[m]);
+        part[v] = o;
+      }
+      reinterpret_cast<uint2*>(P.out)[u] = part[root];
+      continue;
+    }
     for (int m = 0; m < EPU; ++m) {
       const long long gi = iu * EPU + m;  // element index in every rank's buffer
       long long r, o, Sr;
