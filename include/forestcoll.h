@@ -111,7 +111,7 @@ extern "C" {
 #define FC_OPT_LL_WORKER_WARPS 13 /* warps per work item, LL128 (default 4 real, 1 virtual) */
 #define FC_OPT_NVLS_CTAS 14    /* CTAs of the NVLS (multicast) kernel (default 32) */
 #define FC_OPT_PDL 15          /* programmatic dependent launch (default 1) */
-#define FC_OPT_CHUNK_TAIL 16   /* chunk flags: last k chunks of a slice halve in size (default 4) */
+#define FC_OPT_CHUNK_TAIL 16   /* chunk flags: last k chunks of a slice halve in size (default 4; 0 virtual) */
 #define FC_OPT_NVLS_LL_MAX 17  /* NVLS allgather: LL multicast when output bytes <= this (default max(2 MiB, N x 512 KiB)) */
 #define FC_OPT_NVLS_LL_HALF 18 /* read-only: bytes per LL staging half, reserved x2 at the pool top */
 #define FC_OPT_NVLS_LL_RED_MAX 19 /* NVLS allreduce: LL multicast + local tree evaluation up to

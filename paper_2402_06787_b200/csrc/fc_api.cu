@@ -546,6 +546,8 @@ int default_ctas(fc_comm* c) {
   c->ll_worker_warps = c->virt ? 1 : 4;
   // virtual ranks share one HBM: LL staging doubles the traffic, so keep it for small calls
   if (c->virt) c->ll_max = 16LL << 20;
+  // all ranks share one HBM and one grid: no drain to shorten (measured -1 % with tail 4)
+  if (c->virt) c->chunk_tail = 0;
   return make_side_stream(c);
 }
 
