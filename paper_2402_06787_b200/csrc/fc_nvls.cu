@@ -191,40 +191,6 @@ __global__ void __launch_bounds__(FC_NVLS_THREADS) fc_nvls_kernel(const __grid_c
   }
 }
 
-// Load unit `off` of every rank's staging slot at once (independent loads),
-// repeating until every flag reads e.  x[q] gets rank q's 8 payload bytes;
-// the slot of rank `skip` is not read.  Returns false on timeout / error.
-__device__ __forceinline__ bool ll_gather_unit(const char* base, long long slot, long long off,
-                                               int n, int skip, unsigned e, uint2* x, FcCtl* ctl,
-                                               unsigned long long t0, long long timeout_ns) {
-  unsigned pending = 0;
-  for (int q = 0; q < n; ++q)
-    if (q != skip) pending |= 1u << q;
-  for (unsigned it = 0; pending; ++it) {
-    unsigned a[FC_MAXR], fa[FC_MAXR], b[FC_MAXR], fb[FC_MAXR];
-#pragma unroll
-    for (int q = 0; q < FC_MAXR; ++q)
-      if ((pending >> q) & 1u)
-        asm volatile("ld.volatile.global.v4.u32 {%0,%1,%2,%3}, [%4];"
-                     : "=r"(a[q]), "=r"(fa[q]), "=r"(b[q]), "=r"(fb[q])
-                     : "l"(base + q * slot + off)
-                     : "memory");
-#pragma unroll
-    for (int q = 0; q < FC_MAXR; ++q)
-      if (((pending >> q) & 1u) && fa[q] == e && fb[q] == e) {
-        x[q] = make_uint2(a[q], b[q]);
-        pending &= ~(1u << q);
-      }
-    if (pending && (it & 255u) == 255u &&
-        (*reinterpret_cast<volatile unsigned*>(&ctl->error) != 0 ||
-         (long long)(globaltimer() - t0) > timeout_ns)) {
-      atomicCAS(&ctl->error, 0u, (unsigned)FC_DEVERR_TIMEOUT_AG);
-      return false;
-    }
-  }
-  return true;
-}
-
 // Allgather of the multicast-pruned forest with an LL protocol: every root
 // stores its shard once into the switch as 16-byte units {d0, e, d1, e} (each
 // 8-byte half pairs data with the launch epoch, NCCL's LL idea); the switch
