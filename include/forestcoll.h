@@ -117,7 +117,7 @@ extern "C" {
 #define FC_OPT_NVLS_LL_RED_MAX 19 /* NVLS allreduce: LL multicast + local tree evaluation up to
                                      this many bytes (default N x 64 KiB; reduce-scatter: 1/N) */
 #define FC_OPT_ONESHOT_MAX 20  /* tree engine: one-shot allreduce (peer stores + local tree
-                                  evaluation) up to this many bytes (default 1 MiB,
+                                  evaluation) up to this many bytes (default 2 MiB,
                                   reduce-scatter 2/N of it; 0 disables) */
 
 typedef struct fc_comm fc_comm_t;

@@ -97,7 +97,7 @@ struct fc_comm {
                                       // (-1: max(2 MiB, N x 512 KiB), measured crossover)
   long long nvls_ll_half = 0;         // LL staging half (2 halves reserved at the pool top)
   long long oneshot_max = -1;         // tree engine: one-shot allreduce up to this many bytes
-                                      // (-1: 1 MiB; reduce-scatter 2/N of it; 0: off)
+                                      // (-1: 2 MiB; reduce-scatter 2/N of it; 0: off)
   long long nvls_ll_red_max = -1;     // NVLS allreduce via LL multicast up to this many bytes
                                       // (-1: N x 64 KiB; reduce-scatter: 1/N of it)
   int sm_count = 148;
@@ -247,7 +247,10 @@ int run_oneshot(fc_comm* c, int coll, const Plan& pl, const void* send, void* ou
   memset(&P, 0, sizeof(P));
   P.nranks = c->nranks;
   P.rank = c->rank;
-  P.mode = coll == FC_REDUCE_SCATTER ? 4 : 5;
+  // up to 256 KiB: 8-byte LL units (most parallel); above: LL128 lines (1.07x
+  // the bytes instead of 2x), measured crossover at N=4
+  const bool lines = total * es > (256LL << 10);
+  P.mode = coll == FC_REDUCE_SCATTER ? (lines ? 6 : 4) : (lines ? 7 : 5);
   P.dtype = rd;
   P.op = op;
   P.scale = 1.0f / (float)c->nranks;
@@ -320,9 +323,9 @@ int run(fc_comm* c, int coll, const void* const* sends, void* const* recvs, size
   // small reductions: one-shot (one hop) instead of the forest's two chains
   if (coll != FC_ALLGATHER && !c->virt && c->nlocal == 1 && pl.d_os && c->oneshot_max != 0) {
     const long long bytes = total * es;  // per-rank input bytes (AR: buffer; RS: N shards)
-    // measured crossover vs the forest kernel at N=4: allreduce 1 MiB,
-    // reduce-scatter about 2 MiB / N of input
-    const long long lim = c->oneshot_max > 0 ? c->oneshot_max : (1LL << 20);
+    // measured crossover vs the forest kernel at N=4: allreduce 2 MiB,
+    // reduce-scatter 2 x that / N of input
+    const long long lim = c->oneshot_max > 0 ? c->oneshot_max : (2LL << 20);
     const long long half = (long long)(c->scratch_bytes / 2) / 4096 * 4096;
     if (bytes <= (coll == FC_REDUCE_SCATTER ? 2 * lim / N : lim) && bytes % 8 == 0 &&
         (S * es) % 8 == 0 && (uintptr_t)sends[0] % 8 == 0 && (uintptr_t)recvs[0] % 8 == 0 &&
@@ -991,7 +994,7 @@ int fc_comm_get_option(fc_comm_t* c, int option, long long* v) {
       *v = c->nvls_ll_red_max >= 0 ? c->nvls_ll_red_max : (long long)c->nranks * (64LL << 10);
       return FC_SUCCESS;
     case FC_OPT_ONESHOT_MAX:
-      *v = c->oneshot_max >= 0 ? c->oneshot_max : (1LL << 20);
+      *v = c->oneshot_max >= 0 ? c->oneshot_max : (2LL << 20);
       return FC_SUCCESS;
     case FC_OPT_LL_WORKER_WARPS: *v = c->ll_worker_warps; return FC_SUCCESS;
     default: return fail(c, FC_ERR_INVALID_ARG, "unknown option %d", option);

@@ -466,6 +466,218 @@ __global__ void __launch_bounds__(FC_NVLS_THREADS) fc_nvls_ll_red_kernel(const _
   }
 }
 
+// Reduce one 8-byte payload word (EPU elements at byte offset `pb` of every
+// rank's input; xs[q] = rank q's word) over the forest's in-tree that covers
+// it, in the executor's order.  Shared by the one-shot kernels.
+template <int DT>
+__device__ unsigned long long tree_word(const FcNvlsParams& P, long long pb,
+                                        const unsigned long long* xs) {
+  using R = Red<DT>;
+  using E = typename R::E;
+  using Acc = typename R::A;
+  constexpr int EPU = 8 / (int)sizeof(E);
+  const long long S = P.shard_elems;
+  const long long g0 = pb / (long long)sizeof(E);
+  const int* T0 = nullptr;
+  {
+    long long r0, o0, Sr;
+    if (P.mode == 6) {
+      r0 = P.rank;
+      o0 = g0 - (long long)P.rank * S;
+      Sr = S;
+    } else {
+      r0 = g0 / S;
+      o0 = g0 - r0 * S;
+      Sr = P.count - r0 * S;
+      Sr = Sr < S ? Sr : S;
+    }
+    const long long o1 = o0 + EPU - 1;
+    for (int ti = 0; ti < P.os_ntrees && o1 < Sr; ++ti) {
+      const int* c = P.os_trees + (long long)ti * FC_OS_TREE_WORDS;
+      if (__ldg(c + OS_ROOT) != (int)r0) continue;
+      const long long lo = Sr * __ldg(c + OS_MLO) / P.k, hi = Sr * __ldg(c + OS_MHI) / P.k;
+      if (o0 >= lo && o1 < hi) {
+        T0 = c;
+        break;
+      }
+    }
+  }
+  unsigned long long part[FC_MAXR];
+  if (T0 != nullptr) {  // the whole word lies in one slice: evaluate all lanes at once
+    const int np = __ldg(T0 + OS_NPOST), root = __ldg(T0 + OS_ROOT);
+    for (int a = 0; a < np; ++a) {
+      const int v = __ldg(T0 + OS_POST + a);
+      const int nc = __ldg(T0 + OS_NCH + v);
+      if (nc == 0) {
+        part[v] = xs[v];
+        continue;
+      }
+      const E* xv = reinterpret_cast<const E*>(&xs[v]);
+      Acc acc[EPU];
+#pragma unroll
+      for (int m = 0; m < EPU; ++m) acc[m] = R::to(xv[m]);
+      for (int q = 0; q < nc; ++q) {
+        const unsigned long long pc = part[__ldg(T0 + OS_CH + v * FC_MAXR + q)];
+        const E* pe = reinterpret_cast<const E*>(&pc);
+#pragma unroll
+        for (int m = 0; m < EPU; ++m) acc[m] = R::add(acc[m], R::to(pe[m]));
+      }
+      if (P.op == FC_AVG && v == root) {
+#pragma unroll
+        for (int m = 0; m < EPU; ++m) acc[m] = R::mul(acc[m], P.scale);
+      }
+      unsigned long long o;
+      E* oe = reinterpret_cast<E*>(&o);
+#pragma unroll
+      for (int m = 0; m < EPU; ++m) oe[m] = R::from(acc[m]);
+      part[v] = o;
+    }
+    return part[root];
+  }
+  // a slice boundary inside the word: element by element
+  unsigned long long res = 0;
+  E* re = reinterpret_cast<E*>(&res);
+  for (int m = 0; m < EPU; ++m) {
+    const long long gi = g0 + m;
+    long long r, o, Sr;
+    if (P.mode == 6) {
+      r = P.rank;
+      o = gi - (long long)P.rank * S;
+      Sr = S;
+    } else {
+      r = gi / S;
+      o = gi - r * S;
+      Sr = P.count - r * S;
+      Sr = Sr < S ? Sr : S;
+    }
+    const int* T = nullptr;
+    for (int ti = 0; ti < P.os_ntrees; ++ti) {
+      const int* c = P.os_trees + (long long)ti * FC_OS_TREE_WORDS;
+      if (__ldg(c + OS_ROOT) != (int)r) continue;
+      const long long lo = Sr * __ldg(c + OS_MLO) / P.k, hi = Sr * __ldg(c + OS_MHI) / P.k;
+      if (o >= lo && o < hi) {
+        T = c;
+        break;
+      }
+    }
+    if (T == nullptr) {
+      re[m] = reinterpret_cast<const E*>(&xs[P.rank])[m];
+      continue;
+    }
+    E pe[FC_MAXR];
+    const int np = __ldg(T + OS_NPOST), root = __ldg(T + OS_ROOT);
+    for (int a = 0; a < np; ++a) {
+      const int v = __ldg(T + OS_POST + a);
+      const E xv = reinterpret_cast<const E*>(&xs[v])[m];
+      const int nc = __ldg(T + OS_NCH + v);
+      if (nc == 0) {
+        pe[v] = xv;
+        continue;
+      }
+      Acc acc = R::to(xv);
+      for (int q = 0; q < nc; ++q) acc = R::add(acc, R::to(pe[__ldg(T + OS_CH + v * FC_MAXR + q)]));
+      if (P.op == FC_AVG && v == root) acc = R::mul(acc, P.scale);
+      pe[v] = R::from(acc);
+    }
+    re[m] = pe[root];
+  }
+  return res;
+}
+
+// One-shot reduce-scatter (mode 6) / allreduce (mode 7) for the tree engine,
+// in LL128 lines: every rank stores its whole input as 128-byte lines (120
+// payload bytes + the epoch in the last 8) into every rank's staging through
+// the peer mappings -- 1.07x the bytes instead of the 2x of 8-byte LL units --
+// then each GPU evaluates the in-trees locally (tree_word).  A warp's 8-lane
+// group moves one line; NVLink delivers it whole, so the flag in lane 7
+// vouches for the whole line (the LL128 rule of the forest kernel).
+template <int DT>
+__global__ void __launch_bounds__(FC_NVLS_THREADS) fc_oneshot128_kernel(const __grid_constant__ FcNvlsParams P) {
+  using E = typename Red<DT>::E;
+  __shared__ unsigned s_e;
+  FcCtl* ctl = P.ctl;
+  if (threadIdx.x == 0) s_e = *reinterpret_cast<volatile unsigned*>(&ctl->epoch) + 1;
+  __syncthreads();
+  const unsigned e = s_e;
+  const unsigned long long flag = e;
+  const long long B = P.buf_bytes;
+  const long long L = (B + 119) / 120;
+  const long long slot = L * 128;
+  const long long half = (long long)(e & 1u) * P.ll_half;
+  const long long mine = half + (long long)P.rank * slot;
+  const int lane = threadIdx.x & 31, gl = lane & 7;
+  const long long gid = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 3;  // 8-lane group
+  const long long ngrp = ((long long)gridDim.x * blockDim.x) >> 3;
+  const long long p_lane = 16LL * gl;  // this lane's payload bytes within a line: [p_lane, +16)
+  // 1. every line of the own input to every rank's staging
+  for (long long l = gid; l < L; l += ngrp) {
+    const long long pb = 120 * l + p_lane;
+    unsigned long long w0 = 0, w1 = flag;
+    if (pb + 8 <= B) w0 = __ldg(reinterpret_cast<const unsigned long long*>(P.send + pb));
+    if (gl < 7) w1 = (pb + 16 <= B) ? __ldg(reinterpret_cast<const unsigned long long*>(P.send + pb + 8)) : 0ull;
+    for (int q = 0; q < P.nranks; ++q)
+      asm volatile("st.volatile.global.v2.u64 [%0], {%1, %2};" ::"l"(P.peer_stage[q] + mine + 128 * l + 16 * gl),
+                   "l"(w0), "l"(w1)
+                   : "memory");
+  }
+  // 2. the lines holding output words: all of them (allreduce) or those of the own shard
+  const long long S = P.shard_elems;
+  const long long ob = P.mode == 6 ? (long long)P.rank * S * (long long)sizeof(E) : 0;  // first output byte
+  const long long oe = P.mode == 6 ? ob + S * (long long)sizeof(E) : B;
+  const long long l0 = ob / 120, l1 = (oe + 119) / 120;
+  const unsigned long long t0 = globaltimer();
+  // warp-uniform loop: a warp's 4 groups take 4 consecutive lines per step
+  const long long wid = gid >> 2, nw = ngrp >> 2;
+  for (long long lb = l0 + 4 * wid; lb < l1; lb += 4 * nw) {
+    const long long l = lb + (lane >> 3);
+    const bool valid = l < l1;
+    unsigned long long x0[FC_MAXR], x1[FC_MAXR];
+    bool ok = true;
+    for (int q = 0; q < P.nranks && ok; ++q) {
+      const char* pq = P.uc_stage + half + (long long)q * slot + 128 * l + 16 * gl;
+      for (unsigned it = 0;; ++it) {
+        unsigned long long a = 0, b = flag;
+        if (valid)
+          asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(pq) : "memory");
+        const int mine_ok = (gl != 7 || b == flag) ? 1 : 0;
+        const int grp_ok = __shfl_sync(0xffffffffu, mine_ok, (lane & ~7) | 7);
+        if (__all_sync(0xffffffffu, grp_ok)) {
+          x0[q] = a;
+          x1[q] = b;
+          break;
+        }
+        if ((it & 1023u) == 1023u) {
+          int bad = 0;
+          if (lane == 0 && (*reinterpret_cast<volatile unsigned*>(&ctl->error) != 0 ||
+                            (long long)(globaltimer() - t0) > P.timeout_ns)) {
+            atomicCAS(&ctl->error, 0u, (unsigned)FC_DEVERR_TIMEOUT_RS);
+            bad = 1;
+          }
+          if (__shfl_sync(0xffffffffu, bad, 0)) {
+            ok = false;
+            break;
+          }
+        }
+      }
+    }
+    if (!ok) break;
+    if (!valid) continue;
+    const long long pb = 120 * l + p_lane;
+    if (pb >= ob && pb + 8 <= oe)
+      reinterpret_cast<unsigned long long*>(P.out + (pb - ob))[0] = tree_word<DT>(P, pb, x0);
+    if (gl < 7 && pb + 8 >= ob && pb + 16 <= oe)
+      reinterpret_cast<unsigned long long*>(P.out + (pb + 8 - ob))[0] = tree_word<DT>(P, pb + 8, x1);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned prev = atomicAdd(&ctl->done, 1u);
+    if (prev == gridDim.x - 1) {
+      ctl->done = 0;
+      atomicExch(&ctl->epoch, e);
+    }
+  }
+}
+
 }  // namespace
 
 int fc_nvls_launch(const FcNvlsParams& p, int ctas, void* stream) {
@@ -474,6 +686,16 @@ int fc_nvls_launch(const FcNvlsParams& p, int ctas, void* stream) {
   if (p.mode == 3)
     return (int)cudaLaunchKernel((const void*)fc_nvls_ll_ag_kernel, dim3(ctas),
                                  dim3(FC_NVLS_THREADS), args, 0, (cudaStream_t)stream);
+  if (p.mode >= 6) {
+    switch (p.dtype) {
+      case FC_BFLOAT16: fn = (const void*)fc_oneshot128_kernel<FC_BFLOAT16>; break;
+      case FC_FLOAT16: fn = (const void*)fc_oneshot128_kernel<FC_FLOAT16>; break;
+      case FC_INT32: fn = (const void*)fc_oneshot128_kernel<FC_INT32>; break;
+      default: fn = (const void*)fc_oneshot128_kernel<FC_FLOAT32>; break;
+    }
+    return (int)cudaLaunchKernel(fn, dim3(ctas), dim3(FC_NVLS_THREADS), args, 0,
+                                 (cudaStream_t)stream);
+  }
   if (p.mode >= 4) {
     switch (p.dtype) {
       case FC_BFLOAT16: fn = (const void*)fc_nvls_ll_red_kernel<FC_BFLOAT16>; break;

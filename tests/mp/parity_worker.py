@@ -93,7 +93,7 @@ def run_all(comm, rank, n, dev):
     # one-shot path (small reductions: peer stores of every input + local in-tree
     # evaluation): must be bit-identical to the forest kernel / oracle
     for dtype, name in ((torch.float32, "float32"), (torch.bfloat16, "bfloat16"), (torch.int32, "int32")):
-        for count in (8 * n, 4096, 16 * 1024):
+        for count in (8 * n, 4096, 16 * 1024, 150 * 1024 + 8 * n):  # last: LL128-line format
             ins = [seeded(count, dtype, 1700 + r + count) for r in range(n)]
             buf = comm.empty(count, dtype=dtype)
             buf.copy_(ins[rank].to(dev))
