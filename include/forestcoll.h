@@ -119,6 +119,8 @@ extern "C" {
 #define FC_OPT_ONESHOT_MAX 20  /* tree engine: one-shot allreduce (peer stores + local tree
                                   evaluation) up to this many bytes (default 2 MiB,
                                   reduce-scatter 2/N of it; 0 disables) */
+#define FC_OPT_ONESHOT_AG_MAX 21 /* tree engine: one-hop allgather (LL128 lines to every peer)
+                                    up to this output size (default 16 MiB; 0 disables) */
 
 typedef struct fc_comm fc_comm_t;
 

@@ -21,7 +21,7 @@ OPT_CTAS_PER_RANK, OPT_CHUNK_MAX, OPT_CHUNK_MIN, OPT_ITEMS_PER_WORKER, OPT_TIMEO
 OPT_LAG, OPT_COPY_MODE, OPT_DMA_ROOT_COPY, OPT_WORKER_WARPS = 6, 7, 8, 9
 OPT_PROTO, OPT_LL_MAX, OPT_LL_CHUNK_MAX, OPT_LL_WORKER_WARPS, OPT_NVLS_CTAS = 10, 11, 12, 13, 14
 OPT_PDL, OPT_CHUNK_TAIL, OPT_NVLS_LL_MAX, OPT_NVLS_LL_HALF, OPT_NVLS_LL_RED_MAX = 15, 16, 17, 18, 19
-OPT_ONESHOT_MAX = 20
+OPT_ONESHOT_MAX, OPT_ONESHOT_AG_MAX = 20, 21
 OPTIONS = {
     "ctas_per_rank": OPT_CTAS_PER_RANK,
     "chunk_max": OPT_CHUNK_MAX,
@@ -43,6 +43,7 @@ OPTIONS = {
     "nvls_ll_half": OPT_NVLS_LL_HALF,
     "nvls_ll_red_max": OPT_NVLS_LL_RED_MAX,
     "oneshot_max": OPT_ONESHOT_MAX,
+    "oneshot_ag_max": OPT_ONESHOT_AG_MAX,
 }
 
 # symbol -> (restype, argtypes)

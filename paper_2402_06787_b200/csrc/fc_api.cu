@@ -96,6 +96,8 @@ struct fc_comm {
   long long nvls_ll_max = -1;         // NVLS allgather: LL multicast up to this output size
                                       // (-1: max(2 MiB, N x 512 KiB), measured crossover)
   long long nvls_ll_half = 0;         // LL staging half (2 halves reserved at the pool top)
+  long long oneshot_ag_max = -1;      // tree engine: one-shot allgather up to this output size
+                                      // (-1: 16 MiB; 0: off)
   long long oneshot_max = -1;         // tree engine: one-shot allreduce up to this many bytes
                                       // (-1: 2 MiB; reduce-scatter 2/N of it; 0: off)
   long long nvls_ll_red_max = -1;     // NVLS allreduce via LL multicast up to this many bytes
@@ -283,6 +285,39 @@ int run_oneshot(fc_comm* c, int coll, const Plan& pl, const void* send, void* ou
   return FC_SUCCESS;
 }
 
+// One-shot allgather (fc_nvls.cu fc_oneshot_ag128_kernel): the output is
+// local only, so no buffer registration is used.
+int run_oneshot_ag(fc_comm* c, const void* send, void* out, long long shard_bytes, long long half,
+                   void* stream) {
+  FcNvlsParams P;
+  memset(&P, 0, sizeof(P));
+  P.nranks = c->nranks;
+  P.rank = c->rank;
+  P.mode = 8;
+  P.ctl = (FcCtl*)c->ws[c->rank];
+  P.send = (const char*)send;
+  P.out = (char*)out;
+  for (int r = 0; r < c->nranks; ++r) P.peer_stage[r] = c->ws[r] + c->scratch_off + c->scratch_bytes;
+  P.uc_stage = P.peer_stage[c->rank];
+  P.ll_half = half;
+  P.shard_bytes = shard_bytes;
+  P.timeout_ns = c->timeout_ms * 1000000LL;
+  {
+    const int st = order_begin(c, (cudaStream_t)stream);
+    if (st) return st;
+  }
+  const int e = fc_nvls_launch(P, c->sm_count, stream);
+  if (e) return fail(c, FC_ERR_CUDA, "one-shot launch failed: %s", cudaGetErrorString((cudaError_t)e));
+  {
+    const int st = order_end(c, (cudaStream_t)stream);
+    if (st) return st;
+  }
+  c->info[0] = 1;
+  c->info[1] = 1;
+  c->info[5] = 4;  // one-shot
+  return FC_SUCCESS;
+}
+
 // Run one collective over this comm's local ranks.
 int run(fc_comm* c, int coll, const void* const* sends, void* const* recvs, size_t count,
         int dtype, int op, void* stream) {
@@ -320,8 +355,22 @@ int run(fc_comm* c, int coll, const void* const* sends, void* const* recvs, size
   for (int i = 0; i < c->nlocal; ++i)
     if (!sends[i] || !recvs[i]) return fail(c, FC_ERR_INVALID_ARG, "null buffer");
 
+  // small allgathers: one hop (every root stores its shard into every peer's
+  // LL128 staging) instead of the forest's depth; same per-GPU egress
+  // (only under automatic protocol selection: a forced protocol is honoured)
+  if (coll == FC_ALLGATHER && !c->virt && c->nlocal == 1 && c->proto < 0 && c->oneshot_ag_max != 0) {
+    const long long bytes = total * es;  // output bytes
+    // measured crossover vs the forest's LL128 at N=4: between 16 and 32 MiB
+    const long long lim = c->oneshot_ag_max > 0 ? c->oneshot_ag_max : (16LL << 20);
+    const long long half = (long long)(c->scratch_bytes / 2) / 4096 * 4096;
+    const long long lines = (S * es + 119) / 120;
+    if (bytes <= lim && (S * es) % 8 == 0 && (uintptr_t)sends[0] % 8 == 0 &&
+        (uintptr_t)recvs[0] % 8 == 0 && (long long)N * lines * 128 <= half)
+      return run_oneshot_ag(c, sends[0], recvs[0], S * es, half, stream);
+  }
   // small reductions: one-shot (one hop) instead of the forest's two chains
-  if (coll != FC_ALLGATHER && !c->virt && c->nlocal == 1 && pl.d_os && c->oneshot_max != 0) {
+  if (coll != FC_ALLGATHER && !c->virt && c->nlocal == 1 && c->proto < 0 && pl.d_os &&
+      c->oneshot_max != 0) {
     const long long bytes = total * es;  // per-rank input bytes (AR: buffer; RS: N shards)
     // measured crossover vs the forest kernel at N=4: allreduce 2 MiB,
     // reduce-scatter 2 x that / N of input
@@ -949,6 +998,10 @@ int fc_comm_set_option(fc_comm_t* c, int option, long long v) {
       if (v < 0) return fail(c, FC_ERR_INVALID_ARG, "oneshot_max < 0");
       c->oneshot_max = v;
       return FC_SUCCESS;
+    case FC_OPT_ONESHOT_AG_MAX:
+      if (v < 0) return fail(c, FC_ERR_INVALID_ARG, "oneshot_ag_max < 0");
+      c->oneshot_ag_max = v;
+      return FC_SUCCESS;
     case FC_OPT_NVLS_CTAS:
       if (v < 1 || v > 1024) return fail(c, FC_ERR_INVALID_ARG, "nvls_ctas out of range");
       c->nvls_ctas = (int)v;
@@ -995,6 +1048,9 @@ int fc_comm_get_option(fc_comm_t* c, int option, long long* v) {
       return FC_SUCCESS;
     case FC_OPT_ONESHOT_MAX:
       *v = c->oneshot_max >= 0 ? c->oneshot_max : (2LL << 20);
+      return FC_SUCCESS;
+    case FC_OPT_ONESHOT_AG_MAX:
+      *v = c->oneshot_ag_max >= 0 ? c->oneshot_ag_max : (16LL << 20);
       return FC_SUCCESS;
     case FC_OPT_LL_WORKER_WARPS: *v = c->ll_worker_warps; return FC_SUCCESS;
     default: return fail(c, FC_ERR_INVALID_ARG, "unknown option %d", option);

@@ -678,6 +678,98 @@ __global__ void __launch_bounds__(FC_NVLS_THREADS) fc_oneshot128_kernel(const __
   }
 }
 
+// One-shot allgather (mode 8) for the tree engine's small messages: every
+// root stores its shard as LL128 lines straight into every other rank's
+// staging (depth-1 trees: the same per-GPU egress as the forest, one hop
+// instead of its depth); receivers copy arrived lines to their output.  The
+// own shard is copied locally.  Staging halves alternate by epoch parity.
+__global__ void __launch_bounds__(FC_NVLS_THREADS) fc_oneshot_ag128_kernel(const __grid_constant__ FcNvlsParams P) {
+  __shared__ unsigned s_e;
+  FcCtl* ctl = P.ctl;
+  if (threadIdx.x == 0) s_e = *reinterpret_cast<volatile unsigned*>(&ctl->epoch) + 1;
+  __syncthreads();
+  const unsigned e = s_e;
+  const unsigned long long flag = e;
+  const long long S = P.shard_bytes;
+  const long long L = (S + 119) / 120;
+  const long long slot = L * 128;
+  const long long half = (long long)(e & 1u) * P.ll_half;
+  const long long mine = half + (long long)P.rank * slot;
+  const int lane = threadIdx.x & 31, gl = lane & 7;
+  const long long gid = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 3;
+  const long long ngrp = ((long long)gridDim.x * blockDim.x) >> 3;
+  const long long p_lane = 16LL * gl;
+  char* own = P.out + (long long)P.rank * S;
+  // 1. own shard: lines to every peer, payload to the own output slot
+  for (long long l = gid; l < L; l += ngrp) {
+    const long long pb = 120 * l + p_lane;
+    unsigned long long w0 = 0, w1 = flag;
+    if (pb + 8 <= S) {
+      w0 = __ldg(reinterpret_cast<const unsigned long long*>(P.send + pb));
+      reinterpret_cast<unsigned long long*>(own + pb)[0] = w0;
+    }
+    if (gl < 7) {
+      w1 = 0;
+      if (pb + 16 <= S) {
+        w1 = __ldg(reinterpret_cast<const unsigned long long*>(P.send + pb + 8));
+        reinterpret_cast<unsigned long long*>(own + pb + 8)[0] = w1;
+      }
+    }
+    for (int q = 0; q < P.nranks; ++q)
+      if (q != P.rank)
+        asm volatile("st.volatile.global.v2.u64 [%0], {%1, %2};" ::"l"(P.peer_stage[q] + mine + 128 * l + 16 * gl),
+                     "l"(w0), "l"(w1)
+                     : "memory");
+  }
+  // 2. every other root's lines: warp-uniform, 4 lines per warp step
+  const unsigned long long t0 = globaltimer();
+  const long long wid = gid >> 2, nw = ngrp >> 2;
+  const long long total = (long long)(P.nranks - 1) * L;  // lines to receive
+  for (long long jb = 4 * wid; jb < total; jb += 4 * nw) {
+    const long long j = jb + (lane >> 3);
+    const bool valid = j < total;
+    const int qi = valid ? (int)(j / L) : 0;
+    const int q = qi < P.rank ? qi : qi + 1;  // skip the own rank
+    const long long l = valid ? j - (long long)qi * L : 0;
+    const char* pq = P.uc_stage + half + (long long)q * slot + 128 * l + 16 * gl;
+    unsigned long long a = 0, b = flag;
+    bool ok = true;
+    for (unsigned it = 0;; ++it) {
+      if (valid)
+        asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(pq) : "memory");
+      const int mine_ok = (!valid || gl != 7 || b == flag) ? 1 : 0;
+      const int grp_ok = __shfl_sync(0xffffffffu, mine_ok, (lane & ~7) | 7);
+      if (__all_sync(0xffffffffu, grp_ok)) break;
+      if ((it & 1023u) == 1023u) {
+        int bad = 0;
+        if (lane == 0 && (*reinterpret_cast<volatile unsigned*>(&ctl->error) != 0 ||
+                          (long long)(globaltimer() - t0) > P.timeout_ns)) {
+          atomicCAS(&ctl->error, 0u, (unsigned)FC_DEVERR_TIMEOUT_AG);
+          bad = 1;
+        }
+        if (__shfl_sync(0xffffffffu, bad, 0)) {
+          ok = false;
+          break;
+        }
+      }
+    }
+    if (!ok) break;
+    if (!valid) continue;
+    char* dst = P.out + (long long)q * S;
+    const long long pb = 120 * l + p_lane;
+    if (pb + 8 <= S) reinterpret_cast<unsigned long long*>(dst + pb)[0] = a;
+    if (gl < 7 && pb + 16 <= S) reinterpret_cast<unsigned long long*>(dst + pb + 8)[0] = b;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned prev = atomicAdd(&ctl->done, 1u);
+    if (prev == gridDim.x - 1) {
+      ctl->done = 0;
+      atomicExch(&ctl->epoch, e);
+    }
+  }
+}
+
 }  // namespace
 
 int fc_nvls_launch(const FcNvlsParams& p, int ctas, void* stream) {
@@ -685,6 +777,9 @@ int fc_nvls_launch(const FcNvlsParams& p, int ctas, void* stream) {
   const void* fn;
   if (p.mode == 3)
     return (int)cudaLaunchKernel((const void*)fc_nvls_ll_ag_kernel, dim3(ctas),
+                                 dim3(FC_NVLS_THREADS), args, 0, (cudaStream_t)stream);
+  if (p.mode == 8)
+    return (int)cudaLaunchKernel((const void*)fc_oneshot_ag128_kernel, dim3(ctas),
                                  dim3(FC_NVLS_THREADS), args, 0, (cudaStream_t)stream);
   if (p.mode >= 6) {
     switch (p.dtype) {
