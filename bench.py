@@ -353,6 +353,10 @@ def run_single(args):
     }
     if not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline_allgather(comm.schedule("allgather"), 16 * MIB)
+        try:
+            line["cpu_baseline"]["reference_generate"] = generate_timings()
+        except Exception as exc:  # noqa: BLE001  (supplementary)
+            line["cpu_baseline"]["reference_generate_error"] = f"{type(exc).__name__}: {exc}"[:200]
     comm.close()
     print(json.dumps(line), flush=True)
 
@@ -360,8 +364,12 @@ def run_single(args):
 def _local_copy_comm(ex, dev):
     """1-rank forest (N=1 is outside the reference's API, topology.py:263-266):
     the root task copies send -> recv; the HBM sanity point."""
-    from paper_2402_06787_b200.schedule_io import RootTrees, Schedule, ScheduleBatch
     from fractions import Fraction
+
+    from paper_2402_06787_b200._refpath import require_collsched
+
+    cs = require_collsched()
+    RootTrees, Schedule, ScheduleBatch = cs.RootTrees, cs.Schedule, cs.ScheduleBatch
 
     s = Schedule(collective="allgather", num_compute=1, k=1, U=Fraction(1), y=Fraction(1),
                  inv_x_star=Fraction(0), roots=(RootTrees("g0", (ScheduleBatch(1, ()),)),))
@@ -631,7 +639,42 @@ def sparse_stress(dist, dev, args):
 # ---------------------------------------------------------------------------
 # reference arm: CPU executor on the host
 # ---------------------------------------------------------------------------
+def generate_timings(reps=5):
+    """Single-threaded wall time of the reference's own CPU path,
+    ``collsched.generate()`` (pipeline.py:43-78; cli.py:4-6), per topology:
+    parse_topology + bottleneck search + splitting + tree packing + pruning.
+    SURVEY.md §8d(i) / BASELINE.md §4."""
+    from paper_2402_06787_b200._refpath import require_collsched
+    from paper_2402_06787_b200.topology import canonical_json, groups_switch_doc, nvswitch_doc
+
+    cs = require_collsched()
+    out = {}
+    docs = [(f"nvswitch({n})", nvswitch_doc(n)) for n in (2, 4, 8)]
+    docs += [(f"groups_switch({b})", groups_switch_doc(b)) for b in (450, 300, 100)]
+    for name, doc in docs:
+        text = canonical_json(doc)
+        row = {}
+        for coll in ("allgather", "reduce_scatter", "allreduce"):
+            best = None
+            for _ in range(reps):
+                t0 = time.perf_counter()
+                cs.generate(cs.parse_topology(text), coll)
+                el = time.perf_counter() - t0
+                best = el if best is None else min(best, el)
+            row[coll] = round(best * 1e3, 3)
+        out[name] = row
+    return {"unit": "ms (min of %d, 1 thread)" % reps, "per_topology": out,
+            "what": "collsched.generate(parse_topology(doc), collective) wall time"}
+
+
 def run_reference(args):
+    """The reference arm on the host: the reference's CPU data path for this
+    workload.  The reference ships no executor, so
+    its tree executor is the oracle's C restatement (oracle/forest_oracle.c,
+    OpenMP over trees) run on the SAME workload as our arm: N=1 -> the
+    nvswitch(8) forest, 8 ranks x --shard-mib shards; N>=2 -> the nvswitch(N)
+    forest, M = --msg-mib total output.  The reference's own CPU path
+    (collsched.generate) is timed beside it."""
     rank = int(os.environ.get("RANK", 0))
     if rank != 0:
         return
@@ -640,7 +683,12 @@ def run_reference(args):
 
     n = 8 if args.gpus <= 1 else args.gpus
     s = get_schedule(nvswitch_doc(n), "allgather", validate=False)
-    shard_bytes = 16 * MIB
+    if args.gpus <= 1:
+        shard_bytes = args.shard_mib * MIB
+        wl = f"nvs8-forest-allgather-virtual8-{args.shard_mib}MiBx8"
+    else:
+        shard_bytes = (args.msg_mib * MIB // n) // 4 * 4
+        wl = f"nvs{n}-forest-allgather-{args.msg_mib}MiB"
     step, threads, sample = cpu_allgather_timer(s, shard_bytes)
     for _ in range(args.warmup):
         step()
@@ -650,8 +698,6 @@ def run_reference(args):
     el = (time.perf_counter() - t0) / args.steps
     M = n * shard_bytes
     v = round(gbs(M, el * 1e3), 3)
-    wl = (f"nvs8-forest-allgather-virtual8-{args.shard_mib}MiBx8" if args.gpus <= 1
-          else f"nvs{n}-forest-allgather-{args.msg_mib}MiB")
     line = {
         "impl": "reference",
         "metric": "collective algbw GB/s (ForestColl allgather, M = total output bytes per rank)",
@@ -659,12 +705,17 @@ def run_reference(args):
         "warmup": args.warmup, "ms_per_step": round(el * 1e3, 3), "higher_is_better": True,
         "scaling": "weak" if args.gpus <= 1 else "strong", "vs_baseline": None,
         "dtype": "u8 (fp32 payload, byte copy)", "data": "synthetic numpy fp32 shards",
-        "config": {"workload": wl, "sample_shard_bytes": shard_bytes},
+        "config": {"workload": wl, "M_bytes": M, "shard_bytes": shard_bytes},
         "cpu_baseline": {"value": v, "unit": "GB/s", "cores": threads, "kind": "port",
-                         "sample": f"{sample} per step (the reference ships no executor; this is "
-                                   f"its CPU restatement; host os.cpu_count()={os.cpu_count()})"},
+                         "sample": f"{sample}; the full workload every step (the reference ships "
+                                   f"no executor; this is its CPU restatement; host "
+                                   f"os.cpu_count()={os.cpu_count()})"},
         "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    try:
+        line["cpu_baseline"]["reference_generate"] = generate_timings()
+    except Exception as exc:  # noqa: BLE001  (supplementary)
+        line["cpu_baseline"]["reference_generate_error"] = f"{type(exc).__name__}: {exc}"[:200]
     print(json.dumps(line), flush=True)
 
 

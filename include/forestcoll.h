@@ -46,11 +46,22 @@
  * waits for an event recorded on the previous call's stream at issue time).
  * Outside CUDA-graph capture no further synchronisation is needed.
  *
- * Output buffers: every rank must pass the same registered buffer (same
- * registration, offset and size).  Each launch publishes a tag of its output
- * with its entry epoch; a mismatch is a device error (FC_ERR_DEVICE from
- * fc_comm_check) rather than misplaced peer stores.
- */
+ * Output buffers: only the chunk-flag protocol stores into peers' outputs
+ * (allgather recv, allreduce buf; fc_call_path tells which path a call
+ * takes).  For it, the allocation holding the output must be registered
+ * (fc_buffer_export / fc_buffer_register, collective), and every rank must
+ * pass a buffer at the same offset from the buffer it registered, with the
+ * same size (SPMD allocation order).  Each launch publishes a tag of its
+ * output with its entry epoch; a mismatch is a device error (FC_ERR_DEVICE
+ * from fc_comm_check) rather than misplaced peer stores.  The one-hop,
+ * one-shot and LL128 paths write only the library's own staging and accept
+ * any device buffers, at any alignment.
+ *
+ * Workspace: scratch_bytes (fc_comm_init) sizes two regions of that many
+ * bytes each: reduce-scatter windows of the chunk-flag protocol, and the
+ * LL128 staging (two halves alternating by launch parity).  LL128 and the
+ * one-hop paths apply only when their staging fits in half a region.
+  */
 #ifndef FORESTCOLL_H_
 #define FORESTCOLL_H_
 
@@ -100,7 +111,9 @@ extern "C" {
 #define FC_OPT_CHUNK_MAX 2     /* max bytes per chunk, flag protocol (default 256 KiB) */
 #define FC_OPT_CHUNK_MIN 3     /* min bytes per pipeline chunk (default 16 KiB) */
 #define FC_OPT_ITEMS_PER_WORKER 4 /* target work items per CTA (default 4) */
-#define FC_OPT_TIMEOUT_MS 5    /* device flag-wait timeout (default 10000 ms) */
+#define FC_OPT_TIMEOUT_MS 5    /* device flag-wait timeout (default 120000 ms, or the
+                                  FORESTCOLL_TIMEOUT_MS environment variable at init);
+                                  a timed-out wait becomes a sticky FC_ERR_DEVICE */
 #define FC_OPT_LAG 6           /* claim-order skew, chunks per tree stage (default 64) */
 #define FC_OPT_COPY_MODE 7     /* 0: TMA bulk stores, 1: TMA loads + vector stores (default 1) */
 #define FC_OPT_DMA_ROOT_COPY 8 /* allgather: copy engine places the own shard (default 0) */
@@ -121,6 +134,8 @@ extern "C" {
                                   reduce-scatter 2/N of it; 0 disables) */
 #define FC_OPT_ONESHOT_AG_MAX 21 /* tree engine: one-hop allgather (LL128 lines to every peer)
                                     up to this output size (default 16 MiB; 0 disables) */
+#define FC_OPT_MAX_CTAS_PER_RANK 22 /* read-only: largest FC_OPT_CTAS_PER_RANK this
+                                       device co-schedules for the comm's local ranks */
 
 typedef struct fc_comm fc_comm_t;
 
@@ -153,6 +168,18 @@ int fc_buffer_export_multi(fc_comm_t* comm, const void* const* ptrs, size_t byte
                            void* handles);
 int fc_buffer_register_multi(fc_comm_t* comm, const void* const* ptrs,
                              size_t bytes, const void* handles);
+/* Registration covers the whole allocation (cudaMalloc segment) holding the
+ * buffer, identified by the driver's buffer id; it never pins a buffer.
+ * fc_buffer_query: is [ptr, ptr+bytes) inside a live registration?
+ * fc_buffer_count: number of live registrations. */
+int fc_buffer_query(fc_comm_t* comm, const void* ptr, size_t bytes, int* registered);
+int fc_buffer_count(const fc_comm_t* comm);
+/* The path the next collective of this size would take: 0 chunk flags (the
+ * only path that stores into peers' outputs: allgather / allreduce outputs
+ * must then be registered), 1 LL128, 4 one-hop / one-shot, -1 empty.  The
+ * choice depends only on values equal on every rank (count, dtype, plan,
+ * options), never on buffer addresses. */
+int fc_call_path(fc_comm_t* comm, int collective, size_t count, int dtype, int* path);
 
 int fc_plan_load(fc_comm_t* comm, int collective, const int32_t* table,
                  size_t nwords);

@@ -39,7 +39,8 @@ def cmd_topology(a):
 
 
 def cmd_schedule(a):
-    from .generator import export_json, get_schedule
+    from .generator import get_schedule
+    from .schedule_io import export_json
 
     s = get_schedule(_load(a.topology), a.collective, prune=not a.no_prune)
     text = export_json(s)

@@ -21,7 +21,7 @@ OPT_CTAS_PER_RANK, OPT_CHUNK_MAX, OPT_CHUNK_MIN, OPT_ITEMS_PER_WORKER, OPT_TIMEO
 OPT_LAG, OPT_COPY_MODE, OPT_DMA_ROOT_COPY, OPT_WORKER_WARPS = 6, 7, 8, 9
 OPT_PROTO, OPT_LL_MAX, OPT_LL_CHUNK_MAX, OPT_LL_WORKER_WARPS, OPT_NVLS_CTAS = 10, 11, 12, 13, 14
 OPT_PDL, OPT_CHUNK_TAIL, OPT_NVLS_LL_MAX, OPT_NVLS_LL_HALF, OPT_NVLS_LL_RED_MAX = 15, 16, 17, 18, 19
-OPT_ONESHOT_MAX, OPT_ONESHOT_AG_MAX = 20, 21
+OPT_ONESHOT_MAX, OPT_ONESHOT_AG_MAX, OPT_MAX_CTAS_PER_RANK = 20, 21, 22
 OPTIONS = {
     "ctas_per_rank": OPT_CTAS_PER_RANK,
     "chunk_max": OPT_CHUNK_MAX,
@@ -44,6 +44,7 @@ OPTIONS = {
     "nvls_ll_red_max": OPT_NVLS_LL_RED_MAX,
     "oneshot_max": OPT_ONESHOT_MAX,
     "oneshot_ag_max": OPT_ONESHOT_AG_MAX,
+    "max_ctas_per_rank": OPT_MAX_CTAS_PER_RANK,
 }
 
 # symbol -> (restype, argtypes)
@@ -69,6 +70,9 @@ SIGNATURES = {
     "fc_buffer_export": (_I, [_P, _P, _SZ, _P]),
     "fc_buffer_register": (_I, [_P, _P, _SZ, _P]),
     "fc_buffer_deregister": (_I, [_P, _P]),
+    "fc_buffer_query": (_I, [_P, _P, _SZ, ctypes.POINTER(_I)]),
+    "fc_buffer_count": (_I, [_P]),
+    "fc_call_path": (_I, [_P, _I, _SZ, _I, ctypes.POINTER(_I)]),
     "fc_plan_load": (_I, [_P, _I, ctypes.POINTER(ctypes.c_int32), _SZ]),
     "fc_allgather": (_I, [_P, _P, _P, _SZ, _I, _P]),
     "fc_reduce_scatter": (_I, [_P, _P, _P, _SZ, _I, _I, _P]),

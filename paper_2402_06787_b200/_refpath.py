@@ -43,3 +43,20 @@ def import_collsched():
                     sys.path.remove(p)
     _CACHED.append(mod)
     return mod
+
+
+def require_collsched():
+    """The reference package, or ``ReferenceMissing``.  Schedules are always
+    the reference's own objects (parse_schedule / export, schedule.py:439-482):
+    there is no private reader to fall back to."""
+    mod = import_collsched()
+    if mod is None:
+        from .errors import ReferenceMissing
+
+        raise ReferenceMissing(
+            "the reference package `collsched` is not importable: install it with "
+            "`python -m pip install --no-index --no-build-isolation --find-links "
+            "/opt/wheelhouse --target baseline/_ref <copy of /root/reference/pkg>` "
+            "or point FORESTCOLL_REF_PATH at it"
+        )
+    return mod

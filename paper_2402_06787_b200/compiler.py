@@ -46,6 +46,7 @@ K_AG_ROOT, K_AG_FWD, K_RS_FWD, K_RS_ROOT, K_AR_ROOT, K_WAIT_AG = 1, 2, 3, 4, 5, 
 KIND_NAMES = {K_AG_ROOT: "ag_root", K_AG_FWD: "ag_fwd", K_RS_FWD: "rs_fwd",
               K_RS_ROOT: "rs_root", K_AR_ROOT: "ar_root", K_WAIT_AG: "wait_ag"}
 AR_ROOT_STAGE = FC_MAXR
+PLAN_ONEHOP = 1  # TH_FLAGS bit (fc_internal.h FC_PLAN_ONEHOP)
 
 # task word offsets (fc_internal.h)
 TW_KIND, TW_TREE, TW_STAGE, TW_ROOT, TW_MLO, TW_MHI = 0, 1, 2, 3, 4, 5
@@ -113,6 +114,11 @@ class Plan:
     table: np.ndarray
     ag_slot_units: list = field(default_factory=list)
     ag_nslots: list = field(default_factory=list)
+    flags: int = 0  # TH_FLAGS: PLAN_ONEHOP
+
+    @property
+    def onehop(self) -> bool:
+        return bool(self.flags & PLAN_ONEHOP)
 
     @property
     def max_depth(self) -> int:
@@ -328,14 +334,54 @@ def lower(schedule, ranks=None, collective: str | None = None) -> Plan:
         tasks[v] = act + wai
         nactive.append(len(act))
         nwait.append(len(wai))
+    flags = PLAN_ONEHOP if onehop_equivalent(schedule, ranks, trees, k) else 0
     table = encode(coll, n, k, trees, tasks, nactive, nwait, slot_units, nslots, ag_units,
-                   ag_nslots)
+                   ag_nslots, flags)
     return Plan(coll, n, k, ranks, trees, tasks, nactive, nwait, slot_units, nslots, table,
-                ag_units, ag_nslots)
+                ag_units, ag_nslots, flags)
+
+
+def onehop_equivalent(schedule, ranks, trees, k) -> bool:
+    """May a depth-1 all-to-all replace this forest without changing any
+    link's load (so T*, ``congestion_time`` verify.py:537-562, is unchanged)?
+
+    True when (1) every logical edge of every tree is a single physical path
+    ``[src, sw, dst]`` through one and the same switch ``sw`` (paths partition
+    an edge's copies, schedule.py:3-7; path interiors are switches,
+    verify.py:350-353) -- every GPU then has an uplink and a downlink to
+    ``sw``, so every pair has the path ``[i, sw, j]`` -- and (2) every rank
+    sends exactly (N-1)*k tree units, the one-hop scheme's uplink load
+    (downlink loads are (N-1)*k for any spanning forest).  Derived from the
+    schedule alone, so a plan table carries it (FC_PLAN_ONEHOP) to the C ABI.
+    """
+    n = len(ranks)
+    rankset = set(ranks)
+    phases = schedule.phases if schedule.collective == ALLREDUCE else (schedule,)
+    switch = None
+    for ph in phases:
+        for rt in ph.roots:
+            for batch in rt.batches:
+                for e in batch.edges:
+                    if len(e.paths) != 1:
+                        return False
+                    path = tuple(e.paths[0].path)
+                    if len(path) != 3 or path[1] in rankset or {path[0], path[2]} != {e.src, e.dst}:
+                        return False
+                    if switch is None:
+                        switch = path[1]
+                    elif path[1] != switch:
+                        return False
+    if switch is None:
+        return False
+    units = [0] * n
+    for t in trees:
+        for v in range(n):
+            units[v] += len(t.children[v]) * t.multiplicity
+    return all(u == (n - 1) * k for u in units)
 
 
 def encode(coll, n, k, trees, tasks, nactive, nwait, slot_units, nslots, ag_units=None,
-           ag_nslots=None) -> np.ndarray:
+           ag_nslots=None, flags=0) -> np.ndarray:
     ntasks = sum(len(t) for t in tasks)
     words = HEADER_WORDS + n * RANKDESC_WORDS + ntasks * TASK_WORDS
     a = np.zeros(words, dtype=np.int32)
@@ -344,6 +390,7 @@ def encode(coll, n, k, trees, tasks, nactive, nwait, slot_units, nslots, ag_unit
     a[0:12] = [MAGIC, VERSION, COLLECTIVE_CODE[coll], n, k, len(trees), ntasks, TASK_WORDS,
                max(slot_units) if slot_units else 0, max(nslots) if nslots else 0,
                max(ag_units), max(ag_nslots)]
+    a[12] = flags  # TH_FLAGS
     first = 0
     pos = HEADER_WORDS + n * RANKDESC_WORDS
     for v in range(n):

@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -41,10 +42,17 @@ struct Mapping {
   cudaIpcMemHandle_t handle;
   char* base;
 };
+// A registered allocation (the whole cudaMalloc segment holding the buffer,
+// cuMemGetAddressRange), mapped into every peer.  Keyed by the driver's
+// process-unique buffer id, so a segment freed and re-allocated at the same
+// address is recognised as new.  Tensors are never pinned: the number of
+// registrations is bounded by the allocator's segments.
 struct Reg {
-  uintptr_t lo, hi;
+  uintptr_t lo, hi;        // the local segment
+  uintptr_t anchor;        // local buffer registered (local rank 0's pointer)
   unsigned long long seq;  // registration number: equal on every rank (collective calls)
-  char* peer[FC_MAXR];
+  unsigned long long buffer_id;
+  char* peer[FC_MAXR];     // peer r's registered buffer, mapped into this process
 };
 struct Plan {
   bool loaded = false;
@@ -55,9 +63,11 @@ struct Plan {
   int nact[FC_MAXR] = {}, nwait[FC_MAXR] = {}, lag_max[FC_MAXR] = {};
   int* d_os = nullptr;  // RS/AR: one-shot forest program (FC_OS_TREE_WORDS per tree)
   int os_ntrees = 0;
+  int flags = 0;        // TH_FLAGS (FC_PLAN_ONEHOP)
 };
 
 typedef CUresult (*PFN_getRange)(CUdeviceptr*, size_t*, CUdeviceptr);
+typedef CUresult (*PFN_ptrAttr)(void*, CUpointer_attribute, CUdeviceptr);
 
 }  // namespace
 
@@ -74,7 +84,7 @@ struct fc_comm {
   Plan plans[3];
   int ctas_per_rank = 64;
   long long chunk_max = 256 << 10, chunk_min = 16 << 10, items_per_worker = 4;
-  long long timeout_ms = 10000;
+  long long timeout_ms = 120000;  // FORESTCOLL_TIMEOUT_MS overrides (default_ctas)
   int lag = 64;
   int copy_mode = 1;
   int dma_root_copy = 0;
@@ -187,6 +197,35 @@ PFN_getRange get_range_fn() {
   return fn;
 }
 
+PFN_ptrAttr ptr_attr_fn() {
+  static PFN_ptrAttr fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuPointerGetAttribute", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (PFN_ptrAttr)p;
+  }
+  return fn;
+}
+
+// The allocation (segment) holding p: base, size and process-unique buffer id.
+bool segment_of(const void* p, uintptr_t* base, size_t* size, unsigned long long* id) {
+  PFN_getRange range = get_range_fn();
+  PFN_ptrAttr attr = ptr_attr_fn();
+  if (!range || !attr) return false;
+  CUdeviceptr b = 0;
+  size_t n = 0;
+  if (range(&b, &n, (CUdeviceptr)p) != CUDA_SUCCESS) return false;
+  unsigned long long bid = 0;
+  if (attr(&bid, CU_POINTER_ATTRIBUTE_BUFFER_ID, (CUdeviceptr)p) != CUDA_SUCCESS) return false;
+  *base = (uintptr_t)b;
+  *size = n;
+  *id = bid;
+  return true;
+}
+
 int open_mapping(fc_comm* c, const cudaIpcMemHandle_t& h, char** base) {
   for (auto& m : c->maps)
     if (memcmp(&m.handle, &h, sizeof(h)) == 0) {
@@ -200,10 +239,22 @@ int open_mapping(fc_comm* c, const cudaIpcMemHandle_t& h, char** base) {
   return FC_SUCCESS;
 }
 
-const Reg* find_reg(const fc_comm* c, const void* p, size_t bytes) {
+// The live registration covering [p, p + bytes), or null.  A registration
+// whose segment was freed and its address range reused is stale (buffer id
+// differs) and dropped.
+const Reg* find_reg(fc_comm* c, const void* p, size_t bytes) {
   const uintptr_t a = (uintptr_t)p;
-  for (const auto& r : c->regs)
-    if (a >= r.lo && a + bytes <= r.hi) return &r;
+  for (size_t i = 0; i < c->regs.size(); ++i) {
+    const Reg& r = c->regs[i];
+    if (a < r.lo || a + bytes > r.hi) continue;
+    if (c->virt) return &r;
+    uintptr_t base;
+    size_t size;
+    unsigned long long id;
+    if (segment_of(p, &base, &size, &id) && id == r.buffer_id) return &r;
+    c->regs.erase(c->regs.begin() + i);  // stale
+    return nullptr;
+  }
   return nullptr;
 }
 
@@ -238,89 +289,87 @@ int order_end(fc_comm* c, cudaStream_t s) {
   return FC_SUCCESS;
 }
 
+// Tree-engine one-shot launches (fc_nvls.cu, modes 6/7/8): one grid serves
+// every local rank; several local ranks (virtual mode) launch cooperatively
+// with all CTAs co-resident.
+int oneshot_common(fc_comm* c, FcNvlsParams& P, int mode, int rd, const void* const* sends,
+                   void* const* recvs, long long half, void* stream) {
+  P.nranks = c->nranks;
+  P.rank = c->local[0];
+  P.mode = mode;
+  P.dtype = rd;
+  P.scale = 1.0f / (float)c->nranks;
+  for (int r = 0; r < c->nranks; ++r) P.peer_stage[r] = c->ws[r] + c->scratch_off + c->scratch_bytes;
+  P.ll_half = half;
+  P.timeout_ns = c->timeout_ms * 1000000LL;
+  P.nlocal = c->nlocal;
+  for (int i = 0; i < c->nlocal; ++i) {
+    P.lrank[i] = c->local[i];
+    P.lctl[i] = (FcCtl*)c->ws[c->local[i]];
+    P.lsend[i] = (const char*)sends[i];
+    P.lout[i] = (char*)recvs[i];
+  }
+  if (c->nlocal == 1) {
+    P.ctas_per_rank = c->sm_count;  // one CTA per SM: polls and tree evaluation
+  } else {
+    int maxc = 0;
+    FC_CUDA(c, (cudaError_t)fc_oneshot_max_ctas(mode, rd, &maxc));
+    P.ctas_per_rank = std::min(c->sm_count, maxc / c->nlocal);
+    if (P.ctas_per_rank < 1)
+      return fail(c, FC_ERR_UNSUPPORTED, "device cannot co-schedule %d one-shot ranks", c->nlocal);
+  }
+  {
+    const int st = order_begin(c, (cudaStream_t)stream);
+    if (st) return st;
+  }
+  const int e = fc_nvls_launch(P, P.nlocal * P.ctas_per_rank, stream);
+  if (e) return fail(c, FC_ERR_CUDA, "one-shot launch failed: %s", cudaGetErrorString((cudaError_t)e));
+  {
+    const int st = order_end(c, (cudaStream_t)stream);
+    if (st) return st;
+  }
+  c->info[0] = 1;
+  c->info[1] = 1;
+  c->info[3] = P.nlocal * P.ctas_per_rank;
+  c->info[5] = 4;  // one-shot
+  return FC_SUCCESS;
+}
+
 // One-shot reduce-scatter / allreduce for small inputs: every rank stores its
-// whole input (LL units) into every rank's LL staging through the peer
+// whole input as LL128 lines into every rank's staging through the peer
 // mappings, then evaluates the forest's in-trees locally in the executor's
-// order (fc_nvls.cu, fc_nvls_ll_red_kernel; bit-identical to the forest
-// kernel).  One hop instead of RS depth + AG depth.
-int run_oneshot(fc_comm* c, int coll, const Plan& pl, const void* send, void* out, long long S,
-                long long total, int es, int rd, int op, long long half, void* stream) {
+// order (bit-identical to the forest kernel).  One hop instead of RS depth +
+// AG depth.
+int run_oneshot(fc_comm* c, int coll, const Plan& pl, const void* const* sends,
+                void* const* recvs, long long S, long long total, int es, int rd, int op,
+                long long half, void* stream) {
   FcNvlsParams P;
   memset(&P, 0, sizeof(P));
-  P.nranks = c->nranks;
-  P.rank = c->rank;
-  // up to 256 KiB: 8-byte LL units (most parallel); above: LL128 lines (1.07x
-  // the bytes instead of 2x), measured crossover at N=4
-  const bool lines = total * es > (256LL << 10);
-  P.mode = coll == FC_REDUCE_SCATTER ? (lines ? 6 : 4) : (lines ? 7 : 5);
-  P.dtype = rd;
   P.op = op;
-  P.scale = 1.0f / (float)c->nranks;
-  P.ctl = (FcCtl*)c->ws[c->rank];
-  P.send = (const char*)send;
-  P.out = (char*)out;
-  for (int r = 0; r < c->nranks; ++r) P.peer_stage[r] = c->ws[r] + c->scratch_off + c->scratch_bytes;
-  P.uc_stage = P.peer_stage[c->rank];
-  P.ll_half = half;
   P.os_trees = pl.d_os;
   P.os_ntrees = pl.os_ntrees;
   P.k = pl.k;
   P.buf_bytes = total * es;
   P.count = total;
   P.shard_elems = S;
-  P.timeout_ns = c->timeout_ms * 1000000LL;
-  {
-    const int st = order_begin(c, (cudaStream_t)stream);
-    if (st) return st;
-  }
-  const int e = fc_nvls_launch(P, c->sm_count, stream);
-  if (e) return fail(c, FC_ERR_CUDA, "one-shot launch failed: %s", cudaGetErrorString((cudaError_t)e));
-  {
-    const int st = order_end(c, (cudaStream_t)stream);
-    if (st) return st;
-  }
-  c->info[0] = 1;
-  c->info[1] = 1;
-  c->info[5] = 4;  // one-shot
-  return FC_SUCCESS;
+  return oneshot_common(c, P, coll == FC_REDUCE_SCATTER ? 6 : 7, rd, sends, recvs, half, stream);
 }
 
-// One-shot allgather (fc_nvls.cu fc_oneshot_ag128_kernel): the output is
-// local only, so no buffer registration is used.
-int run_oneshot_ag(fc_comm* c, const void* send, void* out, long long shard_bytes, long long half,
-                   void* stream) {
+// One-hop allgather (fc_oneshot_ag128_kernel): outputs are written locally
+// only, so no buffer registration is used.
+int run_oneshot_ag(fc_comm* c, const void* const* sends, void* const* recvs,
+                   long long shard_bytes, long long half, void* stream) {
   FcNvlsParams P;
   memset(&P, 0, sizeof(P));
-  P.nranks = c->nranks;
-  P.rank = c->rank;
-  P.mode = 8;
-  P.ctl = (FcCtl*)c->ws[c->rank];
-  P.send = (const char*)send;
-  P.out = (char*)out;
-  for (int r = 0; r < c->nranks; ++r) P.peer_stage[r] = c->ws[r] + c->scratch_off + c->scratch_bytes;
-  P.uc_stage = P.peer_stage[c->rank];
-  P.ll_half = half;
   P.shard_bytes = shard_bytes;
-  P.timeout_ns = c->timeout_ms * 1000000LL;
-  {
-    const int st = order_begin(c, (cudaStream_t)stream);
-    if (st) return st;
-  }
-  const int e = fc_nvls_launch(P, c->sm_count, stream);
-  if (e) return fail(c, FC_ERR_CUDA, "one-shot launch failed: %s", cudaGetErrorString((cudaError_t)e));
-  {
-    const int st = order_end(c, (cudaStream_t)stream);
-    if (st) return st;
-  }
-  c->info[0] = 1;
-  c->info[1] = 1;
-  c->info[5] = 4;  // one-shot
-  return FC_SUCCESS;
+  return oneshot_common(c, P, 8, FC_FLOAT32, sends, recvs, half, stream);
 }
 
-// Run one collective over this comm's local ranks.
+// Run one collective over this comm's local ranks.  With `path_out` set,
+// only decide: store the path the call would take (0 chunk flags, 1 LL128,
+// 4 one-hop / one-shot) and launch nothing (fc_call_path).
 int run(fc_comm* c, int coll, const void* const* sends, void* const* recvs, size_t count,
-        int dtype, int op, void* stream) {
+        int dtype, int op, void* stream, int* path_out = nullptr) {
   if (!c) return FC_ERR_INVALID_ARG;
   if (!c->virt && !c->connected)
     return fail(c, FC_ERR_INVALID_ARG, "communicator is not connected (fc_comm_connect)");
@@ -350,36 +399,42 @@ int run(fc_comm* c, int coll, const void* const* sends, void* const* recvs, size
     stride = S;
     total = S * N;
   }
-  c->info[0] = c->info[1] = c->info[2] = c->info[3] = 0;
+  if (path_out) *path_out = -1;  // nothing to move
+  else c->info[0] = c->info[1] = c->info[2] = c->info[3] = 0;
   if (total == 0) return FC_SUCCESS;
-  for (int i = 0; i < c->nlocal; ++i)
+  for (int i = 0; i < c->nlocal && !path_out; ++i)
     if (!sends[i] || !recvs[i]) return fail(c, FC_ERR_INVALID_ARG, "null buffer");
 
-  // small allgathers: one hop (every root stores its shard into every peer's
-  // LL128 staging) instead of the forest's depth; same per-GPU egress
-  // (only under automatic protocol selection: a forced protocol is honoured)
-  if (coll == FC_ALLGATHER && !c->virt && c->nlocal == 1 && c->proto < 0 && c->oneshot_ag_max != 0) {
+  // Every choice below depends only on values that are equal on every rank
+  // (sizes, dtype, plan, options): ranks must run the same kernel.  Local
+  // buffer alignment is handled inside the kernels (ld_u64_any/st_u64_any).
+  const long long half = (long long)(c->scratch_bytes / 2) / 4096 * 4096;
+  const bool onehop = (pl.flags & FC_PLAN_ONEHOP) != 0 && c->proto < 0;
+  // small allgathers on a single-switch forest: one hop (every root stores
+  // its shard into every peer's LL128 staging) instead of the forest's depth;
+  // same per-link load (FC_PLAN_ONEHOP).  A forced protocol is honoured.
+  if (coll == FC_ALLGATHER && onehop && c->oneshot_ag_max != 0) {
     const long long bytes = total * es;  // output bytes
     // measured crossover vs the forest's LL128 at N=4: between 16 and 32 MiB
     const long long lim = c->oneshot_ag_max > 0 ? c->oneshot_ag_max : (16LL << 20);
-    const long long half = (long long)(c->scratch_bytes / 2) / 4096 * 4096;
     const long long lines = (S * es + 119) / 120;
-    if (bytes <= lim && (S * es) % 8 == 0 && (uintptr_t)sends[0] % 8 == 0 &&
-        (uintptr_t)recvs[0] % 8 == 0 && (long long)N * lines * 128 <= half)
-      return run_oneshot_ag(c, sends[0], recvs[0], S * es, half, stream);
+    if (bytes <= lim && (S * es) % 8 == 0 && (long long)N * lines * 128 <= half) {
+      if (path_out) return *path_out = 4, FC_SUCCESS;
+      return run_oneshot_ag(c, sends, recvs, S * es, half, stream);
+    }
   }
   // small reductions: one-shot (one hop) instead of the forest's two chains
-  if (coll != FC_ALLGATHER && !c->virt && c->nlocal == 1 && c->proto < 0 && pl.d_os &&
-      c->oneshot_max != 0) {
+  if (coll != FC_ALLGATHER && onehop && pl.d_os && c->oneshot_max != 0) {
     const long long bytes = total * es;  // per-rank input bytes (AR: buffer; RS: N shards)
     // measured crossover vs the forest kernel at N=4: allreduce 2 MiB,
     // reduce-scatter 2 x that / N of input
     const long long lim = c->oneshot_max > 0 ? c->oneshot_max : (2LL << 20);
-    const long long half = (long long)(c->scratch_bytes / 2) / 4096 * 4096;
+    const long long lines = (bytes + 119) / 120;
     if (bytes <= (coll == FC_REDUCE_SCATTER ? 2 * lim / N : lim) && bytes % 8 == 0 &&
-        (S * es) % 8 == 0 && (uintptr_t)sends[0] % 8 == 0 && (uintptr_t)recvs[0] % 8 == 0 &&
-        2LL * bytes * N <= half)
-      return run_oneshot(c, coll, pl, sends[0], recvs[0], S, total, es, rd, op, half, stream);
+        (S * es) % 8 == 0 && (long long)N * lines * 128 <= half) {
+      if (path_out) return *path_out = 4, FC_SUCCESS;
+      return run_oneshot(c, coll, pl, sends, recvs, S, total, es, rd, op, half, stream);
+    }
   }
   FcParams P;
   memset(&P, 0, sizeof(P));
@@ -400,20 +455,6 @@ int run(fc_comm* c, int coll, const void* const* sends, void* const* recvs, size
     P.ctl[i] = (FcCtl*)c->ws[r];
     P.send[r] = (const char*)sends[i];
     P.recv[r] = (char*)recvs[i];
-  }
-  if (!c->virt && coll != FC_REDUCE_SCATTER) {
-    const size_t need = (size_t)total * es;
-    const Reg* reg = find_reg(c, recvs[0], need);
-    if (!reg)
-      return fail(c, FC_ERR_NOT_REGISTERED,
-                  "output buffer %p (%zu bytes) is not registered (fc_buffer_register)",
-                  recvs[0], need);
-    const size_t delta = (uintptr_t)recvs[0] - reg->lo;
-    for (int r = 0; r < N; ++r)
-      if (!c->is_local[r]) P.recv[r] = reg->peer[r] + delta;
-    // identity of the output every peer must be writing to in this call
-    P.tag = (reg->seq * 0x9E3779B97F4A7C15ull) ^ ((unsigned long long)delta * 0xC2B2AE3D27D4EB4Full) ^
-            (unsigned long long)need;
   }
   P.shard_elems = S;
   P.stride_elems = stride;
@@ -453,9 +494,7 @@ int run(fc_comm* c, int coll, const void* const* sends, void* const* recvs, size
   int proto = 0;
   long long n = 0, W = 0;
   if (c->proto != 0) {
-    bool aligned = (stride * es) % 8 == 0;
-    for (int i = 0; i < c->nlocal; ++i)
-      aligned = aligned && ((uintptr_t)sends[i] % 8 == 0) && ((uintptr_t)recvs[i] % 8 == 0);
+    bool aligned = (stride * es) % 8 == 0;  // slice offsets: rank-uniform
     for (int r = 0; r < N && aligned; ++r) {
       long long Sr = std::max(0LL, std::min(S, total - (long long)r * stride));
       for (int m = 0; m <= pl.k && aligned; ++m) aligned = ((Sr * m / pl.k) * es) % 8 == 0;
@@ -468,7 +507,6 @@ int run(fc_comm* c, int coll, const void* const* sends, void* const* recvs, size
     const long long moved = (coll == FC_REDUCE_SCATTER) ? total * es : S * es * N;
     const bool want = c->proto == 1 || moved <= c->ll_max;
     // the LL region (scratch_bytes) is two halves used by alternate epochs
-    const long long half = (long long)(c->scratch_bytes / 2) / 4096 * 4096;
     if (aligned && want && need <= half) {
       proto = 1;
       n = std::min<long long>(chunks_for(c->ll_chunk_max, c->ll_worker_warps), kMaxC);
@@ -507,8 +545,28 @@ int run(fc_comm* c, int coll, const void* const* sends, void* const* recvs, size
       P.unit_bytes = unit_for(W);
     }
   }
+  if (path_out) return *path_out = proto, FC_SUCCESS;
   P.nchunks = (int)n;
   P.proto = proto;
+  // the chunk-flag protocol stores into peers' outputs (AG recv, AR buf):
+  // those must be registered; LL128 only writes peers' staging
+  if (proto == 0 && !c->virt && coll != FC_REDUCE_SCATTER) {
+    const size_t need = (size_t)total * es;
+    const Reg* reg = find_reg(c, recvs[0], need);
+    if (!reg)
+      return fail(c, FC_ERR_NOT_REGISTERED,
+                  "output buffer %p (%zu bytes) is not registered (fc_buffer_register)",
+                  recvs[0], need);
+    // peers' outputs sit at the same offset from their registered buffers
+    // (SPMD allocation order); the tag below makes any rank that disagrees
+    // fail loudly on the device before a single store lands
+    const long long delta = (long long)((uintptr_t)recvs[0] - reg->anchor);
+    for (int r = 0; r < N; ++r)
+      if (!c->is_local[r]) P.recv[r] = reg->peer[r] + delta;
+    // identity of the output every peer must be writing to in this call
+    P.tag = (reg->seq * 0x9E3779B97F4A7C15ull) ^ ((unsigned long long)delta * 0xC2B2AE3D27D4EB4Full) ^
+            (unsigned long long)need;
+  }
   const int coop = c->nlocal > 1 ? 1 : 0;  // local ranks wait on each other in one grid
   int launches = 0, grid = 0;
   {
@@ -582,6 +640,12 @@ int make_side_stream(fc_comm* c) {
 }
 
 int default_ctas(fc_comm* c) {
+  // a straggling rank (checkpoint I/O, data-loader stall) must not kill the
+  // communicator: the device flag-wait timeout defaults to minutes
+  if (const char* t = getenv("FORESTCOLL_TIMEOUT_MS")) {
+    const long long v = atoll(t);
+    if (v > 0) c->timeout_ms = v;
+  }
   int per_sm = 0, sms = 0;
   FC_CUDA(c, (cudaError_t)fc_max_ctas_per_sm(FC_FLOAT32, &per_sm));
   int v = 0;
@@ -990,6 +1054,8 @@ int fc_comm_set_option(fc_comm_t* c, int option, long long v) {
       return FC_SUCCESS;
     case FC_OPT_NVLS_LL_HALF:
       return fail(c, FC_ERR_INVALID_ARG, "nvls_ll_half is read-only");
+    case FC_OPT_MAX_CTAS_PER_RANK:
+      return fail(c, FC_ERR_INVALID_ARG, "max_ctas_per_rank is read-only");
     case FC_OPT_NVLS_LL_RED_MAX:
       if (v < 0) return fail(c, FC_ERR_INVALID_ARG, "nvls_ll_red_max < 0");
       c->nvls_ll_red_max = v;
@@ -1053,6 +1119,12 @@ int fc_comm_get_option(fc_comm_t* c, int option, long long* v) {
       *v = c->oneshot_ag_max >= 0 ? c->oneshot_ag_max : (16LL << 20);
       return FC_SUCCESS;
     case FC_OPT_LL_WORKER_WARPS: *v = c->ll_worker_warps; return FC_SUCCESS;
+    case FC_OPT_MAX_CTAS_PER_RANK: {
+      int per_sm = 0;
+      FC_CUDA(c, (cudaError_t)fc_max_ctas_per_sm(FC_FLOAT32, &per_sm));
+      *v = (long long)per_sm * c->sm_count / c->nlocal;
+      return FC_SUCCESS;
+    }
     default: return fail(c, FC_ERR_INVALID_ARG, "unknown option %d", option);
   }
 }
@@ -1117,18 +1189,17 @@ int fc_buffer_export_multi(fc_comm_t* c, const void* const* ptrs, size_t bytes, 
     memset(&b, 0, sizeof(b));
     b.magic = kBufMagic;
     b.rank = c->local[i];
-    b.bytes = bytes;
     if (!c->virt) {
       FC_CUDA(c, cudaSetDevice(c->device));
-      PFN_getRange fn = get_range_fn();
-      if (!fn) return fail(c, FC_ERR_CUDA, "cuMemGetAddressRange entry point unavailable");
-      CUdeviceptr base = 0;
+      uintptr_t base = 0;
       size_t size = 0;
-      if (fn(&base, &size, (CUdeviceptr)ptrs[i]) != CUDA_SUCCESS)
+      unsigned long long id = 0;
+      if (!segment_of(ptrs[i], &base, &size, &id))
         return fail(c, FC_ERR_INVALID_ARG, "pointer %p is not device memory", ptrs[i]);
-      if ((uintptr_t)ptrs[i] + bytes > (uintptr_t)base + size)
+      if ((uintptr_t)ptrs[i] + bytes > base + size)
         return fail(c, FC_ERR_INVALID_ARG, "buffer exceeds its allocation");
-      b.offset = (uintptr_t)ptrs[i] - (uintptr_t)base;
+      b.offset = (uintptr_t)ptrs[i] - base;  // the buffer within its mapped segment
+      b.bytes = size;
       FC_CUDA(c, cudaIpcGetMemHandle(&b.handle, (void*)base));
     }
     char* dst = (char*)handles + (size_t)i * kHandleBytes;
@@ -1143,9 +1214,11 @@ int fc_buffer_export(fc_comm_t* c, const void* ptr, size_t bytes, void* handle) 
   return fc_buffer_export_multi(c, &ptr, bytes, handle);
 }
 
-// Register one output buffer per local rank (ptrs[0..nlocal)); `handles`
-// holds one blob per rank of the communicator, in rank order.  Remote ranks'
-// buffers are opened via IPC; local ranks use the pointers passed per call.
+// Register the allocation holding one output buffer per local rank
+// (ptrs[0..nlocal)); `handles` holds one blob per rank of the communicator,
+// in rank order.  Remote ranks' segments are opened via IPC; local ranks use
+// the pointers passed per call.  Peers must later pass buffers at the same
+// offset within their segments (checked on the device by the buffer tag).
 int fc_buffer_register_multi(fc_comm_t* c, const void* const* ptrs, size_t bytes,
                              const void* handles) {
   if (!c || !ptrs) return FC_ERR_INVALID_ARG;
@@ -1154,16 +1227,18 @@ int fc_buffer_register_multi(fc_comm_t* c, const void* const* ptrs, size_t bytes
   FC_CUDA(c, cudaSetDevice(c->device));
   Reg reg;
   memset(&reg, 0, sizeof(reg));
-  reg.lo = (uintptr_t)ptrs[0];
-  reg.hi = reg.lo + bytes;
+  size_t size = 0;
+  if (!segment_of(ptrs[0], &reg.lo, &size, &reg.buffer_id))
+    return fail(c, FC_ERR_INVALID_ARG, "pointer %p is not device memory", ptrs[0]);
+  reg.hi = reg.lo + size;
+  reg.anchor = (uintptr_t)ptrs[0];
+  if ((uintptr_t)ptrs[0] + bytes > reg.hi)
+    return fail(c, FC_ERR_INVALID_ARG, "buffer exceeds its allocation");
   for (int r = 0; r < c->nranks; ++r) {
     BufBlob b;
     memcpy(&b, (const char*)handles + (size_t)r * kHandleBytes, sizeof(b));
     if (b.magic != kBufMagic || b.rank != r)
       return fail(c, FC_ERR_INVALID_ARG, "bad buffer handle for rank %d", r);
-    if (b.bytes != bytes)
-      return fail(c, FC_ERR_INVALID_ARG, "rank %d registered %llu bytes, this rank %zu", r,
-                  (unsigned long long)b.bytes, bytes);
     if (c->is_local[r]) continue;
     char* base = nullptr;
     int st = open_mapping(c, b.handle, &base);
@@ -1172,8 +1247,8 @@ int fc_buffer_register_multi(fc_comm_t* c, const void* const* ptrs, size_t bytes
   }
   reg.seq = ++c->reg_seq;
   for (auto& r : c->regs)
-    if (r.lo == reg.lo) {  // same base: keep the widest registered extent
-      if (reg.hi > r.hi) r = reg;
+    if (r.lo == reg.lo) {  // same segment (or a stale one at the same address): replace
+      r = reg;
       return FC_SUCCESS;
     }
   c->regs.push_back(reg);
@@ -1188,12 +1263,28 @@ int fc_buffer_register(fc_comm_t* c, const void* ptr, size_t bytes, const void* 
 
 int fc_buffer_deregister(fc_comm_t* c, const void* ptr) {
   if (!c) return FC_ERR_INVALID_ARG;
+  const uintptr_t a = (uintptr_t)ptr;
   for (size_t i = 0; i < c->regs.size(); ++i)
-    if (c->regs[i].lo == (uintptr_t)ptr) {
+    if (a >= c->regs[i].lo && a < c->regs[i].hi) {
       c->regs.erase(c->regs.begin() + i);
       return FC_SUCCESS;
     }
   return fail(c, FC_ERR_NOT_REGISTERED, "buffer %p was not registered", ptr);
+}
+
+int fc_buffer_query(fc_comm_t* c, const void* ptr, size_t bytes, int* registered) {
+  if (!c || !registered) return FC_ERR_INVALID_ARG;
+  *registered = (c->virt || c->nranks == 1 || find_reg(c, ptr, bytes) != nullptr) ? 1 : 0;
+  return FC_SUCCESS;
+}
+
+int fc_buffer_count(const fc_comm_t* c) { return c ? (int)c->regs.size() : -1; }
+
+int fc_call_path(fc_comm_t* c, int collective, size_t count, int dtype, int* path) {
+  if (!c || !path || collective < 0 || collective > 2) return FC_ERR_INVALID_ARG;
+  const void* no_sends[FC_MAXR] = {};  // decide only: run() touches no buffer
+  void* no_recvs[FC_MAXR] = {};
+  return run(c, collective, no_sends, no_recvs, count, dtype, FC_SUM, nullptr, path);
 }
 
 int fc_plan_load(fc_comm_t* c, int coll, const int32_t* t, size_t nwords) {
@@ -1219,6 +1310,7 @@ int fc_plan_load(fc_comm_t* c, int coll, const int32_t* t, size_t nwords) {
   p.max_slots = t[TH_MAX_SLOTS];
   p.max_ag_slot_units = t[TH_MAX_AG_SLOT_UNITS];
   p.max_ag_slots = t[TH_MAX_AG_SLOTS];
+  p.flags = t[TH_FLAGS];
   if (p.max_ag_slots > kSlotCap) return fail(c, FC_ERR_PLAN, "too many staging slots per rank");
   // validate every row
   for (int i = 0; i < ntasks; ++i) {

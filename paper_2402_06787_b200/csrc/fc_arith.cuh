@@ -73,4 +73,48 @@ struct Red<FC_INT32> {  // also uint32: wrapping two's-complement add
   __device__ static A mul(A a, float) { return a; }  // AVG is rejected for integers
 };
 
+// 8-byte payload words of caller buffers at any alignment.  The LL / LL128
+// paths are chosen from rank-uniform values only (size, dtype, plan,
+// options), so a rank whose tensor view is not 8-byte aligned runs the same
+// protocol as its peers and only its local loads / stores take this branch.
+// Staging lines are always aligned.
+__device__ __forceinline__ unsigned long long ld_u64_any(const char* p) {
+  const uintptr_t a = (uintptr_t)p;
+  if ((a & 7) == 0) return __ldcg(reinterpret_cast<const unsigned long long*>(p));
+  if ((a & 3) == 0) {
+    const unsigned* q = reinterpret_cast<const unsigned*>(p);
+    return (unsigned long long)__ldcg(q) | ((unsigned long long)__ldcg(q + 1) << 32);
+  }
+  if ((a & 1) == 0) {
+    const unsigned short* q = reinterpret_cast<const unsigned short*>(p);
+    unsigned long long v = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) v |= (unsigned long long)__ldcg(q + i) << (16 * i);
+    return v;
+  }
+  unsigned long long v = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+    v |= (unsigned long long)(unsigned char)__ldcg(reinterpret_cast<const signed char*>(p) + i) << (8 * i);
+  return v;
+}
+
+__device__ __forceinline__ void st_u64_any(char* p, unsigned long long v) {
+  const uintptr_t a = (uintptr_t)p;
+  if ((a & 7) == 0) {
+    *reinterpret_cast<unsigned long long*>(p) = v;
+  } else if ((a & 3) == 0) {
+    unsigned* q = reinterpret_cast<unsigned*>(p);
+    q[0] = (unsigned)v;
+    q[1] = (unsigned)(v >> 32);
+  } else if ((a & 1) == 0) {
+    unsigned short* q = reinterpret_cast<unsigned short*>(p);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) q[i] = (unsigned short)(v >> (16 * i));
+  } else {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) p[i] = (char)(v >> (8 * i));
+  }
+}
+
 }  // namespace

@@ -840,10 +840,9 @@ __device__ void run_item_ll(const FcParams& P, int me, FcCtl* ctl, const int* T,
     } else {
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        const unsigned long long* src =
-            reinterpret_cast<const unsigned long long*>(local_src + pay[u]) + q0;
-        if (v0[u]) w0[u] = __ldcg(src);
-        if (v1[u]) w1[u] = __ldcg(src + 1);
+        const char* src = local_src + pay[u] + 8 * q0;  // any alignment (rank-local buffer)
+        if (v0[u]) w0[u] = ld_u64_any(src);
+        if (v1[u]) w1[u] = ld_u64_any(src + 8);
       }
       if (kind != FC_K_AG_ROOT && n_rs > 0) {
         Acc8<DT> a0[U], a1[U];
@@ -883,9 +882,9 @@ __device__ void run_item_ll(const FcParams& P, int me, FcCtl* ctl, const int* T,
     if (out_local) {
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        unsigned long long* o = reinterpret_cast<unsigned long long*>(out_local + pay[u]) + q0;
-        if (v0[u]) o[0] = w0[u];
-        if (v1[u]) o[1] = w1[u];
+        char* o = out_local + pay[u] + 8 * q0;
+        if (v0[u]) st_u64_any(o, w0[u]);
+        if (v1[u]) st_u64_any(o + 8, w1[u]);
       }
     }
     // line stores to peers' staging

@@ -66,7 +66,15 @@ enum {
   TH_MAX_SLOTS = 9,
   TH_MAX_AG_SLOT_UNITS = 10,
   TH_MAX_AG_SLOTS = 11,
+  TH_FLAGS = 12,
 };
+// TH_FLAGS bits (compiler.py computes them from the schedule alone).
+// FC_PLAN_ONEHOP: every logical edge of the forest is one path through the
+// same switch [src, sw, dst], and every rank sends exactly (N-1)*k units.
+// Then each GPU has an uplink and a downlink to that switch, and a depth-1
+// all-to-all uses every link exactly as much as the forest does (same T*):
+// the one-hop allgather and the one-shot reductions may replace the forest.
+#define FC_PLAN_ONEHOP 1
 // Rank descriptor words: first task, n active, n wait, slot units, n slots.
 enum { RD_FIRST = 0, RD_NACTIVE = 1, RD_NWAIT = 2, RD_SLOT_UNITS = 3, RD_NSLOTS = 4 };
 
@@ -171,9 +179,16 @@ struct FcNvlsParams {
   long long buf_bytes;            // bytes of each rank's input buffer
   long long count;                // AR: elements of the buffer
   long long shard_elems;          // elements per root shard
-  // one-shot without multicast (tree-engine communicators): mc_stage == null and
-  // each input unit is stored to every rank's staging through its peer mapping
+  // one-shot without multicast (tree-engine communicators, modes 6/7/8): LL128
+  // lines go to every rank's staging through its peer mapping.  One grid
+  // serves `nlocal` ranks (several in virtual mode, cooperative launch):
+  // CTAs [i*ctas_per_rank, (i+1)*ctas_per_rank) run local rank lrank[i].
   char* peer_stage[FC_MAXR];
+  int nlocal, ctas_per_rank;
+  int lrank[FC_MAXR];
+  FcCtl* lctl[FC_MAXR];
+  const char* lsend[FC_MAXR];
+  char* lout[FC_MAXR];
 };
 
 // One tree of a reduce-scatter / allreduce forest for the NVLS engine's
@@ -190,3 +205,5 @@ int fc_launch(const FcParams& p, int reduce_dtype, int cooperative,
 int fc_max_ctas_per_sm(int reduce_dtype, int* out);
 int fc_warps_per_cta();
 int fc_nvls_launch(const FcNvlsParams& p, int ctas, void* stream);
+// grid size for the one-shot kernels (modes 6/7/8): every CTA co-resident
+int fc_oneshot_max_ctas(int mode, int dtype, int* out);

@@ -198,7 +198,8 @@ __global__ void __launch_bounds__(FC_NVLS_THREADS) fc_nvls_kernel(const __grid_c
 // until both flags read e.  No entry or exit barrier: staging alternates
 // between two halves by epoch parity (a rank in launch e has finished e-1,
 // which needed every rank's shard, so every rank has finished e-2, the last
-// user of this half).  Output and input may be any device buffers.
+// user of this half).  Output and input may be any device buffers (any
+// alignment: ld_u64_any / st_u64_any).
 __global__ void __launch_bounds__(FC_NVLS_THREADS) fc_nvls_ll_ag_kernel(const __grid_constant__ FcNvlsParams P) {
   __shared__ unsigned s_e;
   FcCtl* ctl = P.ctl;
@@ -211,16 +212,15 @@ __global__ void __launch_bounds__(FC_NVLS_THREADS) fc_nvls_ll_ag_kernel(const __
   const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const long long stride = (long long)gridDim.x * blockDim.x;
   // 1. own shard: one multicast store per 8 payload bytes; local copy direct
-  const uint2* src = reinterpret_cast<const uint2*>(P.send);
-  uint2* own = reinterpret_cast<uint2*>(P.out + (long long)P.rank * P.shard_bytes);
+  char* own = P.out + (long long)P.rank * P.shard_bytes;
   char* mst = P.mc_stage + half + (long long)P.rank * slot;
   for (long long i = tid; i < nunits; i += stride) {
-    const uint2 v = __ldg(src + i);
+    const unsigned long long v = ld_u64_any(P.send + 8 * i);
     asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(mst + 16 * i),
-                 "f"(__uint_as_float(v.x)), "f"(__uint_as_float(e)), "f"(__uint_as_float(v.y)),
-                 "f"(__uint_as_float(e))
+                 "f"(__uint_as_float((unsigned)v)), "f"(__uint_as_float(e)),
+                 "f"(__uint_as_float((unsigned)(v >> 32))), "f"(__uint_as_float(e))
                  : "memory");
-    own[i] = v;
+    st_u64_any(own + 8 * i, v);
   }
   // 2. every other root's shard from the local staging copy, root by root
   //    (measured ~1 us faster than gathering all roots' units together)
@@ -229,7 +229,7 @@ __global__ void __launch_bounds__(FC_NVLS_THREADS) fc_nvls_ll_ag_kernel(const __
   for (int q = 0; q < P.nranks && ok; ++q) {
     if (q == P.rank) continue;
     const char* us = P.uc_stage + half + (long long)q * slot;
-    uint2* dst = reinterpret_cast<uint2*>(P.out + (long long)q * P.shard_bytes);
+    char* dst = P.out + (long long)q * P.shard_bytes;
     for (long long i = tid; i < nunits && ok; i += stride) {
       unsigned a, fa, b, fb;
       for (unsigned it = 0;; ++it) {
@@ -246,7 +246,7 @@ __global__ void __launch_bounds__(FC_NVLS_THREADS) fc_nvls_ll_ag_kernel(const __
           break;
         }
       }
-      if (ok) dst[i] = make_uint2(a, b);
+      if (ok) st_u64_any(dst + 8 * i, (unsigned long long)a | ((unsigned long long)b << 32));
     }
   }
   __syncthreads();
@@ -259,218 +259,29 @@ __global__ void __launch_bounds__(FC_NVLS_THREADS) fc_nvls_ll_ag_kernel(const __
   }
 }
 
-// Reduce-scatter (mode 4) / allreduce (mode 5) for small buffers: every rank
-// multicasts its whole input once as LL units (same staging scheme as the
-// allgather above), so after one switch hop every GPU holds every rank's
-// input.  Each GPU then evaluates the forest's in-trees locally, in the
-// executor's order: post-order; a node adds its own value and its children's
-// partials in ascending rank order in the accumulation type and rounds once
-// (leaves forward their own value; AVG scales at the root).  The result is
-// bit-identical to the tree engine and the oracle.  Allreduce computes the
-// whole buffer on every GPU; reduce-scatter only the own shard.
-template <int DT>
-__global__ void __launch_bounds__(FC_NVLS_THREADS) fc_nvls_ll_red_kernel(const __grid_constant__ FcNvlsParams P) {
-  using R = Red<DT>;
-  using E = typename R::E;
-  using Acc = typename R::A;
-  constexpr int EPU = 8 / (int)sizeof(E);  // elements per 8-byte payload unit
-  __shared__ unsigned s_e;
-  FcCtl* ctl = P.ctl;
-  if (threadIdx.x == 0) s_e = *reinterpret_cast<volatile unsigned*>(&ctl->epoch) + 1;
-  __syncthreads();
-  const unsigned e = s_e;
-  const long long half = (long long)(e & 1u) * P.ll_half;
-  const long long slot = 2 * P.buf_bytes;
-  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  const long long stride = (long long)gridDim.x * blockDim.x;
-  // 1. the whole own input to every rank's staging: one multicast store, or
-  //    (no multicast object) one store per rank through the peer mappings
-  const uint2* src = reinterpret_cast<const uint2*>(P.send);
-  const long long nin = P.buf_bytes / 8;
-  const long long mine = half + (long long)P.rank * slot;
-  if (P.mc_stage) {
-    char* mst = P.mc_stage + mine;
-    for (long long i = tid; i < nin; i += stride) {
-      const uint2 v = __ldg(src + i);
-      asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(mst + 16 * i),
-                   "f"(__uint_as_float(v.x)), "f"(__uint_as_float(e)), "f"(__uint_as_float(v.y)),
-                   "f"(__uint_as_float(e))
-                   : "memory");
-    }
-  } else {
-    constexpr int U1 = 4;  // loads in flight per thread
-    for (long long i0 = tid; i0 < nin; i0 += stride * U1) {
-      uint2 v[U1];
-#pragma unroll
-      for (int k = 0; k < U1; ++k)
-        if (i0 + k * stride < nin) v[k] = __ldg(src + i0 + k * stride);
-      for (int q = 0; q < P.nranks; ++q) {
-        char* dq = P.peer_stage[q] + mine;
-#pragma unroll
-        for (int k = 0; k < U1; ++k)
-          if (i0 + k * stride < nin)
-            asm volatile("st.volatile.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(dq + 16 * (i0 + k * stride)),
-                         "r"(v[k].x), "r"(e), "r"(v[k].y), "r"(e)
-                         : "memory");
-      }
-    }
+// The in-tree (one-shot program row) of root r0 whose slice holds elements
+// [o0, o1] of that root's shard of Sr elements, or null if they straddle a
+// slice boundary (or lie past the shard: allreduce padding).
+__device__ __forceinline__ const int* os_tree_of(const FcNvlsParams& P, long long r0,
+                                                 long long o0, long long o1, long long Sr) {
+  for (int ti = 0; ti < P.os_ntrees && o1 < Sr; ++ti) {
+    const int* c = P.os_trees + (long long)ti * FC_OS_TREE_WORDS;
+    if (__ldg(c + OS_ROOT) != (int)r0) continue;
+    const long long lo = Sr * __ldg(c + OS_MLO) / P.k, hi = Sr * __ldg(c + OS_MHI) / P.k;
+    if (o0 >= lo && o1 < hi) return c;
   }
-  // 2. output units: allreduce the whole buffer, reduce-scatter the own shard
-  const long long S = P.shard_elems;
-  const long long u0 = P.mode == 4 ? (long long)P.rank * S * (long long)sizeof(E) / 8 : 0;
-  const long long nout = P.mode == 4 ? S * (long long)sizeof(E) / 8 : nin;
-  const unsigned long long t0 = globaltimer();
-  for (long long u = tid; u < nout; u += stride) {
-    const long long iu = u0 + u;
-    uint2 x[FC_MAXR];
-    // every slot including our own (its arrival proves the input was read),
-    // one rank at a time: a single poll in flight per thread keeps the
-    // staging reads from competing with the arriving stores
-    bool ok = true;
-    for (int q = 0; q < P.nranks && ok; ++q) {
-      const char* pq = P.uc_stage + half + (long long)q * slot + 16 * iu;
-      unsigned a, fa, b, fb;
-      for (unsigned it = 0;; ++it) {
-        asm volatile("ld.volatile.global.v4.u32 {%0,%1,%2,%3}, [%4];"
-                     : "=r"(a), "=r"(fa), "=r"(b), "=r"(fb)
-                     : "l"(pq)
-                     : "memory");
-        if (fa == e && fb == e) break;
-        if ((it & 1023u) == 1023u &&
-            (*reinterpret_cast<volatile unsigned*>(&ctl->error) != 0 ||
-             (long long)(globaltimer() - t0) > P.timeout_ns)) {
-          atomicCAS(&ctl->error, 0u, (unsigned)FC_DEVERR_TIMEOUT_RS);
-          ok = false;
-          break;
-        }
-      }
-      x[q] = make_uint2(a, b);
-    }
-    if (!ok) break;
-    uint2 res;
-    E* re = reinterpret_cast<E*>(&res);
-    // the tree of the unit's first element; if its last element is in the same
-    // slice (almost always), evaluate the tree once for all EPU lanes
-    const int* T0 = nullptr;
-    {
-      const long long g0 = iu * EPU, g1 = g0 + EPU - 1;
-      long long r0, o0, o1, Sr;
-      if (P.mode == 4) {
-        r0 = P.rank;
-        o0 = g0 - (long long)P.rank * S;
-        o1 = o0 + EPU - 1;
-        Sr = S;
-      } else {
-        r0 = g0 / S;
-        o0 = g0 - r0 * S;
-        o1 = g1 - r0 * S;
-        Sr = P.count - r0 * S;
-        Sr = Sr < S ? Sr : S;
-      }
-      for (int ti = 0; ti < P.os_ntrees && o1 < Sr; ++ti) {
-        const int* c = P.os_trees + (long long)ti * FC_OS_TREE_WORDS;
-        if (__ldg(c + OS_ROOT) != (int)r0) continue;
-        const long long lo = Sr * __ldg(c + OS_MLO) / P.k, hi = Sr * __ldg(c + OS_MHI) / P.k;
-        if (o0 >= lo && o1 < hi) {
-          T0 = c;
-          break;
-        }
-      }
-    }
-    if (T0 != nullptr) {
-      uint2 part[FC_MAXR];
-      const int np = __ldg(T0 + OS_NPOST), root = __ldg(T0 + OS_ROOT);
-      for (int a = 0; a < np; ++a) {
-        const int v = __ldg(T0 + OS_POST + a);
-        const int nc = __ldg(T0 + OS_NCH + v);
-        if (nc == 0) {
-          part[v] = x[v];
-          continue;
-        }
-        const E* xv = reinterpret_cast<const E*>(&x[v]);
-        Acc acc[EPU];
-#pragma unroll
-        for (int m = 0; m < EPU; ++m) acc[m] = R::to(xv[m]);
-        for (int q = 0; q < nc; ++q) {
-          const uint2 pc = part[__ldg(T0 + OS_CH + v * FC_MAXR + q)];
-          const E* pe = reinterpret_cast<const E*>(&pc);
-#pragma unroll
-          for (int m = 0; m < EPU; ++m) acc[m] = R::add(acc[m], R::to(pe[m]));
-        }
-        if (P.op == FC_AVG && v == root) {
-#pragma unroll
-          for (int m = 0; m < EPU; ++m) acc[m] = R::mul(acc[m], P.scale);
-        }
-        uint2 o;
-        E* oe = reinterpret_cast<E*>(&o);
-#pragma unroll
-        for (int m = 0; m < EPU; ++m) oe[m] = R::from(acc[m]);
-        part[v] = o;
-      }
-      reinterpret_cast<uint2*>(P.out)[u] = part[root];
-      continue;
-    }
-    for (int m = 0; m < EPU; ++m) {
-      const long long gi = iu * EPU + m;  // element index in every rank's buffer
-      long long r, o, Sr;
-      if (P.mode == 4) {
-        r = P.rank;
-        o = gi - (long long)P.rank * S;
-        Sr = S;
-      } else {
-        r = gi / S;
-        o = gi - r * S;
-        Sr = P.count - r * S;
-        Sr = Sr < S ? Sr : S;
-      }
-      const int* T = nullptr;
-      for (int ti = 0; ti < P.os_ntrees; ++ti) {
-        const int* c = P.os_trees + (long long)ti * FC_OS_TREE_WORDS;
-        if (__ldg(c + OS_ROOT) != (int)r) continue;
-        const long long lo = Sr * __ldg(c + OS_MLO) / P.k, hi = Sr * __ldg(c + OS_MHI) / P.k;
-        if (o >= lo && o < hi) {
-          T = c;
-          break;
-        }
-      }
-      if (T == nullptr) {  // past the last shard (padding): nothing to reduce
-        re[m] = reinterpret_cast<const E*>(&x[P.rank])[m];
-        continue;
-      }
-      E part[FC_MAXR];
-      const int np = __ldg(T + OS_NPOST), root = __ldg(T + OS_ROOT);
-      for (int a = 0; a < np; ++a) {
-        const int v = __ldg(T + OS_POST + a);
-        const E xv = reinterpret_cast<const E*>(&x[v])[m];
-        const int nc = __ldg(T + OS_NCH + v);
-        if (nc == 0) {
-          part[v] = xv;
-          continue;
-        }
-        Acc acc = R::to(xv);
-        for (int q = 0; q < nc; ++q) acc = R::add(acc, R::to(part[__ldg(T + OS_CH + v * FC_MAXR + q)]));
-        if (P.op == FC_AVG && v == root) acc = R::mul(acc, P.scale);
-        part[v] = R::from(acc);
-      }
-      re[m] = part[root];
-    }
-    reinterpret_cast<uint2*>(P.out)[u] = res;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    const unsigned prev = atomicAdd(&ctl->done, 1u);
-    if (prev == gridDim.x - 1) {
-      ctl->done = 0;
-      atomicExch(&ctl->epoch, e);
-    }
-  }
+  return nullptr;
 }
 
 // Reduce one 8-byte payload word (EPU elements at byte offset `pb` of every
 // rank's input; xs[q] = rank q's word) over the forest's in-tree that covers
-// it, in the executor's order.  Shared by the one-shot kernels.
+// it, in the executor's order: post-order; a node adds its own value and its
+// children's partials in ascending rank order in the accumulation type and
+// rounds once (leaves forward their own value; AVG scales at the root).
+// `rs` (reduce-scatter): offsets are relative to `rank`'s shard.  Shared by
+// the one-shot kernels; bit-identical to the forest kernel and the oracle.
 template <int DT>
-__device__ unsigned long long tree_word(const FcNvlsParams& P, long long pb,
+__device__ unsigned long long tree_word(const FcNvlsParams& P, bool rs, int rank, long long pb,
                                         const unsigned long long* xs) {
   using R = Red<DT>;
   using E = typename R::E;
@@ -478,12 +289,12 @@ __device__ unsigned long long tree_word(const FcNvlsParams& P, long long pb,
   constexpr int EPU = 8 / (int)sizeof(E);
   const long long S = P.shard_elems;
   const long long g0 = pb / (long long)sizeof(E);
-  const int* T0 = nullptr;
+  const int* T0;
   {
     long long r0, o0, Sr;
-    if (P.mode == 6) {
-      r0 = P.rank;
-      o0 = g0 - (long long)P.rank * S;
+    if (rs) {
+      r0 = rank;
+      o0 = g0 - (long long)rank * S;
       Sr = S;
     } else {
       r0 = g0 / S;
@@ -491,16 +302,7 @@ __device__ unsigned long long tree_word(const FcNvlsParams& P, long long pb,
       Sr = P.count - r0 * S;
       Sr = Sr < S ? Sr : S;
     }
-    const long long o1 = o0 + EPU - 1;
-    for (int ti = 0; ti < P.os_ntrees && o1 < Sr; ++ti) {
-      const int* c = P.os_trees + (long long)ti * FC_OS_TREE_WORDS;
-      if (__ldg(c + OS_ROOT) != (int)r0) continue;
-      const long long lo = Sr * __ldg(c + OS_MLO) / P.k, hi = Sr * __ldg(c + OS_MHI) / P.k;
-      if (o0 >= lo && o1 < hi) {
-        T0 = c;
-        break;
-      }
-    }
+    T0 = os_tree_of(P, r0, o0, o0 + EPU - 1, Sr);
   }
   unsigned long long part[FC_MAXR];
   if (T0 != nullptr) {  // the whole word lies in one slice: evaluate all lanes at once
@@ -540,9 +342,9 @@ __device__ unsigned long long tree_word(const FcNvlsParams& P, long long pb,
   for (int m = 0; m < EPU; ++m) {
     const long long gi = g0 + m;
     long long r, o, Sr;
-    if (P.mode == 6) {
-      r = P.rank;
-      o = gi - (long long)P.rank * S;
+    if (rs) {
+      r = rank;
+      o = gi - (long long)rank * S;
       Sr = S;
     } else {
       r = gi / S;
@@ -550,18 +352,9 @@ __device__ unsigned long long tree_word(const FcNvlsParams& P, long long pb,
       Sr = P.count - r * S;
       Sr = Sr < S ? Sr : S;
     }
-    const int* T = nullptr;
-    for (int ti = 0; ti < P.os_ntrees; ++ti) {
-      const int* c = P.os_trees + (long long)ti * FC_OS_TREE_WORDS;
-      if (__ldg(c + OS_ROOT) != (int)r) continue;
-      const long long lo = Sr * __ldg(c + OS_MLO) / P.k, hi = Sr * __ldg(c + OS_MHI) / P.k;
-      if (o >= lo && o < hi) {
-        T = c;
-        break;
-      }
-    }
-    if (T == nullptr) {
-      re[m] = reinterpret_cast<const E*>(&xs[P.rank])[m];
+    const int* T = os_tree_of(P, r, o, o, Sr);
+    if (T == nullptr) {  // past the last shard (padding): nothing to reduce
+      re[m] = reinterpret_cast<const E*>(&xs[rank])[m];
       continue;
     }
     E pe[FC_MAXR];
@@ -584,89 +377,70 @@ __device__ unsigned long long tree_word(const FcNvlsParams& P, long long pb,
   return res;
 }
 
-// One-shot reduce-scatter (mode 6) / allreduce (mode 7) for the tree engine,
-// in LL128 lines: every rank stores its whole input as 128-byte lines (120
-// payload bytes + the epoch in the last 8) into every rank's staging through
-// the peer mappings -- 1.07x the bytes instead of the 2x of 8-byte LL units --
-// then each GPU evaluates the in-trees locally (tree_word).  A warp's 8-lane
-// group moves one line; NVLink delivers it whole, so the flag in lane 7
-// vouches for the whole line (the LL128 rule of the forest kernel).
+// Reduce-scatter (mode 4) / allreduce (mode 5) for small buffers on the NVLS
+// engine: every rank multicasts its whole input once as LL units (same
+// staging scheme as the allgather above), so after one switch hop every GPU
+// holds every rank's input.  Each GPU then evaluates the forest's in-trees
+// locally in the executor's order (tree_word): bit-identical to the tree
+// engine and the oracle.  Allreduce computes the whole buffer on every GPU;
+// reduce-scatter only the own shard.  The staging is the pool's own (only
+// this 16-byte unit format is ever written there).
 template <int DT>
-__global__ void __launch_bounds__(FC_NVLS_THREADS) fc_oneshot128_kernel(const __grid_constant__ FcNvlsParams P) {
-  using E = typename Red<DT>::E;
+__global__ void __launch_bounds__(FC_NVLS_THREADS) fc_nvls_ll_red_kernel(const __grid_constant__ FcNvlsParams P) {
   __shared__ unsigned s_e;
   FcCtl* ctl = P.ctl;
   if (threadIdx.x == 0) s_e = *reinterpret_cast<volatile unsigned*>(&ctl->epoch) + 1;
   __syncthreads();
   const unsigned e = s_e;
-  const unsigned long long flag = e;
-  const long long B = P.buf_bytes;
-  const long long L = (B + 119) / 120;
-  const long long slot = L * 128;
   const long long half = (long long)(e & 1u) * P.ll_half;
-  const long long mine = half + (long long)P.rank * slot;
-  const int lane = threadIdx.x & 31, gl = lane & 7;
-  const long long gid = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 3;  // 8-lane group
-  const long long ngrp = ((long long)gridDim.x * blockDim.x) >> 3;
-  const long long p_lane = 16LL * gl;  // this lane's payload bytes within a line: [p_lane, +16)
-  // 1. every line of the own input to every rank's staging
-  for (long long l = gid; l < L; l += ngrp) {
-    const long long pb = 120 * l + p_lane;
-    unsigned long long w0 = 0, w1 = flag;
-    if (pb + 8 <= B) w0 = __ldg(reinterpret_cast<const unsigned long long*>(P.send + pb));
-    if (gl < 7) w1 = (pb + 16 <= B) ? __ldg(reinterpret_cast<const unsigned long long*>(P.send + pb + 8)) : 0ull;
-    for (int q = 0; q < P.nranks; ++q)
-      asm volatile("st.volatile.global.v2.u64 [%0], {%1, %2};" ::"l"(P.peer_stage[q] + mine + 128 * l + 16 * gl),
-                   "l"(w0), "l"(w1)
-                   : "memory");
+  const long long slot = 2 * P.buf_bytes;
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  const bool rs = P.mode == 4;
+  // 1. the whole own input to every rank's staging: one multicast store
+  const long long nin = P.buf_bytes / 8;
+  char* mst = P.mc_stage + half + (long long)P.rank * slot;
+  for (long long i = tid; i < nin; i += stride) {
+    const unsigned long long v = ld_u64_any(P.send + 8 * i);
+    asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(mst + 16 * i),
+                 "f"(__uint_as_float((unsigned)v)), "f"(__uint_as_float(e)),
+                 "f"(__uint_as_float((unsigned)(v >> 32))), "f"(__uint_as_float(e))
+                 : "memory");
   }
-  // 2. the lines holding output words: all of them (allreduce) or those of the own shard
+  // 2. output words: allreduce the whole buffer, reduce-scatter the own shard
+  using E = typename Red<DT>::E;
   const long long S = P.shard_elems;
-  const long long ob = P.mode == 6 ? (long long)P.rank * S * (long long)sizeof(E) : 0;  // first output byte
-  const long long oe = P.mode == 6 ? ob + S * (long long)sizeof(E) : B;
-  const long long l0 = ob / 120, l1 = (oe + 119) / 120;
+  const long long u0 = rs ? (long long)P.rank * S * (long long)sizeof(E) / 8 : 0;
+  const long long nout = rs ? S * (long long)sizeof(E) / 8 : nin;
   const unsigned long long t0 = globaltimer();
-  // warp-uniform loop: a warp's 4 groups take 4 consecutive lines per step
-  const long long wid = gid >> 2, nw = ngrp >> 2;
-  for (long long lb = l0 + 4 * wid; lb < l1; lb += 4 * nw) {
-    const long long l = lb + (lane >> 3);
-    const bool valid = l < l1;
-    unsigned long long x0[FC_MAXR], x1[FC_MAXR];
+  for (long long u = tid; u < nout; u += stride) {
+    const long long iu = u0 + u;
+    unsigned long long x[FC_MAXR];
+    // every slot including our own (its arrival proves the input was read),
+    // one rank at a time: a single poll in flight per thread keeps the
+    // staging reads from competing with the arriving stores
     bool ok = true;
     for (int q = 0; q < P.nranks && ok; ++q) {
-      const char* pq = P.uc_stage + half + (long long)q * slot + 128 * l + 16 * gl;
+      const char* pq = P.uc_stage + half + (long long)q * slot + 16 * iu;
+      unsigned a, fa, b, fb;
       for (unsigned it = 0;; ++it) {
-        unsigned long long a = 0, b = flag;
-        if (valid)
-          asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(pq) : "memory");
-        const int mine_ok = (gl != 7 || b == flag) ? 1 : 0;
-        const int grp_ok = __shfl_sync(0xffffffffu, mine_ok, (lane & ~7) | 7);
-        if (__all_sync(0xffffffffu, grp_ok)) {
-          x0[q] = a;
-          x1[q] = b;
+        asm volatile("ld.volatile.global.v4.u32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(a), "=r"(fa), "=r"(b), "=r"(fb)
+                     : "l"(pq)
+                     : "memory");
+        if (fa == e && fb == e) break;
+        if ((it & 1023u) == 1023u &&
+            (*reinterpret_cast<volatile unsigned*>(&ctl->error) != 0 ||
+             (long long)(globaltimer() - t0) > P.timeout_ns)) {
+          atomicCAS(&ctl->error, 0u, (unsigned)FC_DEVERR_TIMEOUT_RS);
+          ok = false;
           break;
         }
-        if ((it & 1023u) == 1023u) {
-          int bad = 0;
-          if (lane == 0 && (*reinterpret_cast<volatile unsigned*>(&ctl->error) != 0 ||
-                            (long long)(globaltimer() - t0) > P.timeout_ns)) {
-            atomicCAS(&ctl->error, 0u, (unsigned)FC_DEVERR_TIMEOUT_RS);
-            bad = 1;
-          }
-          if (__shfl_sync(0xffffffffu, bad, 0)) {
-            ok = false;
-            break;
-          }
-        }
       }
+      x[q] = (unsigned long long)a | ((unsigned long long)b << 32);
     }
     if (!ok) break;
-    if (!valid) continue;
-    const long long pb = 120 * l + p_lane;
-    if (pb >= ob && pb + 8 <= oe)
-      reinterpret_cast<unsigned long long*>(P.out + (pb - ob))[0] = tree_word<DT>(P, pb, x0);
-    if (gl < 7 && pb + 8 >= ob && pb + 16 <= oe)
-      reinterpret_cast<unsigned long long*>(P.out + (pb + 8 - ob))[0] = tree_word<DT>(P, pb + 8, x1);
+    st_u64_any(P.out + 8 * u, tree_word<DT>(P, rs, P.rank, 8 * iu, x));
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -678,15 +452,145 @@ __global__ void __launch_bounds__(FC_NVLS_THREADS) fc_oneshot128_kernel(const __
   }
 }
 
-// One-shot allgather (mode 8) for the tree engine's small messages: every
-// root stores its shard as LL128 lines straight into every other rank's
-// staging (depth-1 trees: the same per-GPU egress as the forest, one hop
-// instead of its depth); receivers copy arrived lines to their output.  The
-// own shard is copied locally.  Staging halves alternate by epoch parity.
-__global__ void __launch_bounds__(FC_NVLS_THREADS) fc_oneshot_ag128_kernel(const __grid_constant__ FcNvlsParams P) {
+// The local rank a CTA of a one-shot kernel (modes 6/7/8) serves.  One grid
+// runs P.nlocal ranks (one in production; all N in virtual mode, launched
+// cooperatively so that ranks of one grid can wait on each other).
+struct OneshotView {
+  int rank;
+  FcCtl* ctl;
+  const char* send;
+  char* out;
+  const char* stage;  // this rank's own staging (peers' lines land here)
+  long long cta, nctas;
+};
+
+__device__ __forceinline__ OneshotView oneshot_view(const FcNvlsParams& P) {
+  OneshotView v;
+  const int lr = (int)(blockIdx.x / (unsigned)P.ctas_per_rank);
+  v.rank = P.lrank[lr];
+  v.ctl = P.lctl[lr];
+  v.send = P.lsend[lr];
+  v.out = P.lout[lr];
+  v.stage = P.peer_stage[v.rank];
+  v.cta = blockIdx.x % (unsigned)P.ctas_per_rank;
+  v.nctas = P.ctas_per_rank;
+  return v;
+}
+
+__device__ __forceinline__ void oneshot_finish(const OneshotView& V, const FcNvlsParams& P,
+                                               unsigned e) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned prev = atomicAdd(&V.ctl->done, 1u);
+    if (prev == (unsigned)P.ctas_per_rank - 1u) {
+      V.ctl->done = 0;
+      atomicExch(&V.ctl->epoch, e);
+    }
+  }
+}
+
+// Poll one LL128 line (8-lane group) until its flag (lane 7's second word)
+// equals `flag`; warp-uniform.  Returns false on timeout / sticky error.
+__device__ __forceinline__ bool poll_line(const char* pq, bool valid, unsigned long long flag,
+                                          int lane, unsigned long long& a, unsigned long long& b,
+                                          FcCtl* ctl, unsigned long long t0, long long timeout_ns,
+                                          unsigned code) {
+  const int gl = lane & 7;
+  for (unsigned it = 0;; ++it) {
+    a = 0;
+    b = flag;
+    if (valid)
+      asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(pq) : "memory");
+    const int mine_ok = (!valid || gl != 7 || b == flag) ? 1 : 0;
+    const int grp_ok = __shfl_sync(0xffffffffu, mine_ok, (lane & ~7) | 7);
+    if (__all_sync(0xffffffffu, grp_ok)) return true;
+    if ((it & 1023u) == 1023u) {
+      int bad = 0;
+      if (lane == 0 && (*reinterpret_cast<volatile unsigned*>(&ctl->error) != 0 ||
+                        (long long)(globaltimer() - t0) > timeout_ns)) {
+        atomicCAS(&ctl->error, 0u, code);
+        bad = 1;
+      }
+      if (__shfl_sync(0xffffffffu, bad, 0)) return false;
+    }
+  }
+}
+
+// One-shot reduce-scatter (mode 6) / allreduce (mode 7) for the tree engine,
+// in LL128 lines: every rank stores its whole input as 128-byte lines (120
+// payload bytes + the epoch in the last 8) into every rank's staging through
+// the peer mappings -- 1.07x the bytes of the input -- then each GPU
+// evaluates the in-trees locally (tree_word).  A warp's 8-lane group moves
+// one line; NVLink delivers it whole, so the flag in lane 7 vouches for the
+// whole line (the LL128 rule of the forest kernel).  Every writer of the
+// tree engine's staging uses this line format, so a flag word there only
+// ever holds 0 or an epoch.
+template <int DT>
+__global__ void __launch_bounds__(FC_NVLS_THREADS) fc_oneshot128_kernel(const __grid_constant__ FcNvlsParams P) {
+  using E = typename Red<DT>::E;
+  const OneshotView V = oneshot_view(P);
   __shared__ unsigned s_e;
-  FcCtl* ctl = P.ctl;
-  if (threadIdx.x == 0) s_e = *reinterpret_cast<volatile unsigned*>(&ctl->epoch) + 1;
+  if (threadIdx.x == 0) s_e = *reinterpret_cast<volatile unsigned*>(&V.ctl->epoch) + 1;
+  __syncthreads();
+  const unsigned e = s_e;
+  const unsigned long long flag = e;
+  const bool rs = P.mode == 6;
+  const long long B = P.buf_bytes;
+  const long long L = (B + 119) / 120;
+  const long long slot = L * 128;
+  const long long half = (long long)(e & 1u) * P.ll_half;
+  const long long mine = half + (long long)V.rank * slot;
+  const int lane = threadIdx.x & 31, gl = lane & 7;
+  const long long gid = (V.cta * blockDim.x + threadIdx.x) >> 3;  // 8-lane group
+  const long long ngrp = (V.nctas * blockDim.x) >> 3;
+  const long long p_lane = 16LL * gl;  // this lane's payload bytes within a line: [p_lane, +16)
+  // 1. every line of the own input to every rank's staging
+  for (long long l = gid; l < L; l += ngrp) {
+    const long long pb = 120 * l + p_lane;
+    unsigned long long w0 = 0, w1 = flag;
+    if (pb + 8 <= B) w0 = ld_u64_any(V.send + pb);
+    if (gl < 7) w1 = (pb + 16 <= B) ? ld_u64_any(V.send + pb + 8) : 0ull;
+    for (int q = 0; q < P.nranks; ++q)
+      asm volatile("st.volatile.global.v2.u64 [%0], {%1, %2};" ::"l"(P.peer_stage[q] + mine + 128 * l + 16 * gl),
+                   "l"(w0), "l"(w1)
+                   : "memory");
+  }
+  // 2. the lines holding output words: all of them (allreduce) or those of the own shard
+  const long long S = P.shard_elems;
+  const long long ob = rs ? (long long)V.rank * S * (long long)sizeof(E) : 0;  // first output byte
+  const long long oe = rs ? ob + S * (long long)sizeof(E) : B;
+  const long long l0 = ob / 120, l1 = (oe + 119) / 120;
+  const unsigned long long t0 = globaltimer();
+  // warp-uniform loop: a warp's 4 groups take 4 consecutive lines per step
+  const long long wid = gid >> 2, nw = ngrp >> 2;
+  for (long long lb = l0 + 4 * wid; lb < l1; lb += 4 * nw) {
+    const long long l = lb + (lane >> 3);
+    const bool valid = l < l1;
+    unsigned long long x0[FC_MAXR], x1[FC_MAXR];
+    bool ok = true;
+    for (int q = 0; q < P.nranks && ok; ++q)
+      ok = poll_line(V.stage + half + (long long)q * slot + 128 * l + 16 * gl, valid, flag, lane,
+                     x0[q], x1[q], V.ctl, t0, P.timeout_ns, FC_DEVERR_TIMEOUT_RS);
+    if (!ok) break;
+    if (!valid) continue;
+    const long long pb = 120 * l + p_lane;
+    if (pb >= ob && pb + 8 <= oe) st_u64_any(V.out + (pb - ob), tree_word<DT>(P, rs, V.rank, pb, x0));
+    if (gl < 7 && pb + 8 >= ob && pb + 16 <= oe)
+      st_u64_any(V.out + (pb + 8 - ob), tree_word<DT>(P, rs, V.rank, pb + 8, x1));
+  }
+  oneshot_finish(V, P, e);
+}
+
+// One-hop allgather (mode 8) for the tree engine's small messages on a
+// single-switch forest (FC_PLAN_ONEHOP): every root stores its shard as LL128
+// lines straight into every other rank's staging (depth-1 trees: the same
+// per-link load as the forest, one hop instead of its depth); receivers copy
+// arrived lines to their output.  The own shard is copied locally.  Staging
+// halves alternate by epoch parity.
+__global__ void __launch_bounds__(FC_NVLS_THREADS) fc_oneshot_ag128_kernel(const __grid_constant__ FcNvlsParams P) {
+  const OneshotView V = oneshot_view(P);
+  __shared__ unsigned s_e;
+  if (threadIdx.x == 0) s_e = *reinterpret_cast<volatile unsigned*>(&V.ctl->epoch) + 1;
   __syncthreads();
   const unsigned e = s_e;
   const unsigned long long flag = e;
@@ -694,29 +598,29 @@ __global__ void __launch_bounds__(FC_NVLS_THREADS) fc_oneshot_ag128_kernel(const
   const long long L = (S + 119) / 120;
   const long long slot = L * 128;
   const long long half = (long long)(e & 1u) * P.ll_half;
-  const long long mine = half + (long long)P.rank * slot;
+  const long long mine = half + (long long)V.rank * slot;
   const int lane = threadIdx.x & 31, gl = lane & 7;
-  const long long gid = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 3;
-  const long long ngrp = ((long long)gridDim.x * blockDim.x) >> 3;
+  const long long gid = (V.cta * blockDim.x + threadIdx.x) >> 3;
+  const long long ngrp = (V.nctas * blockDim.x) >> 3;
   const long long p_lane = 16LL * gl;
-  char* own = P.out + (long long)P.rank * S;
+  char* own = V.out + (long long)V.rank * S;
   // 1. own shard: lines to every peer, payload to the own output slot
   for (long long l = gid; l < L; l += ngrp) {
     const long long pb = 120 * l + p_lane;
     unsigned long long w0 = 0, w1 = flag;
     if (pb + 8 <= S) {
-      w0 = __ldg(reinterpret_cast<const unsigned long long*>(P.send + pb));
-      reinterpret_cast<unsigned long long*>(own + pb)[0] = w0;
+      w0 = ld_u64_any(V.send + pb);
+      st_u64_any(own + pb, w0);
     }
     if (gl < 7) {
       w1 = 0;
       if (pb + 16 <= S) {
-        w1 = __ldg(reinterpret_cast<const unsigned long long*>(P.send + pb + 8));
-        reinterpret_cast<unsigned long long*>(own + pb + 8)[0] = w1;
+        w1 = ld_u64_any(V.send + pb + 8);
+        st_u64_any(own + pb + 8, w1);
       }
     }
     for (int q = 0; q < P.nranks; ++q)
-      if (q != P.rank)
+      if (q != V.rank)
         asm volatile("st.volatile.global.v2.u64 [%0], {%1, %2};" ::"l"(P.peer_stage[q] + mine + 128 * l + 16 * gl),
                      "l"(w0), "l"(w1)
                      : "memory");
@@ -729,48 +633,44 @@ __global__ void __launch_bounds__(FC_NVLS_THREADS) fc_oneshot_ag128_kernel(const
     const long long j = jb + (lane >> 3);
     const bool valid = j < total;
     const int qi = valid ? (int)(j / L) : 0;
-    const int q = qi < P.rank ? qi : qi + 1;  // skip the own rank
+    const int q = qi < V.rank ? qi : qi + 1;  // skip the own rank
     const long long l = valid ? j - (long long)qi * L : 0;
-    const char* pq = P.uc_stage + half + (long long)q * slot + 128 * l + 16 * gl;
-    unsigned long long a = 0, b = flag;
-    bool ok = true;
-    for (unsigned it = 0;; ++it) {
-      if (valid)
-        asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(pq) : "memory");
-      const int mine_ok = (!valid || gl != 7 || b == flag) ? 1 : 0;
-      const int grp_ok = __shfl_sync(0xffffffffu, mine_ok, (lane & ~7) | 7);
-      if (__all_sync(0xffffffffu, grp_ok)) break;
-      if ((it & 1023u) == 1023u) {
-        int bad = 0;
-        if (lane == 0 && (*reinterpret_cast<volatile unsigned*>(&ctl->error) != 0 ||
-                          (long long)(globaltimer() - t0) > P.timeout_ns)) {
-          atomicCAS(&ctl->error, 0u, (unsigned)FC_DEVERR_TIMEOUT_AG);
-          bad = 1;
-        }
-        if (__shfl_sync(0xffffffffu, bad, 0)) {
-          ok = false;
-          break;
-        }
-      }
-    }
-    if (!ok) break;
+    unsigned long long a, b;
+    if (!poll_line(V.stage + half + (long long)q * slot + 128 * l + 16 * gl, valid, flag, lane, a, b,
+                   V.ctl, t0, P.timeout_ns, FC_DEVERR_TIMEOUT_AG))
+      break;
     if (!valid) continue;
-    char* dst = P.out + (long long)q * S;
+    char* dst = V.out + (long long)q * S;
     const long long pb = 120 * l + p_lane;
-    if (pb + 8 <= S) reinterpret_cast<unsigned long long*>(dst + pb)[0] = a;
-    if (gl < 7 && pb + 16 <= S) reinterpret_cast<unsigned long long*>(dst + pb + 8)[0] = b;
+    if (pb + 8 <= S) st_u64_any(dst + pb, a);
+    if (gl < 7 && pb + 16 <= S) st_u64_any(dst + pb + 8, b);
   }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    const unsigned prev = atomicAdd(&ctl->done, 1u);
-    if (prev == gridDim.x - 1) {
-      ctl->done = 0;
-      atomicExch(&ctl->epoch, e);
-    }
-  }
+  oneshot_finish(V, P, e);
 }
 
 }  // namespace
+
+namespace {
+const void* oneshot_fn(int mode, int dtype) {
+  if (mode == 8) return (const void*)fc_oneshot_ag128_kernel;
+  switch (dtype) {
+    case FC_BFLOAT16: return (const void*)fc_oneshot128_kernel<FC_BFLOAT16>;
+    case FC_FLOAT16: return (const void*)fc_oneshot128_kernel<FC_FLOAT16>;
+    case FC_INT32: return (const void*)fc_oneshot128_kernel<FC_INT32>;
+    default: return (const void*)fc_oneshot128_kernel<FC_FLOAT32>;
+  }
+}
+}  // namespace
+
+int fc_oneshot_max_ctas(int mode, int dtype, int* out) {
+  int per_sm = 0, dev = 0, sms = 0;
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, oneshot_fn(mode, dtype),
+                                                                FC_NVLS_THREADS, 0);
+  if (e == cudaSuccess) e = cudaGetDevice(&dev);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  *out = per_sm * sms;
+  return (int)e;
+}
 
 int fc_nvls_launch(const FcNvlsParams& p, int ctas, void* stream) {
   void* args[] = {(void*)&p};
@@ -778,18 +678,15 @@ int fc_nvls_launch(const FcNvlsParams& p, int ctas, void* stream) {
   if (p.mode == 3)
     return (int)cudaLaunchKernel((const void*)fc_nvls_ll_ag_kernel, dim3(ctas),
                                  dim3(FC_NVLS_THREADS), args, 0, (cudaStream_t)stream);
-  if (p.mode == 8)
-    return (int)cudaLaunchKernel((const void*)fc_oneshot_ag128_kernel, dim3(ctas),
-                                 dim3(FC_NVLS_THREADS), args, 0, (cudaStream_t)stream);
   if (p.mode >= 6) {
-    switch (p.dtype) {
-      case FC_BFLOAT16: fn = (const void*)fc_oneshot128_kernel<FC_BFLOAT16>; break;
-      case FC_FLOAT16: fn = (const void*)fc_oneshot128_kernel<FC_FLOAT16>; break;
-      case FC_INT32: fn = (const void*)fc_oneshot128_kernel<FC_INT32>; break;
-      default: fn = (const void*)fc_oneshot128_kernel<FC_FLOAT32>; break;
-    }
-    return (int)cudaLaunchKernel(fn, dim3(ctas), dim3(FC_NVLS_THREADS), args, 0,
-                                 (cudaStream_t)stream);
+    // tree-engine one-shot: ctas_per_rank CTAs per local rank; ranks of one
+    // grid wait on each other, so several local ranks need co-residency
+    fn = oneshot_fn(p.mode, p.dtype);
+    const dim3 grid(p.nlocal * p.ctas_per_rank);
+    if (p.nlocal > 1)
+      return (int)cudaLaunchCooperativeKernel(fn, grid, dim3(FC_NVLS_THREADS), args, 0,
+                                              (cudaStream_t)stream);
+    return (int)cudaLaunchKernel(fn, grid, dim3(FC_NVLS_THREADS), args, 0, (cudaStream_t)stream);
   }
   if (p.mode >= 4) {
     switch (p.dtype) {

@@ -56,6 +56,11 @@ class NativeLibraryMissing(ExecutorError):
     """The compiled sm_100a library is absent: the executor has no fallback."""
 
 
+class ReferenceMissing(ExecutorError):
+    """The reference package (``collsched``) is not importable: schedules are
+    parsed, generated and validated only by the reference itself."""
+
+
 FC_CODES = {
     1: InvalidArgument,
     2: DeviceError,

@@ -144,7 +144,7 @@ class _CommBase:
 
     def t_star(self, collective: str, message_bytes: int) -> float:
         """ForestColl optimal time (seconds) for M bytes."""
-        return t_star_seconds(self.schedule(collective), message_bytes, collective)
+        return t_star_seconds(self.schedule(collective), message_bytes, collective, self.topology)
 
     # -- options / status ---------------------------------------------------
     def set_option(self, name: str, value: int) -> None:
@@ -267,7 +267,6 @@ class ForestCollComm(_CommBase):
             allh = self._allgather_obj(mine.raw)
             blob = ctypes.create_string_buffer(b"".join(allh), hb * world_size)
             _lib.check(self._lib.fc_comm_connect(self._comm, blob), self._comm, "comm_connect")
-        self._registered = {}
         self._nvls_base = None
         self._nvls_bytes = 0
         self._nvls_next = 0
@@ -420,29 +419,51 @@ class ForestCollComm(_CommBase):
 
     # -- buffers ------------------------------------------------------------
     def register(self, t: torch.Tensor) -> None:
-        """Map `t` into every peer (collective: all ranks call together with
-        same-sized tensors).  Outputs of all_gather / all_reduce must be
-        registered; first use registers automatically."""
-        key = (t.data_ptr(), t.numel() * t.element_size())
-        if key in self._registered or self.nranks == 1 or any(lo <= key[0] and key[0] + key[1] <= lo + nb
-                                   for lo, nb in self._registered):
-            return  # already mapped (views of a registered buffer included)
+        """Map the allocation (cudaMalloc segment) holding `t` into every peer.
+        Collective: all ranks call together.  Nothing is pinned: the
+        registration is keyed by the driver's buffer id and tracks the
+        segment, so the caching allocator's reuse of it costs nothing and a
+        freed-and-reused address range is recognised as new."""
+        if self.nranks == 1:
+            return
+        nbytes = t.numel() * t.element_size()
         hb = self._lib.fc_handle_bytes()
         mine = ctypes.create_string_buffer(hb)
-        _lib.check(self._lib.fc_buffer_export(self._comm, key[0], key[1], mine), self._comm,
+        _lib.check(self._lib.fc_buffer_export(self._comm, t.data_ptr(), nbytes, mine), self._comm,
                    "buffer_export")
         allh = self._allgather_obj(mine.raw)
         blob = ctypes.create_string_buffer(b"".join(allh), hb * self.nranks)
-        _lib.check(self._lib.fc_buffer_register(self._comm, key[0], key[1], blob), self._comm,
+        _lib.check(self._lib.fc_buffer_register(self._comm, t.data_ptr(), nbytes, blob), self._comm,
                    "buffer_register")
-        self._registered[key] = t  # keep the allocation alive while mapped
+
+    def _ensure_registered(self, collective: str, out: torch.Tensor, count: int, code: int) -> None:
+        """Register `out`'s allocation when this call takes the chunk-flag
+        path, the only one that stores into peers' outputs (fc_call_path; the
+        one-hop, one-shot and LL128 paths write only the library's staging).
+        The path is the same on every rank, the local registration state need
+        not be: ranks agree (one host all-gather, only on that path, i.e. for
+        messages above the LL128 limit) and register together."""
+        if self.nranks == 1:
+            return
+        path = ctypes.c_int()
+        _lib.check(self._lib.fc_call_path(self._comm, COLL_CODE[collective], count, code,
+                                          ctypes.byref(path)), self._comm, "call_path")
+        if path.value != 0:
+            return
+        have = ctypes.c_int()
+        _lib.check(self._lib.fc_buffer_query(self._comm, out.data_ptr(),
+                                             out.numel() * out.element_size(), ctypes.byref(have)),
+                   self._comm, "buffer_query")
+        if any(self._allgather_obj(not have.value)):
+            self.register(out)
+
+    def registration_count(self) -> int:
+        """Live peer registrations (one per allocator segment, never per tensor)."""
+        return int(self._lib.fc_buffer_count(self._comm))
 
     def deregister(self, t: torch.Tensor) -> None:
-        """Drop the peer mapping of a buffer registered with exactly this
-        (pointer, size); views of it are covered by the same entry."""
-        key = (t.data_ptr(), t.numel() * t.element_size())
-        if self._registered.pop(key, None) is not None:
-            self._lib.fc_buffer_deregister(self._comm, key[0])
+        """Drop the peer mapping of the allocation holding `t` (local)."""
+        self._lib.fc_buffer_deregister(self._comm, t.data_ptr())
 
     def empty(self, *shape, dtype=torch.float32) -> torch.Tensor:
         t = torch.empty(*shape, dtype=dtype, device=f"cuda:{self.device}")
@@ -467,7 +488,7 @@ class ForestCollComm(_CommBase):
                        self._comm, "nvls_allgather")
             return out
         self.plan(ALLGATHER)
-        self.register(out)
+        self._ensure_registered(ALLGATHER, out, count, code)
         _lib.check(self._lib.fc_allgather(self._comm, inp.data_ptr(), out.data_ptr(), count, code,
                                           self._stream()), self._comm, "allgather")
         return out
@@ -513,7 +534,7 @@ class ForestCollComm(_CommBase):
                                                    self._stream()), self._comm, "nvls_allreduce")
             return out
         self.plan(ALLREDUCE)
-        self.register(out)
+        self._ensure_registered(ALLREDUCE, out, buf.numel(), DTYPE_CODE[buf.dtype])
         _lib.check(self._lib.fc_allreduce(self._comm, buf.data_ptr(), out.data_ptr(), buf.numel(),
                                           DTYPE_CODE[buf.dtype], _op_code(op), self._stream()),
                    self._comm, "allreduce")
@@ -632,7 +653,6 @@ class MultiRankComm(_CommBase):
         blobs = self._gather_by_rank(mine.raw, hb)
         _lib.check(self._lib.fc_comm_connect(self._comm, ctypes.create_string_buffer(blobs, len(blobs))),
                    self._comm, "comm_connect")
-        self._registered = set()
 
     def _gather_by_rank(self, raw, hb):
         import torch.distributed as dist
@@ -645,13 +665,29 @@ class MultiRankComm(_CommBase):
                 per[r] = blob[i * hb:(i + 1) * hb]
         return b"".join(per[r] for r in range(self.nranks))
 
-    def _register(self, outs):
-        key = tuple(t.data_ptr() for t in outs) + (outs[0].numel() * outs[0].element_size(),)
-        if key in self._registered:
+    def _register(self, outs, collective, count, code):
+        """Register the local ranks' output allocations when the call takes the
+        chunk-flag path (see ForestCollComm._ensure_registered)."""
+        path = ctypes.c_int()
+        _lib.check(self._lib.fc_call_path(self._comm, COLL_CODE[collective], count, code,
+                                          ctypes.byref(path)), self._comm, "call_path")
+        if path.value != 0:
+            return
+        nbytes = outs[0].numel() * outs[0].element_size()
+        have = ctypes.c_int(1)
+        for t in outs:
+            h = ctypes.c_int()
+            _lib.check(self._lib.fc_buffer_query(self._comm, t.data_ptr(), nbytes, ctypes.byref(h)),
+                       self._comm, "buffer_query")
+            have.value &= h.value
+        import torch.distributed as dist
+
+        flags = [None] * dist.get_world_size(self._group)
+        dist.all_gather_object(flags, not have.value, group=self._group)
+        if not any(flags):
             return
         hb = self._lib.fc_handle_bytes()
         ptrs = (ctypes.c_void_p * len(outs))(*[t.data_ptr() for t in outs])
-        nbytes = outs[0].numel() * outs[0].element_size()
         mine = ctypes.create_string_buffer(hb * len(outs))
         _lib.check(self._lib.fc_buffer_export_multi(self._comm, ptrs, nbytes, mine), self._comm,
                    "buffer_export")
@@ -659,7 +695,6 @@ class MultiRankComm(_CommBase):
         _lib.check(self._lib.fc_buffer_register_multi(self._comm, ptrs, nbytes,
                                                       ctypes.create_string_buffer(blobs, len(blobs))),
                    self._comm, "buffer_register")
-        self._registered.add(key)
 
     def _ptrs(self, ts, name):
         if len(ts) != len(self.local_ranks):
@@ -673,8 +708,8 @@ class MultiRankComm(_CommBase):
 
     def all_gather(self, outs, inps):
         self.plan(ALLGATHER)
-        self._register(outs)
         count, code = _dtype_args(inps[0], inps[0].numel())
+        self._register(outs, ALLGATHER, count, code)
         _lib.check(self._lib.fc_allgather_multi(self._comm, self._ptrs(inps, "input"),
                                                 self._ptrs(outs, "output"), count, code,
                                                 self._stream()), self._comm, "allgather")
@@ -689,7 +724,7 @@ class MultiRankComm(_CommBase):
 
     def all_reduce(self, bufs, op="sum"):
         self.plan(ALLREDUCE)
-        self._register(bufs)
+        self._register(bufs, ALLREDUCE, bufs[0].numel(), DTYPE_CODE[bufs[0].dtype])
         _lib.check(self._lib.fc_allreduce_multi(
             self._comm, self._ptrs(bufs, "buffer"), self._ptrs(bufs, "buffer"), bufs[0].numel(),
             DTYPE_CODE[bufs[0].dtype], _op_code(op), self._stream()), self._comm, "allreduce")

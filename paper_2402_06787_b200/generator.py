@@ -21,9 +21,9 @@ import json
 import os
 from types import SimpleNamespace
 
-from ._refpath import import_collsched
-from .errors import PlanError, Unsupported
-from .schedule_io import COLLECTIVES, parse_schedule_json
+from ._refpath import require_collsched
+from .errors import PlanError
+from .schedule_io import COLLECTIVES, export_json, parse_schedule_json
 from .topology import canonical_json
 
 PACKAGE_CACHE = os.path.join(os.path.dirname(os.path.abspath(__file__)), "schedules")
@@ -58,13 +58,7 @@ def meta_of(schedule) -> SimpleNamespace:
 
 def generate_json(topology_doc: dict, collective: str, prune: bool = True, fixed_k=None) -> str:
     """Run the reference generator and return its canonical JSON export."""
-    cs = import_collsched()
-    if cs is None:
-        raise Unsupported(
-            "no cached schedule for this topology and collsched (the reference "
-            "generator) is not importable; install it into baseline/_ref or set "
-            "FORESTCOLL_REF_PATH"
-        )
+    cs = require_collsched()
     t = cs.parse_topology(json.dumps(topology_doc))
     s, _meta = cs.generate(t, collective, fixed_k=fixed_k, prune=prune)
     return cs.export(s, "json")
@@ -74,10 +68,9 @@ def get_schedule(topology_doc: dict, collective: str, prune: bool = True, fixed_
                  validate: bool = True, write_cache: bool = True):
     """Schedule for (topology, collective): cache hit or reference generation.
 
-    Returns the schedule (reference objects when collsched is importable,
-    else schedule_io records).  With `validate` and the reference present,
-    runs ``validate_schedule`` against the topology and raises PlanError on a
-    failing report.
+    Returns the reference's own ``Schedule`` (parsed by
+    ``collsched.parse_schedule``).  With `validate`, runs ``validate_schedule``
+    against the topology and raises PlanError on a failing report.
     """
     if collective not in COLLECTIVES:
         raise PlanError(f"unknown collective {collective!r}")
@@ -107,11 +100,11 @@ def get_schedule(topology_doc: dict, collective: str, prune: bool = True, fixed_
 
 
 def preflight(schedule, topology_doc: dict) -> None:
-    """``validate_schedule`` pre-flight (verify.py:478-534) when the reference
-    is importable; the compiler's own structural checks always run too."""
-    cs = import_collsched()
-    if cs is None:
-        return
+    """``validate_schedule`` pre-flight (verify.py:478-534), as the reference
+    CLI runs it before emitting a schedule (cli.py:186-195, exit 3).  Never
+    skipped: without the reference package this raises ReferenceMissing.
+    The compiler's own structural checks run as well."""
+    cs = require_collsched()
     t = cs.parse_topology(json.dumps(topology_doc))
     if not isinstance(schedule, cs.Schedule):
         schedule = cs.parse_schedule(export_json(schedule))
@@ -122,42 +115,3 @@ def preflight(schedule, topology_doc: dict) -> None:
             + "; ".join(f"{v.kind}: {v.detail}" for v in report.violations),
             report.violations,
         )
-
-
-def export_json(schedule) -> str:
-    """JSON export of either schedule flavour (reference field layout)."""
-    cs = import_collsched()
-    if cs is not None and isinstance(schedule, cs.Schedule):
-        return cs.export(schedule, "json")
-    return json.dumps(_doc(schedule), indent=2) + "\n"
-
-
-def _frac(f) -> str:
-    return f"{f.numerator}/{f.denominator}"
-
-
-def _doc(s) -> dict:
-    doc = {
-        "collective": s.collective,
-        "num_compute_nodes": s.num_compute,
-        "trees_per_root": s.k,
-        "optimal_inv_x": _frac(s.inv_x_star),
-        "tree_bandwidth": _frac(s.y),
-        "scale_U": _frac(s.U),
-        "exact_bound": s.exact,
-    }
-    if s.collective == "allreduce":
-        doc["phases"] = [_doc(p) for p in s.phases]
-        return doc
-    doc["roots"] = [
-        {"root": rt.root, "batches": [
-            {"multiplicity": b.multiplicity,
-             "edges": [{"src": e.src, "dst": e.dst,
-                        "paths": [{"path": list(p.path), "multiplicity": p.multiplicity}
-                                  for p in e.paths]} for e in b.edges],
-             "pruned": [{"src": h.src, "dst": h.dst, "multiplicity": h.multiplicity}
-                        for h in b.pruned]}
-            for b in rt.batches]}
-        for rt in s.roots
-    ]
-    return doc

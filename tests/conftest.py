@@ -27,11 +27,11 @@ def golden_names(collective=None):
 
 
 def load_golden(name):
-    """Golden schedule as schedule_io records (no reference needed)."""
-    from paper_2402_06787_b200.schedule_io import parse_schedule_json
+    """Golden schedule, parsed by the reference's own parse_schedule
+    (schedule.py:439-448) from the baseline/_ref install."""
+    from paper_2402_06787_b200.schedule_io import load_schedule
 
-    with open(os.path.join(GOLDEN, "schedules", name + ".json")) as f:
-        return parse_schedule_json(f.read(), prefer_reference=False)
+    return load_schedule(os.path.join(GOLDEN, "schedules", name + ".json"))
 
 
 def load_golden_topology(name):

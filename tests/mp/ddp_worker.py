@@ -7,11 +7,13 @@ import sys
 
 REPO = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, REPO)
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
 
 import torch  # noqa: E402
 import torch.distributed as dist  # noqa: E402
 from torch.nn.parallel import DistributedDataParallel as DDP  # noqa: E402
 
+from _common import init  # noqa: E402
 from paper_2402_06787_b200 import ForestCollComm  # noqa: E402
 from paper_2402_06787_b200.ddp import forestcoll_allreduce_hook  # noqa: E402
 from paper_2402_06787_b200.topology import nvswitch_doc  # noqa: E402
@@ -35,9 +37,7 @@ def grads(model, comm=None, steps=3):
 
 
 def main():
-    local = int(os.environ["LOCAL_RANK"])
-    torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    local = init()
     n = dist.get_world_size()
     comm = ForestCollComm(nvswitch_doc(n), rank=dist.get_rank(), world_size=n, device=local)
 

@@ -8,11 +8,13 @@ import sys
 
 REPO = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, REPO)
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
 
 import torch  # noqa: E402
 import torch.distributed as dist  # noqa: E402
 from torch.distributed.fsdp import FSDPModule, MixedPrecisionPolicy, fully_shard  # noqa: E402
 
+from _common import init  # noqa: E402
 from paper_2402_06787_b200 import ForestCollComm  # noqa: E402
 from paper_2402_06787_b200.fsdp import ForestCollAllGather, ForestCollReduceScatter  # noqa: E402
 from paper_2402_06787_b200.topology import nvswitch_doc  # noqa: E402
@@ -38,13 +40,24 @@ def train(net, steps=4):
         opt.zero_grad()
         loss.backward()
         opt.step()
-    return [p.full_tensor().detach().float().clone() for p in net.parameters()]
+    return [full(p) for p in net.parameters()]
+
+
+def full(p):
+    """The unsharded parameter.  DTensor.full_tensor() on a gloo group with
+    CUDA shards (FC_SAMEDEV) crashes inside gloo, so there the dim-0 shards
+    travel through host memory instead."""
+    from _common import samedev
+
+    if not samedev():
+        return p.full_tensor().detach().float().clone()
+    parts = [None] * dist.get_world_size()
+    dist.all_gather_object(parts, p.to_local().detach().float().cpu())
+    return torch.cat(parts, dim=0).cuda()
 
 
 def main():
-    local = int(os.environ["LOCAL_RANK"])
-    torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    local = init()
     rank, n = dist.get_rank(), dist.get_world_size()
     comm = ForestCollComm(nvswitch_doc(n), rank=rank, world_size=n, device=local)
     # a small first segment: the pool must grow (collectively) during training

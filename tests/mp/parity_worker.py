@@ -10,12 +10,14 @@ import sys
 
 REPO = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, REPO)
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
 
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
 import torch.distributed as dist  # noqa: E402
 
 from oracle import forest_oracle as fo  # noqa: E402
+from _common import init  # noqa: E402
 from paper_2402_06787_b200 import ForestCollComm  # noqa: E402
 from paper_2402_06787_b200.topology import nvswitch_doc  # noqa: E402
 
@@ -37,18 +39,20 @@ def seeded(n_el, dtype, seed, bits=False):
 
 
 def main():
-    local = int(os.environ["LOCAL_RANK"])
-    torch.cuda.set_device(local)
+    local = init()
     dev = torch.device(f"cuda:{local}")
-    dist.init_process_group("nccl", device_id=dev)
     rank, n = dist.get_rank(), dist.get_world_size()
     topo = nvswitch_doc(n)
     comm = ForestCollComm(topo, rank=rank, world_size=n, device=local,
                           options={"timeout_ms": 20000})
     fails = []
-    for proto in (-1, 0):  # auto (LL128 where aligned) and the chunk-flag protocol
+    # auto (one-hop / one-shot, else LL128 where aligned), auto with the
+    # one-hop paths off (the forest's LL128 lines), the chunk-flag protocol
+    for proto, onehop in ((-1, True), (-1, False), (0, True)):
         comm.set_option("proto", proto)
-        fails += [f"proto={proto}: {f}" for f in run_all(comm, rank, n, dev)]
+        comm.set_option("oneshot_ag_max", (16 << 20) if onehop else 0)
+        comm.set_option("oneshot_max", (2 << 20) if onehop else 0)
+        fails += [f"proto={proto} onehop={onehop}: {f}" for f in run_all(comm, rank, n, dev)]
     comm.check()
     print(f"RANK {rank} {'OK' if not fails else 'FAIL ' + '; '.join(fails)}", flush=True)
     comm.close()
@@ -66,6 +70,12 @@ def run_all(comm, rank, n, dev):
             out.fill_(-7.0)
             comm.all_gather(out, sends[rank].to(dev))
             torch.cuda.synchronize()
+            got = comm.last_call_info()["proto"]
+            enabled = comm.get_option("proto") < 0 and comm.get_option("oneshot_ag_max") > 0
+            if enabled and S == 4096 and got != "oneshot":
+                fails.append(f"allgather S={S} took {got}, expected the one-hop path")
+            if not enabled and got == "oneshot":
+                fails.append(f"allgather S={S} took the one-hop path although it is off")
             ref = fo.allgather(comm.schedule("allgather"), [host(x) for x in sends])[rank]
             if not np.array_equal(host(out).view(np.uint8), ref.view(np.uint8)):
                 fails.append(f"allgather S={S} seed={seed}")
@@ -98,7 +108,8 @@ def run_all(comm, rank, n, dev):
             buf = comm.empty(count, dtype=dtype)
             buf.copy_(ins[rank].to(dev))
             comm.all_reduce(buf)
-            if comm.get_option("proto") < 0 and comm.last_call_info()["proto"] != "oneshot":
+            want = "oneshot" if comm.get_option("oneshot_max") > 0 else None
+            if comm.get_option("proto") < 0 and want and comm.last_call_info()["proto"] != want:
                 fails.append(f"allreduce {name} count={count} did not take the one-shot path")
             torch.cuda.synchronize()
             ref = fo.allreduce(comm.schedule("allreduce"), [host(x) for x in ins], name)[rank]

@@ -1,0 +1,153 @@
+"""torchrun worker: N rank processes on ONE GPU (cuda:0), real peer mapping.
+
+Every rank is its own process with its own CUDA context, so the
+communicator takes the production path exactly as on N GPUs: workspace and
+output-buffer CUDA IPC handles exchanged over gloo, cudaIpcOpenMemHandle of
+the peers' memory (same device), the entry barrier with the output-buffer
+tag check, programmatic dependent launch, and the one-hop / one-shot paths
+(which virtual mode reaches only inside one grid).  Contexts of different
+processes time-slice the GPU, so every cross-rank wait spans a context
+switch: sizes stay small.  Launched by tests/test_gpu_samedev.py.
+"""
+
+import os
+import sys
+
+REPO = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, REPO)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+from oracle import forest_oracle as fo  # noqa: E402
+from paper_2402_06787_b200 import ForestCollComm  # noqa: E402
+from paper_2402_06787_b200.topology import nvswitch_doc  # noqa: E402
+
+
+def host(t):
+    if t.dtype == torch.bfloat16:
+        return t.view(torch.int16).cpu().numpy().view(np.uint16)
+    return t.cpu().numpy()
+
+
+def seeded(n_el, dtype, seed):
+    g = torch.Generator().manual_seed(seed)
+    if dtype == torch.int32:
+        return torch.randint(-2**20, 2**20, (n_el,), generator=g, dtype=torch.int32)
+    return torch.empty(n_el).uniform_(-1, 1, generator=g).to(dtype)
+
+
+def main():
+    torch.cuda.set_device(0)
+    dev = torch.device("cuda:0")
+    dist.init_process_group("gloo")
+    rank, n = dist.get_rank(), dist.get_world_size()
+    mode = sys.argv[1] if len(sys.argv) > 1 else "parity"
+    comm = ForestCollComm(nvswitch_doc(n), rank=rank, world_size=n, device=0,
+                          scratch_bytes=64 << 20, options={"timeout_ms": 60000})
+    fails = []
+    if mode == "parity":
+        fails = parity(comm, rank, n, dev)
+    elif mode == "fresh_outputs":
+        fails = fresh_outputs(comm, rank, n, dev)
+    elif mode == "mismatch":
+        fails = mismatch(comm, rank, n, dev)
+    comm.check() if mode != "mismatch" else None
+    print(f"RANK {rank} {'OK' if not fails else 'FAIL ' + '; '.join(fails)}", flush=True)
+    comm.close()
+    dist.destroy_process_group()
+    sys.exit(1 if fails else 0)
+
+
+def _check(got, ref, what, fails):
+    if not np.array_equal(np.ascontiguousarray(got).view(np.uint8),
+                          np.ascontiguousarray(ref).view(np.uint8)):
+        fails.append(what)
+
+
+def parity(comm, rank, n, dev):
+    fails = []
+    s_ag, s_rs, s_ar = (comm.schedule(c) for c in ("allgather", "reduce_scatter", "allreduce"))
+    cases = [(-1, 1 << 12, "oneshot"), (-1, (1 << 12) + 1, None), (1, 1 << 14, "ll128"),
+             (0, (1 << 14) + 3, "flags")]
+    for proto, S, want in cases:
+        comm.set_option("proto", proto)
+        ins = [seeded(S, torch.float32, 100 + r + S) for r in range(n)]
+        out = torch.empty(n * S, device=dev)
+        comm.all_gather(out, ins[rank].to(dev))
+        torch.cuda.synchronize()
+        got = comm.last_call_info()["proto"]
+        if want and got != want:
+            fails.append(f"allgather S={S}: path {got}, expected {want}")
+        _check(out.cpu().numpy(), fo.allgather(s_ag, [x.numpy() for x in ins])[rank],
+               f"allgather proto={proto} S={S}", fails)
+        for dt, dname in ((torch.bfloat16, "bfloat16"), (torch.int32, "int32")):
+            ins = [seeded(n * S, dt, 200 + r + S) for r in range(n)]
+            out = torch.empty(S, device=dev, dtype=dt)
+            comm.reduce_scatter(out, ins[rank].to(dev))
+            torch.cuda.synchronize()
+            _check(host(out), fo.reduce_scatter(s_rs, [host(x) for x in ins], dname)[rank],
+                   f"reduce_scatter proto={proto} {dname} S={S}", fails)
+            buf = seeded(n * S, dt, 300 + rank + S).to(dev)
+            hosts = [host(seeded(n * S, dt, 300 + r + S)) for r in range(n)]
+            comm.all_reduce(buf)
+            torch.cuda.synchronize()
+            _check(host(buf), fo.allreduce(s_ar, hosts, dname)[rank],
+                   f"allreduce proto={proto} {dname} S={S}", fails)
+    comm.set_option("proto", -1)
+    return fails
+
+
+def fresh_outputs(comm, rank, n, dev):
+    """The NCCL idiom: a fresh output tensor every call.  Registrations track
+    allocator segments, never tensors: their number stays bounded and no
+    tensor is kept alive."""
+    fails = []
+    comm.set_option("proto", 0)  # the chunk-flag protocol writes peers' outputs
+    S = 1 << 12
+    inp = torch.full((S,), float(rank), device=dev)
+    ref = torch.cat([torch.full((S,), float(r)) for r in range(n)])
+    torch.cuda.synchronize()
+    base = torch.cuda.memory_allocated(dev)
+    for i in range(1000):
+        out = torch.empty(n * S + (i % 7), device=dev)[: n * S]
+        comm.all_gather(out, inp)
+        if i % 97 == 0 and not torch.equal(out.cpu(), ref):
+            fails.append(f"call {i}: wrong output")
+        del out
+    torch.cuda.synchronize()
+    grown = torch.cuda.memory_allocated(dev) - base
+    if grown > (1 << 20):
+        fails.append(f"allocated memory grew by {grown} bytes over 1000 calls")
+    nreg = comm.registration_count()
+    if nreg > 4:
+        fails.append(f"{nreg} registrations after 1000 calls")
+    return fails
+
+
+def mismatch(comm, rank, n, dev):
+    """Rank 0 passes a different (registered) output than its peers: the
+    device check fails loudly instead of receiving misplaced stores."""
+    from paper_2402_06787_b200 import DeviceError
+
+    comm.set_option("proto", 0)
+    comm.set_option("timeout_ms", 4000)
+    S = 1 << 12
+    a = torch.empty(n * S, device=dev)
+    b = torch.empty(n * S, device=dev)
+    inp = torch.ones(S, device=dev)
+    comm.all_gather(a, inp)  # registers the segment(s)
+    comm.all_gather(b, inp)
+    torch.cuda.synchronize()
+    comm.all_gather(b if rank == 0 else a, inp)
+    try:
+        comm.check()
+    except DeviceError as e:
+        print(f"RANK {rank} detected: {e}", flush=True)
+        return []
+    return ["mismatch not detected"] if rank == 0 else []
+
+
+if __name__ == "__main__":
+    main()

@@ -9,20 +9,20 @@ import sys
 
 REPO = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, REPO)
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
 
 import torch  # noqa: E402
 import torch.distributed as dist  # noqa: E402
 
+from _common import init  # noqa: E402
 from paper_2402_06787_b200 import ForestCollComm  # noqa: E402
 from paper_2402_06787_b200.topology import nvswitch_doc  # noqa: E402
 
 
 def main():
     iters = int(sys.argv[1]) if len(sys.argv) > 1 else 200
-    local = int(os.environ["LOCAL_RANK"])
-    torch.cuda.set_device(local)
+    local = init()
     dev = torch.device(f"cuda:{local}")
-    dist.init_process_group("nccl", device_id=dev)
     rank, n = dist.get_rank(), dist.get_world_size()
     comm = ForestCollComm(nvswitch_doc(n), rank=rank, world_size=n, device=local,
                           scratch_bytes=256 << 20, options={"timeout_ms": 20000})

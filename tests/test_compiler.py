@@ -8,7 +8,10 @@ import pytest
 from conftest import golden_names, load_golden
 from paper_2402_06787_b200 import compiler as C
 from paper_2402_06787_b200.errors import PlanError
-from paper_2402_06787_b200.schedule_io import ScheduleBatch, ScheduleEdge
+from paper_2402_06787_b200._refpath import require_collsched
+
+_cs = require_collsched()
+ScheduleBatch, ScheduleEdge = _cs.ScheduleBatch, _cs.ScheduleEdge
 
 
 @pytest.mark.parametrize("name", golden_names())

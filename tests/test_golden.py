@@ -37,13 +37,21 @@ def test_fixture_validates_and_attains_bound(name):
     assert cs.congestion_time(s, t) == phases * Fraction(s.inv_x_star) / s.num_compute
 
 
-def test_package_cache_serves_reference_schedules_without_reference(monkeypatch):
-    """The GPU box has no reference: the shipped cache must yield the same
-    forests as the fixtures, through the package's own JSON reader."""
-    from paper_2402_06787_b200 import _refpath, generator
+def test_package_cache_serves_reference_schedules_without_generating(monkeypatch):
+    """The shipped cache yields the fixtures' forests without running the
+    generator: schedules are parsed by the reference's own parse_schedule
+    (schedule.py:439-448) and re-exported byte-identical by its export."""
+    from paper_2402_06787_b200 import generator
+    from paper_2402_06787_b200._refpath import require_collsched
+    from paper_2402_06787_b200.schedule_io import export_json
     from paper_2402_06787_b200.topology import groups_switch_doc, nvswitch_doc
 
-    monkeypatch.setattr(_refpath, "_CACHED", [None])
+    cs = require_collsched()
+
+    def no_generate(*a, **k):
+        raise AssertionError("generate() called although the schedule is cached")
+
+    monkeypatch.setattr(cs, "generate", no_generate)
     monkeypatch.setenv("FORESTCOLL_CACHE", "/nonexistent-cache-dir")
     cases = {f"nvs{n}": nvswitch_doc(n) for n in (2, 4, 8)}
     cases.update({f"groups{b}": groups_switch_doc(b) for b in (450, 300, 100)})
@@ -51,8 +59,24 @@ def test_package_cache_serves_reference_schedules_without_reference(monkeypatch)
         assert doc == load_golden_topology(name)
         for coll in ("allgather", "reduce_scatter", "allreduce"):
             s = generator.get_schedule(doc, coll, validate=False, write_cache=False)
+            assert isinstance(s, cs.Schedule)
             with open(os.path.join(GOLDEN, "schedules", f"{name}_{coll}.json")) as f:
-                assert generator.export_json(s) == f.read()
+                assert export_json(s) == f.read()
+
+
+def test_missing_reference_fails_loudly(monkeypatch):
+    """No private schedule reader: without collsched every schedule entry
+    point raises ReferenceMissing (and pre-flight is never skipped)."""
+    from paper_2402_06787_b200 import _refpath, generator
+    from paper_2402_06787_b200.errors import ReferenceMissing
+    from paper_2402_06787_b200.topology import nvswitch_doc
+
+    s = load_golden("nvs4_allgather")
+    monkeypatch.setattr(_refpath, "_CACHED", [None])
+    with pytest.raises(ReferenceMissing):
+        generator.get_schedule(nvswitch_doc(4), "allgather", validate=False, write_cache=False)
+    with pytest.raises(ReferenceMissing):
+        generator.preflight(s, nvswitch_doc(4))
 
 
 def test_appendix_a_forest_shape():

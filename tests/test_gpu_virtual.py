@@ -46,7 +46,9 @@ def _comm(s, proto="auto", **kw):
     return VirtualComm(schedules={s.collective: s}, options=opts, **kw)
 
 
-PROTOS = ["auto", "flags"]  # auto = LL128 whenever slices are 8-byte aligned
+PROTOS = ["auto", "flags"]  # auto: one-hop / one-shot (single-switch forests), else LL128
+# whenever slices are 8-byte aligned; the forest LL128 path at production
+# widths is pinned in test_gpu_production.py
 
 
 @pytest.mark.parametrize("proto", PROTOS)
@@ -170,6 +172,7 @@ def test_avg_rejected_for_integers(dev):
 def test_ll128_is_used_for_aligned_medium_messages(dev, name):
     s = load_golden(name)
     comm = _comm(s)
+    comm.set_option("oneshot_ag_max", 0)  # nvs8: keep the forest (not the one-hop path)
     n = comm.nranks
     S = 6 * 10924  # 8-byte aligned batch slices for k in {1, 2, 3, 6, 7?}
     S = S - S % (2 * s.k)
