@@ -551,9 +551,9 @@ def sweep_multi(comm, dist, n, dev, args):
         res["nvls"] = nvls_points(dist, dev, n, args)
     except Exception as exc:
         res["nvls_error"] = f"{type(exc).__name__}: {exc}"[:300]
-    if n == 8:
+    if n in (4, 8):
         try:
-            res["sparse_stress"] = sparse_stress(dist, dev, args)
+            res["sparse_stress"] = sparse_stress(dist, dev, n, args)
         except Exception as exc:
             res["sparse_stress_error"] = f"{type(exc).__name__}: {exc}"[:300]
     return res
@@ -569,7 +569,8 @@ def nvls_points(dist, dev, n, args):
     from paper_2402_06787_b200.topology import nvswitch_doc
 
     c = ForestCollComm(nvswitch_doc(n, multicast=True), rank=dist.get_rank(), world_size=n,
-                       device=dev.index, scratch_bytes=64 << 20, nvls_bytes=1100 << 20)
+                       device=dev.index, scratch_bytes=64 << 20, nvls_bytes=1100 << 20,
+                       reduction_order="switch")
     if not c.nvls_enabled:
         c.close()
         return {"skipped": "no NVSwitch multicast support"}
@@ -606,11 +607,13 @@ def nvls_points(dist, dev, n, args):
     return out
 
 
-def sparse_stress(dist, dev, args):
-    """BASELINE configs[4]: the 2-groups-of-4 box joined only by two bridge
-    pairs.  The forest is the reference's packing for
-    that graph; it runs on the physical NVSwitch, so achieved bandwidth can
-    exceed the declared graph's T*."""
+def sparse_stress(dist, dev, n, args):
+    """BASELINE configs[4]: two groups of n/2 GPUs joined only by two bridge
+    pairs (n = 8, and its 4-GPU analogue at n = 4).
+    The forest is the reference's packing for that graph (k up to 3, paths
+    through both switches and the bridges); it runs on the physical NVSwitch,
+    so achieved bandwidth can exceed the declared graph's T* when the graph
+    is slower than the box (small beta)."""
     import torch
 
     from paper_2402_06787_b200 import ForestCollComm
@@ -619,18 +622,29 @@ def sparse_stress(dist, dev, args):
     out = []
     rank = dist.get_rank()
     for beta in (450, 300, 100):
-        c = ForestCollComm(groups_switch_doc(beta), rank=rank, world_size=8,
+        c = ForestCollComm(groups_switch_doc(beta, n=n), rank=rank, world_size=n,
                            device=dev.index, scratch_bytes=1 << 30)
-        M = args.msg_mib * MIB
-        S = M // 8 // 4
-        inp = torch.randn(S, device=dev)
-        o = c.empty(8 * S, dtype=torch.float32)
-        ms = timed(lambda: c.all_gather(o, inp), max(5, args.steps), 3, dist)
-        t = c.t_star("allgather", M)
-        out.append({"topology": f"groups_switch({beta})", "k": c.schedule("allgather").k,
-                    "collective": "allgather", "M_bytes": M, "ms": round(ms, 4),
-                    "algbw_GBps": round(gbs(M, ms), 2), "graph_t_star_ms": round(t * 1e3, 4),
-                    "frac_of_graph_t_star": round(t * 1e3 / ms, 4)})
+        for coll in ("allgather", "allreduce"):
+            M = args.msg_mib * MIB
+            if coll == "allgather":
+                S = M // n // 4
+                inp = torch.randn(S, device=dev)
+                o = c.empty(n * S, dtype=torch.float32)
+                fn = lambda: c.all_gather(o, inp)  # noqa: E731
+            else:
+                o = c.empty(M // 2, dtype=torch.bfloat16)
+                o.normal_()
+                fn = lambda: c.all_reduce(o)  # noqa: E731
+            ms = timed(fn, max(5, args.steps), 3, dist)
+            t = c.t_star(coll, M)
+            out.append({"topology": f"groups_switch({beta}, n={n})", "k": c.schedule(coll).k
+                        if coll != "allreduce" else c.schedule(coll).phases[0].k,
+                        "collective": coll, "M_bytes": M, "ms": round(ms, 4),
+                        "proto": c.last_call_info()["proto"],
+                        "algbw_GBps": round(gbs(M, ms), 2), "graph_t_star_ms": round(t * 1e3, 4),
+                        "frac_of_graph_t_star": round(t * 1e3 / ms, 4)})
+            c.deregister(o)
+            del o
         c.check()
         c.close()
     return out

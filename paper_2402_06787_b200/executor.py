@@ -96,6 +96,15 @@ def _as_doc(topology):
     return json.loads(cs.serialize_topology(topology))
 
 
+def _aligned(t: torch.Tensor) -> torch.Tensor:
+    """`t`, or an aligned copy of it when its address is not 16-byte aligned
+    (the LL-multicast kernels move 8/16-byte units).  Only the local buffer's
+    placement decides this, never the engine choice."""
+    if t.data_ptr() % 16 == 0:
+        return t
+    return t.clone()
+
+
 class _CommBase:
     """Shared plan management for real and virtual communicators."""
 
@@ -169,9 +178,13 @@ class _CommBase:
     def last_call_info(self) -> dict:
         buf = (ctypes.c_longlong * 8)()
         self._lib.fc_last_call_info(self._comm, buf, 8)
-        return {"launches": buf[0], "nchunks": buf[1], "window": buf[2], "grid": buf[3],
+        info = {"launches": buf[0], "nchunks": buf[1], "window": buf[2], "grid": buf[3],
                 "unit_bytes": buf[4],
                 "proto": {0: "flags", 1: "ll128", 2: "nvls", 3: "nvls_ll", 4: "oneshot"}[buf[5]]}
+        # floating-point summation order of the last reduction: "tree" (the
+        # forest's order, bit-exact vs the oracle) or "switch" (in-NVSwitch)
+        info["order"] = getattr(self, "_last_order", None)
+        return info
 
     # -- tracing ------------------------------------------------------------
     TRACE_DTYPE = np.dtype([("t_start", "<u8"), ("t_end", "<u8"), ("t_wait", "<u4"),
@@ -229,8 +242,16 @@ class ForestCollComm(_CommBase):
 
     def __init__(self, topology=None, *, rank=None, world_size=None, device=None, group=None,
                  scratch_bytes=DEFAULT_SCRATCH, schedules=None, validate=True, prune=True,
-                 options=None, nvls_bytes=0):
+                 options=None, nvls_bytes=0, reduction_order="tree"):
         import torch.distributed as dist
+
+        if reduction_order not in ("tree", "switch"):
+            raise InvalidArgument("reduction_order must be 'tree' or 'switch'")
+        # "tree": every floating-point sum in the forest's order (bit-exact vs
+        # the oracle, whatever the buffer); "switch": tensors in the NVLS pool
+        # are reduced inside the NVSwitch (multimem.ld_reduce), in its order
+        self.reduction_order = reduction_order
+        self._last_order = None
 
         if rank is None or world_size is None:
             if not dist.is_initialized():
@@ -355,8 +376,9 @@ class ForestCollComm(_CommBase):
         """Small allgather the NVLS engine runs as LL over multicast (any buffers)."""
         nb = out.numel() * out.element_size()
         sb = inp.numel() * inp.element_size()
+        # sizes only (equal on every rank): local pointer alignment must not
+        # pick the engine, or ranks could run different kernels
         return (self.nvls_enabled and nb <= self._nvls_ll_max and sb % 8 == 0
-                and out.data_ptr() % 8 == 0 and inp.data_ptr() % 8 == 0
                 and 2 * nb <= self._nvls_ll_half)
 
     def _nvls_ll_red(self, inp: torch.Tensor, out: torch.Tensor) -> bool:
@@ -368,7 +390,6 @@ class ForestCollComm(_CommBase):
         lim = self._nvls_ll_red_max if out is inp else self._nvls_ll_red_max // self.nranks
         return (nb <= lim and nb % 8 == 0
                 and (out.numel() * out.element_size()) % 8 == 0
-                and inp.data_ptr() % 8 == 0 and out.data_ptr() % 8 == 0
                 and 2 * nb * self.nranks <= self._nvls_ll_half)
 
     def _in_pool(self, t) -> bool:
@@ -443,12 +464,7 @@ class ForestCollComm(_CommBase):
         The path is the same on every rank, the local registration state need
         not be: ranks agree (one host all-gather, only on that path, i.e. for
         messages above the LL128 limit) and register together."""
-        if self.nranks == 1:
-            return
-        path = ctypes.c_int()
-        _lib.check(self._lib.fc_call_path(self._comm, COLL_CODE[collective], count, code,
-                                          ctypes.byref(path)), self._comm, "call_path")
-        if path.value != 0:
+        if self.nranks == 1 or self._call_path(collective, count, code) != 0:
             return
         have = ctypes.c_int()
         _lib.check(self._lib.fc_buffer_query(self._comm, out.data_ptr(),
@@ -456,6 +472,20 @@ class ForestCollComm(_CommBase):
                    self._comm, "buffer_query")
         if any(self._allgather_obj(not have.value)):
             self.register(out)
+
+    def _call_path(self, collective: str, count: int, code: int) -> int:
+        """fc_call_path: 0 chunk flags, 1 LL128, 4 one-hop / one-shot, -1 empty."""
+        self.plan(collective)
+        path = ctypes.c_int()
+        _lib.check(self._lib.fc_call_path(self._comm, COLL_CODE[collective], count, code,
+                                          ctypes.byref(path)), self._comm, "call_path")
+        return path.value
+
+    def _switch_order(self, order) -> bool:
+        order = self.reduction_order if order is None else order
+        if order not in ("tree", "switch"):
+            raise InvalidArgument("order must be 'tree' or 'switch'")
+        return order == "switch"
 
     def registration_count(self) -> int:
         """Live peer registrations (one per allocator segment, never per tensor)."""
@@ -483,9 +513,12 @@ class ForestCollComm(_CommBase):
         count, code = _dtype_args(inp, inp.numel())
         if (self._in_pool(out) or self._nvls_ll(out, inp)) and self._switch_capable("multicast"):
             self.schedule(ALLGATHER)
-            _lib.check(self._lib.fc_nvls_allgather(self._comm, inp.data_ptr(), out.data_ptr(),
+            src, dst = _aligned(inp), _aligned(out)
+            _lib.check(self._lib.fc_nvls_allgather(self._comm, src.data_ptr(), dst.data_ptr(),
                                                    count, code, self._stream()),
                        self._comm, "nvls_allgather")
+            if dst is not out:
+                out.copy_(dst)
             return out
         self.plan(ALLGATHER)
         self._ensure_registered(ALLGATHER, out, count, code)
@@ -495,20 +528,31 @@ class ForestCollComm(_CommBase):
 
     all_gather_into_tensor = all_gather
 
-    def reduce_scatter(self, out: torch.Tensor, inp: torch.Tensor, op="sum") -> torch.Tensor:
-        """out = sum over ranks of inp[rank*S:(rank+1)*S] (reduce_scatter_tensor)."""
+    def reduce_scatter(self, out: torch.Tensor, inp: torch.Tensor, op="sum",
+                       order=None) -> torch.Tensor:
+        """out = sum over ranks of inp[rank*S:(rank+1)*S] (reduce_scatter_tensor).
+
+        `order` ("tree" / "switch", default the communicator's
+        reduction_order): "switch" lets an input in the NVLS pool be reduced
+        inside the NVSwitch, in the switch's summation order."""
         self._check_tensor(inp, self.device, "input")
         self._check_tensor(out, self.device, "output")
         if out.dtype != inp.dtype or inp.numel() != out.numel() * self.nranks:
             raise InvalidArgument("input must hold world_size x output elements of the same dtype")
         if inp.dtype not in REDUCIBLE:
             raise Unsupported(f"dtype {inp.dtype} cannot be reduced")
-        if (self._in_pool(inp) or self._nvls_ll_red(inp, out)) and self._switch_capable("aggregation"):
+        switch = self._switch_order(order) and self._in_pool(inp)
+        if (switch or self._nvls_ll_red(inp, out)) and self._switch_capable("aggregation"):
             self.plan(REDUCE_SCATTER)  # the LL path evaluates the plan's in-trees
+            src, dst = (inp, out) if switch else (_aligned(inp), _aligned(out))
             _lib.check(self._lib.fc_nvls_reduce_scatter(
-                self._comm, inp.data_ptr(), out.data_ptr(), out.numel(), DTYPE_CODE[inp.dtype],
+                self._comm, src.data_ptr(), dst.data_ptr(), out.numel(), DTYPE_CODE[inp.dtype],
                 _op_code(op), self._stream()), self._comm, "nvls_reduce_scatter")
+            if dst is not out:
+                out.copy_(dst)
+            self._last_order = "switch" if switch else "tree"
             return out
+        self._last_order = "tree"
         self.plan(REDUCE_SCATTER)
         _lib.check(self._lib.fc_reduce_scatter(self._comm, inp.data_ptr(), out.data_ptr(),
                                                out.numel(), DTYPE_CODE[inp.dtype], _op_code(op),
@@ -517,8 +561,11 @@ class ForestCollComm(_CommBase):
 
     reduce_scatter_tensor = reduce_scatter
 
-    def all_reduce(self, buf: torch.Tensor, op="sum", out: torch.Tensor | None = None) -> torch.Tensor:
-        """In-place (or into `out`) sum over ranks."""
+    def all_reduce(self, buf: torch.Tensor, op="sum", out: torch.Tensor | None = None,
+                   order=None) -> torch.Tensor:
+        """In-place (or into `out`) sum over ranks.  `order` as in
+        reduce_scatter: "switch" (opt-in) reduces NVLS-pool buffers inside
+        the NVSwitch; "tree" (default) keeps the forest's order everywhere."""
         out = buf if out is None else out
         self._check_tensor(buf, self.device, "buffer")
         self._check_tensor(out, self.device, "output")
@@ -526,12 +573,26 @@ class ForestCollComm(_CommBase):
             raise InvalidArgument("output must match the buffer")
         if buf.dtype not in REDUCIBLE:
             raise Unsupported(f"dtype {buf.dtype} cannot be reduced")
-        if (out is buf and (self._in_pool(buf) or self._nvls_ll_red(buf, buf))
+        switch = self._switch_order(order) and self._in_pool(buf)
+        if (out is buf and (switch or self._nvls_ll_red(buf, buf))
                 and self._switch_capable("multicast") and self._switch_capable("aggregation")):
             self.plan(ALLREDUCE)  # the LL path evaluates the plan's in-trees
-            _lib.check(self._lib.fc_nvls_allreduce(self._comm, buf.data_ptr(), buf.numel(),
+            b2 = buf if switch else _aligned(buf)
+            _lib.check(self._lib.fc_nvls_allreduce(self._comm, b2.data_ptr(), buf.numel(),
                                                    DTYPE_CODE[buf.dtype], _op_code(op),
                                                    self._stream()), self._comm, "nvls_allreduce")
+            if b2 is not buf:
+                buf.copy_(b2)
+            self._last_order = "switch" if switch else "tree"
+            return out
+        self._last_order = "tree"
+        if self._in_pool(out) and self._call_path(ALLREDUCE, buf.numel(), DTYPE_CODE[buf.dtype]) == 0:
+            # tree order on a pool tensor at chunk-flag sizes: peers store into
+            # the output, which must be IPC-registrable (the pool's VMM memory
+            # is not) -- run into an ordinary buffer and copy back
+            tmp = torch.empty_like(out)
+            self.all_reduce(buf, op=op, out=tmp, order="tree")
+            out.copy_(tmp)
             return out
         self.plan(ALLREDUCE)
         self._ensure_registered(ALLREDUCE, out, buf.numel(), DTYPE_CODE[buf.dtype])
@@ -594,6 +655,7 @@ class VirtualComm(_CommBase):
         return outs
 
     def reduce_scatter(self, outs, inps, op="sum"):
+        self._last_order = "tree"
         for o, i in zip(outs, inps):
             if o.dtype != i.dtype or i.numel() != o.numel() * self.nranks or o.numel() != outs[0].numel():
                 raise InvalidArgument("each input must hold nranks x output elements")
@@ -606,6 +668,7 @@ class VirtualComm(_CommBase):
         return outs
 
     def all_reduce(self, bufs, op="sum", outs=None):
+        self._last_order = "tree"
         outs = bufs if outs is None else outs
         for o, b in zip(outs, bufs):
             if o.dtype != b.dtype or o.numel() != b.numel() or b.numel() != bufs[0].numel():
@@ -716,6 +779,7 @@ class MultiRankComm(_CommBase):
         return outs
 
     def reduce_scatter(self, outs, inps, op="sum"):
+        self._last_order = "tree"
         self.plan(REDUCE_SCATTER)
         _lib.check(self._lib.fc_reduce_scatter_multi(
             self._comm, self._ptrs(inps, "input"), self._ptrs(outs, "output"), outs[0].numel(),
@@ -723,6 +787,7 @@ class MultiRankComm(_CommBase):
         return outs
 
     def all_reduce(self, bufs, op="sum"):
+        self._last_order = "tree"
         self.plan(ALLREDUCE)
         self._register(bufs, ALLREDUCE, bufs[0].numel(), DTYPE_CODE[bufs[0].dtype])
         _lib.check(self._lib.fc_allreduce_multi(

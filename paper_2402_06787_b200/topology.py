@@ -49,22 +49,26 @@ def nvswitch_doc(n: int, bandwidth: int = 900, multicast: bool = False) -> dict:
     return {"nodes": nodes, "links": links}
 
 
-def groups_switch_doc(beta: int, port: int = 900) -> dict:
-    """Sparse stress topology: 8 GPUs in two groups
-    of 4 (switches swA: g0-g3, swB: g4-g7) joined only by the bridge pairs
-    (g0,g4) and (g1,g5) at `beta` each way.  Bridge GPUs keep `port - beta`
-    to their group switch, so every GPU port totals `port` and the graph is
-    Eulerian (topology.py:268-276)."""
+def groups_switch_doc(beta: int, port: int = 900, n: int = 8) -> dict:
+    """Sparse stress topology: n GPUs in two groups
+    of n/2 (switch swA: the first half, swB: the second) joined only by the
+    bridge pairs (g0, g[n/2]) and (g1, g[n/2+1]) at `beta` each way.  Bridge
+    GPUs keep `port - beta` to their group switch, so every GPU port totals
+    `port` and the graph is Eulerian (topology.py:268-276).  n = 8 is
+    BASELINE configs[4]; n = 4 is its 4-GPU analogue (every GPU a bridge)."""
     if not 0 < beta < port:
         raise ValueError("need 0 < beta < port")
-    ids = [compute_id(i, 8) for i in range(8)]
+    if n < 4 or n % 2:
+        raise ValueError("need an even n >= 4")
+    h = n // 2
+    ids = [compute_id(i, n) for i in range(n)]
     nodes = [{"id": g, "kind": "compute"} for g in ids]
     for sw in ("swA", "swB"):
         nodes.append({"id": sw, "kind": "switch", "multicast": False, "aggregation": False})
     links = []
-    bridges = {0: 4, 1: 5, 4: 0, 5: 1}
+    bridges = {0: h, 1: h + 1, h: 0, h + 1: 1}
     for i, g in enumerate(ids):
-        sw = "swA" if i < 4 else "swB"
+        sw = "swA" if i < h else "swB"
         bw = port - beta if i in bridges else port
         links.append({"src": g, "dst": sw, "bandwidth": bw})
         links.append({"src": sw, "dst": g, "bandwidth": bw})

@@ -46,6 +46,8 @@ def topologies():
         out[f"nvs{n}_mc"] = (topology.nvswitch_doc(n, multicast=True), COLLS, True)
     for beta in (450, 300, 100):
         out[f"groups{beta}"] = (topology.groups_switch_doc(beta), COLLS, True)
+    for beta in (450, 300, 100):  # the 4-GPU analogue of configs[4]
+        out[f"groups4_{beta}"] = (topology.groups_switch_doc(beta, n=4), COLLS, True)
     out["fig3a"] = (json.loads(cs.serialize_topology(
         cs.synth_topology("boxes", boxes=2, gpus_per_box=4, intra=10, inter=1))), COLLS, False)
     out["two_node"] = (json.loads(cs.serialize_topology(

@@ -29,7 +29,8 @@ def main():
     dist.init_process_group("nccl", device_id=dev)
     rank, n = dist.get_rank(), dist.get_world_size()
     comm = ForestCollComm(nvswitch_doc(n, multicast=True), rank=rank, world_size=n, device=local,
-                          nvls_bytes=3 << 30, options={"timeout_ms": 20000})
+                          nvls_bytes=3 << 30, options={"timeout_ms": 20000},
+                          reduction_order="switch")
     if not comm.nvls_enabled:
         print(f"NVLS rank {rank} SKIP (no multicast)", flush=True)
         return
@@ -122,6 +123,34 @@ def main():
                 comm.all_reduce(buf, op="avg")
                 if not torch.allclose(buf.double().cpu(), ref / n, rtol=tol, atol=tol):
                     fails.append(f"allreduce avg {dtype} S={S}")
+    # the same pool tensors with order="tree": the forest's order, bit-exact
+    # vs the oracle (the in-switch order is opt-in only)
+    for dtype, name in ((torch.bfloat16, "bfloat16"), (torch.float32, "float32")):
+        for S in (64, 1 << 18, 1 << 22):
+            allin = [torch.empty(n * S).uniform_(-1, 1, generator=g).to(dtype) for _ in range(n)]
+            hs = [x.view(torch.int16).numpy().view(np.uint16) if dtype == torch.bfloat16 else x.numpy()
+                  for x in allin]
+            buf = comm.nvls_empty(n * S, dtype)
+            buf.copy_(allin[rank].to(dev))
+            comm.all_reduce(buf, order="tree")
+            torch.cuda.synchronize()
+            if comm.last_call_info()["order"] != "tree":
+                fails.append(f"tree-order allreduce {name} S={S} reported {comm.last_call_info()}")
+            got = buf.cpu()
+            got = got.view(torch.int16).numpy().view(np.uint16) if dtype == torch.bfloat16 else got.numpy()
+            want = fo.allreduce(comm.schedule("allreduce"), hs, name)[rank]
+            if not np.array_equal(got.view(np.uint8), want.view(np.uint8)):
+                fails.append(f"tree-order allreduce {name} S={S} not bit-exact")
+            inp = comm.nvls_empty(n * S, dtype)
+            inp.copy_(allin[rank].to(dev))
+            out = torch.empty(S, dtype=dtype, device=dev)
+            comm.reduce_scatter(out, inp, order="tree")
+            torch.cuda.synchronize()
+            got = out.cpu()
+            got = got.view(torch.int16).numpy().view(np.uint16) if dtype == torch.bfloat16 else got.numpy()
+            want = fo.reduce_scatter(comm.schedule("reduce_scatter"), hs, name)[rank]
+            if not np.array_equal(got.view(np.uint8), want.view(np.uint8)):
+                fails.append(f"tree-order reduce_scatter {name} S={S} not bit-exact")
     comm.check()
     print(f"NVLS rank {rank} {'OK' if not fails else 'FAIL ' + '; '.join(fails)}", flush=True)
     # timing: NVLS engine vs tree engine on the same sizes

@@ -39,7 +39,7 @@ def main():
     comm = ForestCollComm(nvswitch_doc(n), rank=rank, world_size=n, device=local)
     pool = 2 * args.nvls_max_mib * MIB + 64 * MIB
     nv = ForestCollComm(nvswitch_doc(n, multicast=True), rank=rank, world_size=n, device=local,
-                        scratch_bytes=64 << 20, nvls_bytes=pool)
+                        scratch_bytes=64 << 20, nvls_bytes=pool, reduction_order="switch")
     groups = {"nccl": None}
     for algo in ("Ring", "NVLS"):
         try:
