@@ -637,8 +637,7 @@ def sparse_stress(dist, dev, n, args):
                 fn = lambda: c.all_reduce(o)  # noqa: E731
             ms = timed(fn, max(5, args.steps), 3, dist)
             t = c.t_star(coll, M)
-            out.append({"topology": f"groups_switch({beta}, n={n})", "k": c.schedule(coll).k
-                        if coll != "allreduce" else c.schedule(coll).phases[0].k,
+            out.append({"topology": f"groups_switch({beta}, n={n})", "k": c.schedule(coll).k,
                         "collective": coll, "M_bytes": M, "ms": round(ms, 4),
                         "proto": c.last_call_info()["proto"],
                         "algbw_GBps": round(gbs(M, ms), 2), "graph_t_star_ms": round(t * 1e3, 4),
