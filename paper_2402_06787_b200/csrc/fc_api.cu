@@ -771,8 +771,11 @@ int run_nvls(fc_comm* c, int mode, const void* send, void* buf, void* out, size_
   const size_t usable = c->nvls_bytes - 2 * (size_t)c->nvls_ll_half;  // LL staging on top
   const long long ll_max =
       c->nvls_ll_max >= 0 ? c->nvls_ll_max : std::max<long long>(2LL << 20, N * (512LL << 10));
-  if (mode == 0 && total <= ll_max && shard % 8 == 0 && (uintptr_t)send % 8 == 0 &&
-      (uintptr_t)buf % 8 == 0 && 2LL * shard * N <= c->nvls_ll_half)
+  // Engine choice from rank-uniform values only (sizes, options, plan): every
+  // rank must run the same kernel.  The LL kernels move 8-byte units, so a
+  // rank whose buffers are not 8-byte aligned fails loudly below instead of
+  // silently taking another engine (the Python layer stages such views).
+  if (mode == 0 && total <= ll_max && shard % 8 == 0 && 2LL * shard * N <= c->nvls_ll_half)
     mode = 3;  // LL over multicast: any device buffers
   // small reductions: LL multicast of the whole input + local tree evaluation
   // (needs the forest program of the loaded plan)
@@ -784,9 +787,13 @@ int run_nvls(fc_comm* c, int mode, const void* send, void* buf, void* out, size_
   const Plan& rp = c->plans[mode == 1 ? FC_REDUCE_SCATTER : FC_ALLREDUCE];
   const long long red_lim = mode == 1 ? red_max / N : red_max;
   if ((mode == 1 || mode == 2) && rp.loaded && rp.d_os && total <= red_lim && total % 8 == 0 &&
-      shard % 8 == 0 && (uintptr_t)buf % 8 == 0 && (out == nullptr || (uintptr_t)out % 8 == 0) &&
-      2LL * total * N <= c->nvls_ll_half)
+      shard % 8 == 0 && 2LL * total * N <= c->nvls_ll_half)
     mode = mode == 1 ? 4 : 5;
+  if (mode >= 3 && ((uintptr_t)buf % 8 || (send && (uintptr_t)send % 8) ||
+                    (out && (uintptr_t)out % 8)))
+    return fail(c, FC_ERR_INVALID_ARG,
+                "NVLS LL path: buffers must be 8-byte aligned (the path is chosen from sizes "
+                "alone, equal on every rank)");
   if (mode < 3) {
     if (b < lo || b + (size_t)total > lo + usable)
       return fail(c, FC_ERR_NOT_REGISTERED, "buffer %p is not inside the NVLS pool", buf);

@@ -334,8 +334,8 @@ __device__ void warp_copy(const char* src, char* const* dst, int ndst, long long
   const long long nu = (nbytes - head) / g;
   const long long o2 = off + head;
   switch (g) {
-    case 16: warp_copy_units<uint4, 8>(src, dst, ndst, o2, nu, lane); break;
-    case 8: warp_copy_units<uint2, 8>(src, dst, ndst, o2, nu, lane); break;
+    case 16: warp_copy_units<uint4, 4>(src, dst, ndst, o2, nu, lane); break;
+    case 8: warp_copy_units<uint2, 4>(src, dst, ndst, o2, nu, lane); break;
     case 4: warp_copy_units<unsigned, 8>(src, dst, ndst, o2, nu, lane); break;
     case 2: warp_copy_units<unsigned short, 8>(src, dst, ndst, o2, nu, lane); break;
     default: warp_copy_units<unsigned char, 8>(src, dst, ndst, o2, nu, lane); break;
@@ -389,10 +389,13 @@ struct Ring {
   unsigned seq;
 };
 
-// Copy `nbytes` (16-aligned src/dst, multiple of 16) from src to every dst.
-// Lane 0 issues; bulk store groups stay pending (caller waits before flags).
-__device__ void bulk_copy(Ring& rg, const char* src, char* const* dst, int ndst,
+// Copy `nbytes` (16-aligned src/dst, multiple of 16) from src + off0 to
+// every dst[d] + off0.  Lane 0 issues; bulk store groups stay pending (caller
+// waits before flags).  Pointer arrays live in shared memory (no local-memory
+// copies on any mover path).
+__device__ void bulk_copy(Ring& rg, const char* src, char* const* dst, int ndst, long long off0,
                           long long nbytes, int lane) {
+  src += off0;
   const long long npieces = (nbytes + FC_STAGE - 1) / FC_STAGE;
   if (lane == 0) {
     const unsigned base = rg.seq;
@@ -409,7 +412,7 @@ __device__ void bulk_copy(Ring& rg, const char* src, char* const* dst, int ndst,
       const char* sb = rg.buf + (q % FC_NST) * FC_STAGE;
       const long long off = i * FC_STAGE;
       const unsigned len = (unsigned)((nbytes - off) < FC_STAGE ? (nbytes - off) : FC_STAGE);
-      for (int d = 0; d < ndst; ++d) bulk_store(dst[d] + off, sb, len);
+      for (int d = 0; d < ndst; ++d) bulk_store(dst[d] + off0 + off, sb, len);
       bulk_commit();
       const long long nx = i + FC_NST - 1;
       if (nx < npieces) {
@@ -429,7 +432,8 @@ __device__ void bulk_copy(Ring& rg, const char* src, char* const* dst, int ndst,
 // destination: smem is released as soon as the lanes have read a stage, so
 // outstanding NVLink writes hold no shared memory.
 __device__ void bulk_copy_stg(Ring& rg, const char* src, char* const* dst, int ndst,
-                              long long nbytes, int lane) {
+                              long long off0, long long nbytes, int lane) {
+  src += off0;
   const long long npieces = (nbytes + FC_STAGE - 1) / FC_STAGE;
   const unsigned base = rg.seq;
   if (lane == 0) {
@@ -447,26 +451,37 @@ __device__ void bulk_copy_stg(Ring& rg, const char* src, char* const* dst, int n
     const uint4* sb = reinterpret_cast<const uint4*>(rg.buf + (q % FC_NST) * FC_STAGE);
     const long long off = i * FC_STAGE;
     const int nv = (int)(((nbytes - off) < FC_STAGE ? (nbytes - off) : FC_STAGE) / 16);
-    constexpr int PER = FC_STAGE / 16 / 32;  // vectors per lane per full stage
-    uint4 v[PER];
+    // the stage in halves: 8 vectors per lane in registers (a full stage
+    // would hold 16, pushing the kernel past 255 registers)
+    constexpr int PER = FC_STAGE / 16 / 32 / 2;
 #pragma unroll
-    for (int u = 0; u < PER; ++u)
-      if (lane + 32 * u < nv) v[u] = sb[lane + 32 * u];
-    __syncwarp();
-    if (lane == 0 && i + FC_NST - 1 < npieces) {
-      const long long p = i + FC_NST - 1;
-      const unsigned q2 = base + (unsigned)p;
-      const long long off2 = p * FC_STAGE;
-      const unsigned len2 = (unsigned)((nbytes - off2) < FC_STAGE ? (nbytes - off2) : FC_STAGE);
-      fence_proxy_async_smem();
-      mbar_expect_tx(&rg.bar[q2 % FC_NST], len2);
-      bulk_load(rg.buf + (q2 % FC_NST) * FC_STAGE, src + off2, len2, &rg.bar[q2 % FC_NST]);
-    }
-    for (int d = 0; d < ndst; ++d) {
-      uint4* dp = reinterpret_cast<uint4*>(dst[d] + off);
+    for (int h = 0; h < 2; ++h) {
+      uint4 v[PER];
 #pragma unroll
-      for (int u = 0; u < PER; ++u)
-        if (lane + 32 * u < nv) dp[lane + 32 * u] = v[u];
+      for (int u = 0; u < PER; ++u) {
+        const int j = lane + 32 * (u + PER * h);
+        if (j < nv) v[u] = sb[j];
+      }
+      if (h == 1) {
+        __syncwarp();  // every lane has read the stage: refill it
+        if (lane == 0 && i + FC_NST - 1 < npieces) {
+          const long long p = i + FC_NST - 1;
+          const unsigned q2 = base + (unsigned)p;
+          const long long off2 = p * FC_STAGE;
+          const unsigned len2 = (unsigned)((nbytes - off2) < FC_STAGE ? (nbytes - off2) : FC_STAGE);
+          fence_proxy_async_smem();
+          mbar_expect_tx(&rg.bar[q2 % FC_NST], len2);
+          bulk_load(rg.buf + (q2 % FC_NST) * FC_STAGE, src + off2, len2, &rg.bar[q2 % FC_NST]);
+        }
+      }
+      for (int d = 0; d < ndst; ++d) {
+        uint4* dp = reinterpret_cast<uint4*>(dst[d] + off0 + off);
+#pragma unroll
+        for (int u = 0; u < PER; ++u) {
+          const int j = lane + 32 * (u + PER * h);
+          if (j < nv) dp[j] = v[u];
+        }
+      }
     }
   }
   rg.seq += (unsigned)npieces;
@@ -476,7 +491,8 @@ __device__ void bulk_copy_stg(Ring& rg, const char* src, char* const* dst, int n
 // bulk-loaded into the ring, 32 lanes sum them and store 16-byte vectors.
 template <int DT, bool SC>
 __device__ void bulk_reduce(Ring& rg, const char* const* src, int nsrc, char* const* dst,
-                            int ndst, long long nbytes, int lane, bool scaled, float sc) {
+                            int ndst, long long off0, long long nbytes, int lane, bool scaled,
+                            float sc) {
   const long long seg = (long long)(FC_STAGE / nsrc) & ~15LL;  // bytes per source per piece
   const long long npieces = (nbytes + seg - 1) / seg;
   const unsigned base = rg.seq;
@@ -487,7 +503,8 @@ __device__ void bulk_reduce(Ring& rg, const char* const* src, int nsrc, char* co
       const unsigned len = (unsigned)((nbytes - off) < seg ? (nbytes - off) : seg);
       char* sb = rg.buf + (q % FC_NST) * FC_STAGE;
       mbar_expect_tx(&rg.bar[q % FC_NST], len * nsrc);
-      for (int s = 0; s < nsrc; ++s) bulk_load(sb + s * seg, src[s] + off, len, &rg.bar[q % FC_NST]);
+      for (int s = 0; s < nsrc; ++s)
+        bulk_load(sb + s * seg, src[s] + off0 + off, len, &rg.bar[q % FC_NST]);
     }
   }
   for (long long i = 0; i < npieces; ++i) {
@@ -504,7 +521,7 @@ __device__ void bulk_reduce(Ring& rg, const char* const* src, int nsrc, char* co
         if (scaled) acc.scale(sc);
       }
       const uint4 out = acc.pack();
-      for (int d = 0; d < ndst; ++d) reinterpret_cast<uint4*>(dst[d] + off)[j] = out;
+      for (int d = 0; d < ndst; ++d) reinterpret_cast<uint4*>(dst[d] + off0 + off)[j] = out;
     }
     __syncwarp();
     // refill the stage consumed in iteration i-1 (all lanes passed its __syncwarp)
@@ -517,7 +534,7 @@ __device__ void bulk_reduce(Ring& rg, const char* const* src, int nsrc, char* co
       fence_proxy_async_smem();  // generic reads of the reused stage before async writes
       mbar_expect_tx(&rg.bar[q2 % FC_NST], len2 * nsrc);
       for (int s = 0; s < nsrc; ++s)
-        bulk_load(sb2 + s * seg, src[s] + off2, len2, &rg.bar[q2 % FC_NST]);
+        bulk_load(sb2 + s * seg, src[s] + off0 + off2, len2, &rg.bar[q2 % FC_NST]);
     }
   }
   rg.seq += (unsigned)npieces;
@@ -564,13 +581,11 @@ __device__ void move(Ring& rg, const char* const* src, int ns, char* const* dst,
       const long long head = (long long)((16 - (a0 & 15)) & 15);
       const long long body = (nbytes - head) & ~15LL;
       warp_copy(src[0], dst, nd, 0, head, lane);
-      char* d1[FC_MAXS];
-      for (int d = 0; d < nd; ++d) d1[d] = dst[d] + head;
       if (copy_mode == 0) {
-        bulk_copy(rg, src[0] + head, d1, nd, body, lane);
+        bulk_copy(rg, src[0], dst, nd, head, body, lane);
         used_bulk = true;
       } else {
-        bulk_copy_stg(rg, src[0] + head, d1, nd, body, lane);
+        bulk_copy_stg(rg, src[0], dst, nd, head, body, lane);
       }
       warp_copy(src[0], dst, nd, head + body, nbytes - head - body, lane);
     } else {
@@ -584,14 +599,10 @@ __device__ void move(Ring& rg, const char* const* src, int ns, char* const* dst,
     warp_reduce_scalar<DT, SC>(src, ns, dst, nd, 0, head / esize, lane, scaled, sc);
     const long long body = (nbytes - head) & ~15LL;
     if (body > 0) {
-      const char* s1[FC_MAXS];
-      char* d1[FC_MAXS];
-      for (int s = 0; s < ns; ++s) s1[s] = src[s] + head;
-      for (int d = 0; d < nd; ++d) d1[d] = dst[d] + head;
       if (ns <= 8 && body >= 1024)
-        bulk_reduce<DT, SC>(rg, s1, ns, d1, nd, body, lane, scaled, sc);
+        bulk_reduce<DT, SC>(rg, src, ns, dst, nd, head, body, lane, scaled, sc);
       else
-        warp_reduce_vec<DT, SC>(s1, ns, d1, nd, 0, body / 16, lane, scaled, sc);
+        warp_reduce_vec<DT, SC>(src, ns, dst, nd, head, body / 16, lane, scaled, sc);
     }
     const long long t0 = head + body;
     warp_reduce_scalar<DT, SC>(src, ns, dst, nd, t0, (nbytes - t0) / esize, lane, scaled, sc);
@@ -605,6 +616,18 @@ struct ItemShared {
   int item;
   int ok;
 };
+// Per-warp source / destination pointer tables of the current item.
+struct ItemPtrs {
+  const char* src[FC_WPC][FC_MAXS];
+  char* dst[FC_WPC][FC_MAXS];
+};
+// Append `val` to a shared pointer table (lane 0 stores, every lane counts).
+#define FC_PUT(arr, cnt, val)        \
+  do {                               \
+    auto fc_v_ = (val);              \
+    if (lane == 0) (arr)[(cnt)] = fc_v_; \
+    ++(cnt);                         \
+  } while (0)
 
 // One item (task, chunk) executed by the whole CTA: thread 0 waits for the
 // inputs, every warp moves a 128-byte-aligned 1/FC_WW sub-range through its
@@ -612,7 +635,7 @@ struct ItemShared {
 template <int DT, int WW, bool AVG>
 __device__ void run_item(const FcParams& P, int me, FcCtl* ctl, const int* T, int c,
                          unsigned e, int w, int lane, unsigned& ready_mask, Ring& rg,
-                         ItemShared* sh, unsigned long long& t_ready,
+                         ItemShared* sh, ItemPtrs* ptrs, unsigned long long& t_ready,
                          unsigned long long& t_moved) {
   const int kind = __ldg(T + TW_KIND);
   const int t = __ldg(T + TW_TREE);
@@ -675,30 +698,35 @@ __device__ void run_item(const FcParams& P, int me, FcCtl* ctl, const int* T, in
   long long s0 = b0 + (((b1 - b0) * wl / WW) & ~(long long)(FC_ALIGN - 1));
   long long s1 = (wl == WW - 1) ? b1 : b0 + (((b1 - b0) * (wl + 1) / WW) & ~(long long)(FC_ALIGN - 1));
   if (s1 < s0) s1 = s0;
-  const char* src[FC_MAXS];
-  char* dst[FC_MAXS];
+  // this warp's source / destination pointers, in shared memory: filled by
+  // lane 0, read by every lane (no local-memory arrays, no spills)
+  const char** const src = ptrs->src[w];
+  char** const dst = ptrs->dst[w];
   int ns = 0, nd = 0;
   const long long slot_phase = s0 - wbase;
+  __syncwarp();  // the previous item's readers are done with the table
   if (kind == FC_K_AG_ROOT || kind == FC_K_AG_FWD) {
-    src[ns++] = (kind == FC_K_AG_ROOT) ? P.send[me] + (s0 - g.base) : P.recv[me] + s0;
-    if (kind == FC_K_AG_ROOT && !P.root_local_done && P.recv[me] + s0 != src[0])
-      dst[nd++] = P.recv[me] + s0;
-    for (int j = 0; j < n_ag; ++j) dst[nd++] = P.recv[__ldg(T + TW_AG_CHILD + j)] + s0;
+    const char* first = (kind == FC_K_AG_ROOT) ? P.send[me] + (s0 - g.base) : P.recv[me] + s0;
+    FC_PUT(src, ns, first);
+    if (kind == FC_K_AG_ROOT && !P.root_local_done && P.recv[me] + s0 != first)
+      FC_PUT(dst, nd, P.recv[me] + s0);
+    for (int j = 0; j < n_ag; ++j) FC_PUT(dst, nd, P.recv[__ldg(T + TW_AG_CHILD + j)] + s0);
   } else {
-    src[ns++] = P.send[me] + s0;
+    FC_PUT(src, ns, P.send[me] + s0);
     for (int j = 0; j < n_rs; ++j)
-      src[ns++] = P.scratch[me] + P.unit_bytes * __ldg(T + TW_RS_CPREFIX + j) +
-                  2LL * FC_ALIGN * __ldg(T + TW_RS_CSLOT + j) + slot_phase;
+      FC_PUT(src, ns, P.scratch[me] + P.unit_bytes * __ldg(T + TW_RS_CPREFIX + j) +
+                  2LL * FC_ALIGN * __ldg(T + TW_RS_CSLOT + j) + slot_phase);
     if (kind == FC_K_RS_FWD) {
-      dst[nd++] = P.scratch[rs_parent] + P.unit_bytes * __ldg(T + TW_RS_PPREFIX) +
-                  2LL * FC_ALIGN * __ldg(T + TW_RS_PSLOT) + slot_phase;
+      FC_PUT(dst, nd, P.scratch[rs_parent] + P.unit_bytes * __ldg(T + TW_RS_PPREFIX) +
+                  2LL * FC_ALIGN * __ldg(T + TW_RS_PSLOT) + slot_phase);
     } else if (kind == FC_K_RS_ROOT) {
-      dst[nd++] = P.recv[me] + (s0 - g.base);
+      FC_PUT(dst, nd, P.recv[me] + (s0 - g.base));
     } else {  // FC_K_AR_ROOT
-      dst[nd++] = P.recv[me] + s0;
-      for (int j = 0; j < n_ag; ++j) dst[nd++] = P.recv[__ldg(T + TW_AG_CHILD + j)] + s0;
+      FC_PUT(dst, nd, P.recv[me] + s0);
+      for (int j = 0; j < n_ag; ++j) FC_PUT(dst, nd, P.recv[__ldg(T + TW_AG_CHILD + j)] + s0);
     }
   }
+  __syncwarp();  // table complete before any lane reads it
   bool used_bulk = false;
   // AVG: the root scales its fp32 sum once, before the final rounding
   move<DT, AVG>(rg, src, ns, dst, nd, s1 - s0, P.esize, lane, P.copy_mode, used_bulk,
@@ -914,6 +942,7 @@ __global__ void __launch_bounds__(FC_BLOCK, 1) fc_forest_kernel(const __grid_con
   __shared__ __align__(8) uint64_t bars[FC_WPC * FC_NST];
   __shared__ unsigned s_epoch;
   __shared__ ItemShared sh_all[FC_NWK];
+  __shared__ ItemPtrs s_ptrs;
   const int lr = blockIdx.x / P.ctas_per_rank;
   const int me = P.local_rank[lr];
   FcCtl* const ctl = P.ctl[lr];
@@ -984,7 +1013,7 @@ __global__ void __launch_bounds__(FC_BLOCK, 1) fc_forest_kernel(const __grid_con
                           lane, ready_mask, &sh, t_ready);
     else
       run_item<DT, WW, AVG>(P, me, ctl, tasks + (long long)ti * FC_TASK_WORDS, P.c0 + c, e, w, lane,
-                       ready_mask, rg, &sh, t_ready, t_moved);
+                       ready_mask, rg, &sh, &s_ptrs, t_ready, t_moved);
     if (trace && lead) {
       const unsigned idx = atomicAdd(P.trace_count, 1u);
       if (idx < P.trace_cap) {
