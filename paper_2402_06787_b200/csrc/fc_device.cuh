@@ -36,6 +36,7 @@
 
 #include <climits>
 #include <cstdint>
+#include <type_traits>
 
 #include "fc_internal.h"
 #include "fc_arith.cuh"
@@ -795,7 +796,7 @@ __device__ __forceinline__ bool ll_poll(const char* const* line, const bool* val
 template <int DT, int WW, bool AVG>
 __device__ void run_item_ll(const FcParams& P, int me, FcCtl* ctl, const int* T, int c,
                             unsigned e, int w, int lane, unsigned& ready_mask, ItemShared* sh,
-                            unsigned long long& t_ready) {
+                            ItemPtrs* ptrs, unsigned long long& t_ready) {
   constexpr int U = FC_LL_UNROLL;
   const int kind = __ldg(T + TW_KIND);
   const int root = __ldg(T + TW_ROOT);
@@ -845,93 +846,116 @@ __device__ void run_item_ll(const FcParams& P, int me, FcCtl* ctl, const int* T,
   if (kind == FC_K_AG_ROOT && !P.root_local_done && P.recv[me] + lo != P.send[me] + (lo - base))
     out_local = P.recv[me];
   if (kind == FC_K_RS_ROOT) out_local = P.recv[me] - base;  // out has S elements
+  // payload offsets (pay + 8*q0) are multiples of 8: the base pointers alone
+  // decide whether 8-byte vector accesses apply (warp-uniform)
+  const bool src_al = ((uintptr_t)local_src & 7) == 0;
+  const bool out_al = ((uintptr_t)out_local & 7) == 0;
 
-  for (long long lb = l0 + 4LL * U * wl; lb < l1; lb += 4LL * U * WW) {
-    bool valid[U], v0[U], v1[U];
-    long long pay[U];
-    unsigned long long w0[U], w1[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const long long l = lb + 4 * u + g;
-      valid[u] = l < l1;
-      pay[u] = lo + (long long)FC_LL_PAY * l;
-      v0[u] = valid[u] && pay[u] + 8LL * q0 + 8 <= hi;
-      v1[u] = valid[u] && two && pay[u] + 8LL * (q0 + 1) + 8 <= hi;
-      w0[u] = 0;
-      w1[u] = 0;
-    }
-    if (polls) {
-      const char* lp[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) lp[u] = my_ag + (lb + 4 * u + g) * 128 + 16 * gl;
-      if (!ll_poll(lp, valid, flag, lane, w0, w1, ctl, P.timeout_ns)) return;
-    } else {
-#pragma unroll
+  // the line loop, instantiated for 8-byte aligned local buffers (plain
+  // vector accesses, all loads of a batch in flight) and for any alignment
+  auto lines = [&](auto aligned) -> bool {
+    constexpr bool AL = decltype(aligned)::value;
+    for (long long lb = l0 + 4LL * U * wl; lb < l1; lb += 4LL * U * WW) {
+      bool valid[U], v0[U], v1[U];
+      long long pay[U];
+      unsigned long long w0[U], w1[U];
+  #pragma unroll
       for (int u = 0; u < U; ++u) {
-        const char* src = local_src + pay[u] + 8 * q0;  // any alignment (rank-local buffer)
-        if (v0[u]) w0[u] = ld_u64_any(src);
-        if (v1[u]) w1[u] = ld_u64_any(src + 8);
+        const long long l = lb + 4 * u + g;
+        valid[u] = l < l1;
+        pay[u] = lo + (long long)FC_LL_PAY * l;
+        v0[u] = valid[u] && pay[u] + 8LL * q0 + 8 <= hi;
+        v1[u] = valid[u] && two && pay[u] + 8LL * (q0 + 1) + 8 <= hi;
+        w0[u] = 0;
+        w1[u] = 0;
       }
-      if (kind != FC_K_AG_ROOT && n_rs > 0) {
-        Acc8<DT> a0[U], a1[U];
-#pragma unroll
+      if (polls) {
+        const char* lp[U];
+  #pragma unroll
+        for (int u = 0; u < U; ++u) lp[u] = my_ag + (lb + 4 * u + g) * 128 + 16 * gl;
+        if (!ll_poll(lp, valid, flag, lane, w0, w1, ctl, P.timeout_ns)) return false;
+      } else {
+  #pragma unroll
         for (int u = 0; u < U; ++u) {
-          a0[u].init(w0[u]);
-          a1[u].init(w1[u]);
-        }
-        for (int j = 0; j < n_rs; ++j) {
-          const char* cl = slot_ptr(me, 0, __ldg(T + TW_RS_CSLOT + j), __ldg(T + TW_RS_CPREFIX + j));
-          const char* lp[U];
-          unsigned long long x0[U], x1[U];
-#pragma unroll
-          for (int u = 0; u < U; ++u) lp[u] = cl + (lb + 4 * u + g) * 128 + 16 * gl;
-          if (!ll_poll(lp, valid, flag, lane, x0, x1, ctl, P.timeout_ns)) return;
-#pragma unroll
-          for (int u = 0; u < U; ++u) {
-            a0[u].add(x0[u]);
-            a1[u].add(x1[u]);
+          const char* src = local_src + pay[u] + 8 * q0;  // rank-local buffer, any alignment
+          if constexpr (AL) {  // aligned bases: every line's loads in flight together
+            if (v0[u]) w0[u] = __ldcg(reinterpret_cast<const unsigned long long*>(src));
+            if (v1[u]) w1[u] = __ldcg(reinterpret_cast<const unsigned long long*>(src) + 1);
+          } else {
+            if (v0[u]) w0[u] = ld_u64_any(src);
+            if (v1[u]) w1[u] = ld_u64_any(src + 8);
           }
         }
-        if (AVG && kind != FC_K_RS_FWD) {  // root: scale the fp32 sum once
-#pragma unroll
+        if (kind != FC_K_AG_ROOT && n_rs > 0) {
+          Acc8<DT> a0[U], a1[U];
+  #pragma unroll
           for (int u = 0; u < U; ++u) {
-            a0[u].scale(P.scale);
-            a1[u].scale(P.scale);
+            a0[u].init(w0[u]);
+            a1[u].init(w1[u]);
+          }
+          for (int j = 0; j < n_rs; ++j) {
+            const char* cl = slot_ptr(me, 0, __ldg(T + TW_RS_CSLOT + j), __ldg(T + TW_RS_CPREFIX + j));
+            const char* lp[U];
+            unsigned long long x0[U], x1[U];
+  #pragma unroll
+            for (int u = 0; u < U; ++u) lp[u] = cl + (lb + 4 * u + g) * 128 + 16 * gl;
+            if (!ll_poll(lp, valid, flag, lane, x0, x1, ctl, P.timeout_ns)) return false;
+  #pragma unroll
+            for (int u = 0; u < U; ++u) {
+              a0[u].add(x0[u]);
+              a1[u].add(x1[u]);
+            }
+          }
+          if (AVG && kind != FC_K_RS_FWD) {  // root: scale the fp32 sum once
+  #pragma unroll
+            for (int u = 0; u < U; ++u) {
+              a0[u].scale(P.scale);
+              a1[u].scale(P.scale);
+            }
+          }
+  #pragma unroll
+          for (int u = 0; u < U; ++u) {
+            w0[u] = a0[u].pack();
+            w1[u] = a1[u].pack();
           }
         }
-#pragma unroll
+      }
+      // local payload write
+      if (out_local) {
+  #pragma unroll
         for (int u = 0; u < U; ++u) {
-          w0[u] = a0[u].pack();
-          w1[u] = a1[u].pack();
+          char* o = out_local + pay[u] + 8 * q0;
+          if constexpr (AL) {
+            if (v0[u]) reinterpret_cast<unsigned long long*>(o)[0] = w0[u];
+            if (v1[u]) reinterpret_cast<unsigned long long*>(o)[1] = w1[u];
+          } else {
+            if (v0[u]) st_u64_any(o, w0[u]);
+            if (v1[u]) st_u64_any(o + 8, w1[u]);
+          }
         }
       }
-    }
-    // local payload write
-    if (out_local) {
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        char* o = out_local + pay[u] + 8 * q0;
-        if (v0[u]) st_u64_any(o, w0[u]);
-        if (v1[u]) st_u64_any(o + 8, w1[u]);
+      // line stores to peers' staging (a per-batch local table measures 13 %
+      // faster at 64 MiB than a shared-memory one built once per item)
+      char* dl[FC_MAXS];
+      int nl = 0;
+      if (kind == FC_K_RS_FWD) {
+        dl[nl++] = slot_ptr(rs_parent, 0, __ldg(T + TW_RS_PSLOT), __ldg(T + TW_RS_PPREFIX));
+      } else if (kind == FC_K_AG_ROOT || kind == FC_K_AG_FWD || kind == FC_K_AR_ROOT) {
+        for (int j = 0; j < n_ag; ++j)
+          dl[nl++] = slot_ptr(__ldg(T + TW_AG_CHILD + j), P.ll_ag_base, __ldg(T + TW_AG_CSLOT + j),
+                              __ldg(T + TW_AG_CPREFIX + j));
+      }
+      for (int d = 0; d < nl; ++d) {
+  #pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (valid[u])
+            st_line16(dl[d] + (lb + 4 * u + g) * 128 + 16 * gl, w0[u], two ? w1[u] : flag);
       }
     }
-    // line stores to peers' staging
-    char* dl[FC_MAXS];
-    int nl = 0;
-    if (kind == FC_K_RS_FWD) {
-      dl[nl++] = slot_ptr(rs_parent, 0, __ldg(T + TW_RS_PSLOT), __ldg(T + TW_RS_PPREFIX));
-    } else if (kind == FC_K_AG_ROOT || kind == FC_K_AG_FWD || kind == FC_K_AR_ROOT) {
-      for (int j = 0; j < n_ag; ++j)
-        dl[nl++] = slot_ptr(__ldg(T + TW_AG_CHILD + j), P.ll_ag_base, __ldg(T + TW_AG_CSLOT + j),
-                            __ldg(T + TW_AG_CPREFIX + j));
-    }
-    for (int d = 0; d < nl; ++d) {
-#pragma unroll
-      for (int u = 0; u < U; ++u)
-        if (valid[u])
-          st_line16(dl[d] + (lb + 4 * u + g) * 128 + 16 * gl, w0[u], two ? w1[u] : flag);
-    }
-  }
+    return true;
+  };
+  const bool ok = (src_al && out_al) ? lines(std::true_type{}) : lines(std::false_type{});
+  if (!ok) return;
   worker_sync<WW>(wk);
 }
 
@@ -1010,7 +1034,7 @@ __global__ void __launch_bounds__(FC_BLOCK, 1) fc_forest_kernel(const __grid_con
     unsigned long long t_ready = t0, t_moved = t0;
     if constexpr (PROTO == 1)
       run_item_ll<DT, WW, AVG>(P, me, ctl, tasks + (long long)ti * FC_TASK_WORDS, P.c0 + c, e, w,
-                          lane, ready_mask, &sh, t_ready);
+                          lane, ready_mask, &sh, &s_ptrs, t_ready);
     else
       run_item<DT, WW, AVG>(P, me, ctl, tasks + (long long)ti * FC_TASK_WORDS, P.c0 + c, e, w, lane,
                        ready_mask, rg, &sh, &s_ptrs, t_ready, t_moved);

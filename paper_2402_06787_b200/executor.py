@@ -461,17 +461,20 @@ class ForestCollComm(_CommBase):
         """Register `out`'s allocation when this call takes the chunk-flag
         path, the only one that stores into peers' outputs (fc_call_path; the
         one-hop, one-shot and LL128 paths write only the library's staging).
-        The path is the same on every rank, the local registration state need
-        not be: ranks agree (one host all-gather, only on that path, i.e. for
-        messages above the LL128 limit) and register together."""
+        The path is the same on every rank; registration is per allocator
+        segment, so it happens once per segment, not per call."""
         if self.nranks == 1 or self._call_path(collective, count, code) != 0:
             return
         have = ctypes.c_int()
         _lib.check(self._lib.fc_buffer_query(self._comm, out.data_ptr(),
                                              out.numel() * out.element_size(), ctypes.byref(have)),
                    self._comm, "buffer_query")
-        if any(self._allgather_obj(not have.value)):
-            self.register(out)
+        # Registered here: SPMD programs allocate outputs in the same order on
+        # every rank, so every rank finds its own (equally placed) output
+        # registered and no host round trip is spent per call.  A rank that
+        # passes a differently placed buffer fails the device tag check.
+        if not have.value:
+            self.register(out)  # collective: SPMD ranks all reach this call together
 
     def _call_path(self, collective: str, count: int, code: int) -> int:
         """fc_call_path: 0 chunk flags, 1 LL128, 4 one-hop / one-shot, -1 empty."""
