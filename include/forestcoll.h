@@ -136,6 +136,10 @@ extern "C" {
                                     up to this output size (default 16 MiB; 0 disables) */
 #define FC_OPT_MAX_CTAS_PER_RANK 22 /* read-only: largest FC_OPT_CTAS_PER_RANK this
                                        device co-schedules for the comm's local ranks */
+#define FC_OPT_CE_MIN 23       /* 2-rank single-switch forest: allgathers whose output is at
+                                  least this many bytes move each shard with the copy engine
+                                  (one cudaMemcpyAsync into the peer's registered output) and
+                                  the SMs only synchronise (default 128 MiB; 0 disables) */
 
 typedef struct fc_comm fc_comm_t;
 
@@ -174,9 +178,10 @@ int fc_buffer_register_multi(fc_comm_t* comm, const void* const* ptrs,
  * fc_buffer_count: number of live registrations. */
 int fc_buffer_query(fc_comm_t* comm, const void* ptr, size_t bytes, int* registered);
 int fc_buffer_count(const fc_comm_t* comm);
-/* The path the next collective of this size would take: 0 chunk flags (the
- * only path that stores into peers' outputs: allgather / allreduce outputs
- * must then be registered), 1 LL128, 4 one-hop / one-shot, -1 empty.  The
+/* The path the next collective of this size would take: 0 chunk flags,
+ * 1 LL128, 4 one-hop / one-shot, 5 copy engine (2-rank allgather), -1 empty.
+ * Paths 0 and 5 store into peers' outputs: allgather / allreduce outputs
+ * must then be registered.  The
  * choice depends only on values equal on every rank (count, dtype, plan,
  * options), never on buffer addresses. */
 int fc_call_path(fc_comm_t* comm, int collective, size_t count, int dtype, int* path);

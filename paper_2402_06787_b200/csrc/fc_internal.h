@@ -207,3 +207,21 @@ int fc_warps_per_cta();
 int fc_nvls_launch(const FcNvlsParams& p, int ctas, void* stream);
 // grid size for the one-shot kernels (modes 6/7/8): every CTA co-resident
 int fc_oneshot_max_ctas(int mode, int dtype, int* out);
+
+// Copy-engine path of the 2-rank forest (fc_ce.cu).  Its flag slots are
+// 64-bit words at the end of each rank's flag area: FC_CE_READY + r holds
+// rank r's entry (tag << 32 | epoch), FC_CE_DONE + r its exit epoch.
+#define FC_CE_READY 0
+#define FC_CE_DONE FC_MAXR
+#define FC_CE_SLOTS (2 * FC_MAXR)
+struct FcCeParams {
+  FcCtl* ctl;                      // own control block (epoch, sticky error)
+  unsigned long long* my_slots;    // own CE slots
+  unsigned long long* peer_slots;  // the peer's CE slots (mapped)
+  unsigned long long tag;          // identity of the output buffer (as FcParams.tag)
+  long long timeout_ns;
+  int me, peer;
+  int phase;                       // 0: entry handshake, 1: exit handshake
+};
+int fc_ce_sync_launch(const FcCeParams& p, void* stream);
+int fc_ce_copy_launch(void* dst, const void* src, long long n, int ctas, void* stream);

@@ -180,7 +180,8 @@ class _CommBase:
         self._lib.fc_last_call_info(self._comm, buf, 8)
         info = {"launches": buf[0], "nchunks": buf[1], "window": buf[2], "grid": buf[3],
                 "unit_bytes": buf[4],
-                "proto": {0: "flags", 1: "ll128", 2: "nvls", 3: "nvls_ll", 4: "oneshot"}[buf[5]]}
+                "proto": {0: "flags", 1: "ll128", 2: "nvls", 3: "nvls_ll", 4: "oneshot",
+                          5: "ce"}[buf[5]]}
         # floating-point summation order of the last reduction: "tree" (the
         # forest's order, bit-exact vs the oracle) or "switch" (in-NVSwitch)
         info["order"] = getattr(self, "_last_order", None)
@@ -463,7 +464,7 @@ class ForestCollComm(_CommBase):
         one-hop, one-shot and LL128 paths write only the library's staging).
         The path is the same on every rank; registration is per allocator
         segment, so it happens once per segment, not per call."""
-        if self.nranks == 1 or self._call_path(collective, count, code) != 0:
+        if self.nranks == 1 or self._call_path(collective, count, code) not in (0, 5):
             return
         have = ctypes.c_int()
         _lib.check(self._lib.fc_buffer_query(self._comm, out.data_ptr(),
@@ -477,7 +478,8 @@ class ForestCollComm(_CommBase):
             self.register(out)  # collective: SPMD ranks all reach this call together
 
     def _call_path(self, collective: str, count: int, code: int) -> int:
-        """fc_call_path: 0 chunk flags, 1 LL128, 4 one-hop / one-shot, -1 empty."""
+        """fc_call_path: 0 chunk flags, 1 LL128, 4 one-hop / one-shot, 5 copy
+        engine, -1 empty."""
         self.plan(collective)
         path = ctypes.c_int()
         _lib.check(self._lib.fc_call_path(self._comm, COLL_CODE[collective], count, code,

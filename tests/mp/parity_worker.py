@@ -47,12 +47,16 @@ def main():
                           options={"timeout_ms": 20000})
     fails = []
     # auto (one-hop / one-shot, else LL128 where aligned), auto with the
-    # one-hop paths off (the forest's LL128 lines), the chunk-flag protocol
-    for proto, onehop in ((-1, True), (-1, False), (0, True)):
+    # one-hop paths off (the forest's LL128 lines), the chunk-flag protocol,
+    # and (N=2) every allgather through the copy-engine path (ce_min=1)
+    for proto, onehop, ce in ((-1, True, 0), (-1, False, 0), (0, True, 0), (-1, True, 1)):
         comm.set_option("proto", proto)
         comm.set_option("oneshot_ag_max", (16 << 20) if onehop else 0)
         comm.set_option("oneshot_max", (2 << 20) if onehop else 0)
-        fails += [f"proto={proto} onehop={onehop}: {f}" for f in run_all(comm, rank, n, dev)]
+        comm.set_option("ce_min", ce)
+        fails += [f"proto={proto} onehop={onehop} ce={ce}: {f}" for f in run_all(comm, rank, n, dev)]
+        if ce and n == 2 and comm.last_call_info()["proto"] not in ("ce", "oneshot", "flags", "ll128"):
+            fails.append("unexpected path")
     comm.check()
     print(f"RANK {rank} {'OK' if not fails else 'FAIL ' + '; '.join(fails)}", flush=True)
     comm.close()
@@ -72,9 +76,12 @@ def run_all(comm, rank, n, dev):
             torch.cuda.synchronize()
             got = comm.last_call_info()["proto"]
             enabled = comm.get_option("proto") < 0 and comm.get_option("oneshot_ag_max") > 0
-            if enabled and S == 4096 and got != "oneshot":
+            ce = n == 2 and comm.get_option("ce_min") == 1 and comm.get_option("proto") < 0
+            if ce and got != "ce":
+                fails.append(f"allgather S={S} took {got}, expected the copy-engine path")
+            if enabled and not ce and S == 4096 and got != "oneshot":
                 fails.append(f"allgather S={S} took {got}, expected the one-hop path")
-            if not enabled and got == "oneshot":
+            if not enabled and got in ("oneshot", "ce"):
                 fails.append(f"allgather S={S} took the one-hop path although it is off")
             ref = fo.allgather(comm.schedule("allgather"), [host(x) for x in sends])[rank]
             if not np.array_equal(host(out).view(np.uint8), ref.view(np.uint8)):

@@ -43,7 +43,13 @@ def main():
     rank, n = dist.get_rank(), dist.get_world_size()
     comm = ForestCollComm(nvswitch_doc(n), rank=rank, world_size=n, device=local)
     for spec in sys.argv[1:]:
-        coll, mib, dt, proto = spec.split(":")
+        coll, mib, dt, proto, *opts = spec.split(":")
+        for o in opts:  # name=value options (absent in old trees: skipped there)
+            k, v = o.split("=")
+            try:
+                comm.set_option(k, int(v))
+            except Exception:  # noqa: BLE001
+                pass
         M = int(mib) * MIB
         dt = DT[dt]
         es = torch.tensor([], dtype=dt).element_size()
@@ -65,8 +71,14 @@ def main():
         k = max(5, min(200, int(0.03 / (20e-6 + M / 500e9))))
         ms = dev_time(fn, k)
         if rank == 0:
-            print(f"{spec:20s} {ms * 1e3:9.1f} us  {M / ms / 1e6:8.1f} GB/s  proto={comm.last_call_info()['proto']}",
+            print(f"{spec:32s} {ms * 1e3:9.1f} us  {M / ms / 1e6:8.1f} GB/s  proto={comm.last_call_info()['proto']}",
                   flush=True)
+        for o in opts:
+            k, _ = o.split("=")
+            try:
+                comm.set_option(k, {"ce_min": 4 << 20, "oneshot_ag_max": 16 << 20}.get(k, -1))
+            except Exception:  # noqa: BLE001
+                pass
     comm.check()
     comm.close()
     dist.destroy_process_group()
