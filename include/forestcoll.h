@@ -185,6 +185,17 @@ int fc_buffer_count(const fc_comm_t* comm);
  * choice depends only on values equal on every rank (count, dtype, plan,
  * options), never on buffer addresses. */
 int fc_call_path(fc_comm_t* comm, int collective, size_t count, int dtype, int* path);
+/* Workspace sizing.  fc_call_scratch: the scratch_bytes (per region, see
+ * "Workspace" above) the path this call would take with a workspace of `cap`
+ * bytes per region needs -- 0 when it needs none.  fc_comm_grow: re-allocate
+ * every local workspace with scratch_bytes per region; collective (all ranks,
+ * same value, after all their collectives on this communicator completed),
+ * and followed by fc_comm_export / fc_comm_connect.  The Python layer starts
+ * small and grows on demand up to a cap (executor.ForestCollComm). */
+int fc_call_scratch(fc_comm_t* comm, int collective, size_t count, int dtype, size_t cap,
+                    size_t* bytes);
+size_t fc_comm_scratch_bytes(const fc_comm_t* comm);
+int fc_comm_grow(fc_comm_t* comm, size_t scratch_bytes);
 
 int fc_plan_load(fc_comm_t* comm, int collective, const int32_t* table,
                  size_t nwords);

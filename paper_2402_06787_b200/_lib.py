@@ -75,6 +75,9 @@ SIGNATURES = {
     "fc_buffer_query": (_I, [_P, _P, _SZ, ctypes.POINTER(_I)]),
     "fc_buffer_count": (_I, [_P]),
     "fc_call_path": (_I, [_P, _I, _SZ, _I, ctypes.POINTER(_I)]),
+    "fc_call_scratch": (_I, [_P, _I, _SZ, _I, _SZ, ctypes.POINTER(_SZ)]),
+    "fc_comm_scratch_bytes": (_SZ, [_P]),
+    "fc_comm_grow": (_I, [_P, _SZ]),
     "fc_plan_load": (_I, [_P, _I, ctypes.POINTER(ctypes.c_int32), _SZ]),
     "fc_allgather": (_I, [_P, _P, _P, _SZ, _I, _P]),
     "fc_reduce_scatter": (_I, [_P, _P, _P, _SZ, _I, _I, _P]),

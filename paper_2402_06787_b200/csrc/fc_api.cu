@@ -437,7 +437,8 @@ int run_ce_ag(fc_comm* c, const void* send, void* recv, long long shard_bytes, v
 // only decide: store the path the call would take (0 chunk flags, 1 LL128,
 // 4 one-hop / one-shot) and launch nothing (fc_call_path).
 int run(fc_comm* c, int coll, const void* const* sends, void* const* recvs, size_t count,
-        int dtype, int op, void* stream, int* path_out = nullptr) {
+        int dtype, int op, void* stream, int* path_out = nullptr, long long scratch_cap = 0,
+        long long* scratch_need = nullptr) {
   if (!c) return FC_ERR_INVALID_ARG;
   if (!c->virt && !c->connected)
     return fail(c, FC_ERR_INVALID_ARG, "communicator is not connected (fc_comm_connect)");
@@ -476,7 +477,16 @@ int run(fc_comm* c, int coll, const void* const* sends, void* const* recvs, size
   // Every choice below depends only on values that are equal on every rank
   // (sizes, dtype, plan, options): ranks must run the same kernel.  Local
   // buffer alignment is handled inside the kernels (ld_u64_any/st_u64_any).
-  const long long half = (long long)(c->scratch_bytes / 2) / 4096 * 4096;
+  // scratch_need (fc_call_scratch): decide as if the workspace held
+  // scratch_cap bytes per region and report what the chosen path needs
+  const long long scratch = scratch_need ? scratch_cap : (long long)c->scratch_bytes;
+  const long long half = scratch / 2 / 4096 * 4096;
+  auto decided = [&](int path, long long need) {
+    *path_out = path;
+    if (scratch_need) *scratch_need = need;
+    return FC_SUCCESS;
+  };
+  if (scratch_need) *scratch_need = 0;
   const bool onehop = (pl.flags & FC_PLAN_ONEHOP) != 0 && c->proto < 0;
   // 2-rank single-switch forest: each tree is one edge, moved by the copy
   // engine (fc_ce.cu) from ce_min output bytes (the peer's output must be
@@ -486,7 +496,7 @@ int run(fc_comm* c, int coll, const void* const* sends, void* const* recvs, size
     // +10 % at 256 MiB, +9 % at 1 GiB, +12 % at 4 GiB (0.855 of T*)
     const long long lim = c->ce_min > 0 ? c->ce_min : (128LL << 20);
     if (total * es >= lim) {
-      if (path_out) return *path_out = 5, FC_SUCCESS;
+      if (path_out) return decided(5, 0);
       return run_ce_ag(c, sends[0], recvs[0], S * es, stream);
     }
   }
@@ -499,7 +509,7 @@ int run(fc_comm* c, int coll, const void* const* sends, void* const* recvs, size
     const long long lim = c->oneshot_ag_max > 0 ? c->oneshot_ag_max : (16LL << 20);
     const long long lines = (S * es + 119) / 120;
     if (bytes <= lim && (S * es) % 8 == 0 && (long long)N * lines * 128 <= half) {
-      if (path_out) return *path_out = 4, FC_SUCCESS;
+      if (path_out) return decided(4, 2 * (long long)N * lines * 128);
       return run_oneshot_ag(c, sends, recvs, S * es, half, stream);
     }
   }
@@ -512,7 +522,7 @@ int run(fc_comm* c, int coll, const void* const* sends, void* const* recvs, size
     const long long lines = (bytes + 119) / 120;
     if (bytes <= (coll == FC_REDUCE_SCATTER ? 2 * lim / N : lim) && bytes % 8 == 0 &&
         (S * es) % 8 == 0 && (long long)N * lines * 128 <= half) {
-      if (path_out) return *path_out = 4, FC_SUCCESS;
+      if (path_out) return decided(4, 2 * (long long)N * lines * 128);
       return run_oneshot(c, coll, pl, sends, recvs, S, total, es, rd, op, half, stream);
     }
   }
@@ -589,10 +599,11 @@ int run(fc_comm* c, int coll, const void* const* sends, void* const* recvs, size
     // the LL region (scratch_bytes) is two halves used by alternate epochs
     if (aligned && want && need <= half) {
       proto = 1;
+      if (scratch_need) *scratch_need = 2 * need;
       n = std::min<long long>(chunks_for(c->ll_chunk_max, c->ll_worker_warps), kMaxC);
       W = n;
       P.ll_unit_bytes = llu;
-      P.ll_region_off = (long long)c->scratch_bytes;
+      P.ll_region_off = scratch;
       P.ll_half = half;
       P.ll_ag_base = ag_base;
       P.worker_warps = c->ll_worker_warps;
@@ -617,15 +628,16 @@ int run(fc_comm* c, int coll, const void* const* sends, void* const* recvs, size
       auto need = [&](long long w) {
         return (long long)pl.max_slot_units * unit_for(w) + 2LL * FC_ALIGN * pl.max_slots;
       };
-      while (W > 1 && need(W) > (long long)c->scratch_bytes) W = std::max(1LL, W / 2);
-      if (need(W) > (long long)c->scratch_bytes)
+      while (W > 1 && need(W) > scratch) W = std::max(1LL, W / 2);
+      if (scratch_need) *scratch_need = need(W);
+      if (need(W) > scratch && !scratch_need)
         return fail(c, FC_ERR_INVALID_ARG,
                     "scratch too small: %lld bytes needed per window, %zu available",
                     need(W), c->scratch_bytes);
       P.unit_bytes = unit_for(W);
     }
   }
-  if (path_out) return *path_out = proto, FC_SUCCESS;
+  if (path_out) return decided(proto, scratch_need ? *scratch_need : 0);
   P.nchunks = (int)n;
   P.proto = proto;
   // the chunk-flag protocol stores into peers' outputs (AG recv, AR buf):
@@ -1383,6 +1395,57 @@ int fc_call_path(fc_comm_t* c, int collective, size_t count, int dtype, int* pat
   const void* no_sends[FC_MAXR] = {};  // decide only: run() touches no buffer
   void* no_recvs[FC_MAXR] = {};
   return run(c, collective, no_sends, no_recvs, count, dtype, FC_SUM, nullptr, path);
+}
+
+int fc_call_scratch(fc_comm_t* c, int collective, size_t count, int dtype, size_t cap,
+                    size_t* bytes) {
+  if (!c || !bytes || collective < 0 || collective > 2) return FC_ERR_INVALID_ARG;
+  const void* no_sends[FC_MAXR] = {};
+  void* no_recvs[FC_MAXR] = {};
+  int path = -1;
+  long long need = 0;
+  const int st = run(c, collective, no_sends, no_recvs, count, dtype, FC_SUM, nullptr, &path,
+                     (long long)align_up(cap, 4096), &need);
+  *bytes = need > 0 ? align_up((size_t)need, 4096) : 0;
+  return st;
+}
+
+size_t fc_comm_scratch_bytes(const fc_comm_t* c) { return c ? c->scratch_bytes : 0; }
+
+// Re-allocate every local workspace with `scratch_bytes` per region.  All
+// ranks call it together, after every collective that used the old
+// workspaces has completed on every rank (the caller synchronises and
+// barriers); the communicator then needs fc_comm_export / fc_comm_connect
+// again.  Control blocks and flags restart from zero on every rank alike.
+int fc_comm_grow(fc_comm_t* c, size_t scratch_bytes) {
+  if (!c) return FC_ERR_INVALID_ARG;
+  FC_CUDA(c, cudaSetDevice(c->device));
+  FC_CUDA(c, cudaDeviceSynchronize());
+  for (int r = 0; r < c->nranks; ++r) {
+    if (c->is_local[r] || !c->ws[r]) continue;
+    for (size_t i = 0; i < c->maps.size(); ++i)
+      if (c->maps[i].base == c->ws[r]) {
+        cudaIpcCloseMemHandle(c->maps[i].base);
+        c->maps.erase(c->maps.begin() + i);
+        break;
+      }
+    c->ws[r] = nullptr;
+  }
+  for (int r = 0; r < FC_MAXR; ++r)
+    if (c->own[r]) {
+      cudaFree(c->ws[r]);
+      c->ws[r] = nullptr;
+      c->own[r] = false;
+    }
+  setup_layout(c, scratch_bytes);
+  for (int i = 0; i < c->nlocal; ++i) {
+    const int st = alloc_workspace(c, &c->ws[c->local[i]]);
+    if (st) return st;
+    c->own[c->local[i]] = true;
+  }
+  c->have_last = false;
+  c->connected = c->virt || c->nranks == 1;
+  return FC_SUCCESS;
 }
 
 int fc_plan_load(fc_comm_t* c, int coll, const int32_t* t, size_t nwords) {

@@ -42,7 +42,14 @@ REDUCIBLE = {torch.int32, torch.float16, torch.float32, torch.bfloat16}
 if hasattr(torch, "uint32"):
     REDUCIBLE.add(torch.uint32)
 OPS = {"sum": 0, "avg": 4}  # ncclRedOp_t numbering (include/forestcoll.h)
-DEFAULT_SCRATCH = 2 << 30  # per rank: reduction scratch + LL128 staging
+# Per-rank workspace: two regions of scratch_bytes (reduction scratch and the
+# LL128 staging).  ForestCollComm starts at INITIAL_SCRATCH (enough for the
+# one-hop / one-shot paths) and grows on demand, collectively, up to
+# MAX_SCRATCH (fc_call_scratch / fc_comm_grow); an explicit scratch_bytes
+# fixes the size.
+INITIAL_SCRATCH = 64 << 20
+MAX_SCRATCH = 2 << 30
+DEFAULT_SCRATCH = None
 VIRTUAL_SCRATCH = 1 << 30
 
 
@@ -159,6 +166,8 @@ class _CommBase:
     def set_option(self, name: str, value: int) -> None:
         _lib.check(self._lib.fc_comm_set_option(self._comm, _lib.OPTIONS[name], int(value)),
                    self._comm, f"set_option({name})")
+        if hasattr(self, "_scratch_ok"):
+            self._scratch_ok.clear()  # options change paths (and their workspace needs)
         if name == "nvls_ll_max":
             self._nvls_ll_max = int(value)
         if name == "nvls_ll_red_max":
@@ -243,7 +252,8 @@ class ForestCollComm(_CommBase):
 
     def __init__(self, topology=None, *, rank=None, world_size=None, device=None, group=None,
                  scratch_bytes=DEFAULT_SCRATCH, schedules=None, validate=True, prune=True,
-                 options=None, nvls_bytes=0, reduction_order="tree"):
+                 options=None, nvls_bytes=0, reduction_order="tree",
+                 max_scratch_bytes=MAX_SCRATCH):
         import torch.distributed as dist
 
         if reduction_order not in ("tree", "switch"):
@@ -276,24 +286,75 @@ class ForestCollComm(_CommBase):
         if self.topology_source == "nvml" and not schedules:
             doc = self._usable_topology(doc, world_size)
         super().__init__(doc, world_size, schedules, validate, prune)
+        # workspace: fixed when scratch_bytes is given, else grown on demand
+        self._grow = scratch_bytes is None
+        self._max_scratch = int(max_scratch_bytes)
+        self._scratch_ok = set()  # (collective, count, dtype) needing no growth
         comm = ctypes.c_void_p()
-        _lib.check(self._lib.fc_comm_init(rank, world_size, device, int(scratch_bytes),
-                                          ctypes.byref(comm)), None, "fc_comm_init")
+        init = INITIAL_SCRATCH if scratch_bytes is None else int(scratch_bytes)
+        _lib.check(self._lib.fc_comm_init(rank, world_size, device, init, ctypes.byref(comm)),
+                   None, "fc_comm_init")
         self._comm = comm
         for name, value in (options or {}).items():
             self.set_option(name, value)
-        if world_size > 1:
-            hb = self._lib.fc_handle_bytes()
-            mine = ctypes.create_string_buffer(hb)
-            _lib.check(self._lib.fc_comm_export(self._comm, mine), self._comm, "comm_export")
-            allh = self._allgather_obj(mine.raw)
-            blob = ctypes.create_string_buffer(b"".join(allh), hb * world_size)
-            _lib.check(self._lib.fc_comm_connect(self._comm, blob), self._comm, "comm_connect")
+        self._connect()
         self._nvls_base = None
         self._nvls_bytes = 0
         self._nvls_next = 0
         if nvls_bytes and world_size > 1:
             self._setup_nvls(int(nvls_bytes))
+
+    def _connect(self):
+        """Exchange workspace handles and map the peers' (collective)."""
+        if self.nranks == 1:
+            return
+        hb = self._lib.fc_handle_bytes()
+        mine = ctypes.create_string_buffer(hb)
+        _lib.check(self._lib.fc_comm_export(self._comm, mine), self._comm, "comm_export")
+        allh = self._allgather_obj(mine.raw)
+        blob = ctypes.create_string_buffer(b"".join(allh), hb * self.nranks)
+        _lib.check(self._lib.fc_comm_connect(self._comm, blob), self._comm, "comm_connect")
+
+    @property
+    def scratch_bytes(self) -> int:
+        """Current workspace region size (reduction scratch = LL128 staging)."""
+        return int(self._lib.fc_comm_scratch_bytes(self._comm))
+
+    def _ensure_scratch(self, collective: str, count: int, code: int) -> None:
+        """Grow the workspace (collectively) when this call's path wants more
+        than it holds.  The need depends only on rank-uniform values (size,
+        dtype, plan, options), so every rank grows at the same call."""
+        key = (collective, count, code)
+        if not self._grow or key in self._scratch_ok:
+            return
+        self.plan(collective)
+        need = ctypes.c_size_t()
+        _lib.check(self._lib.fc_call_scratch(self._comm, COLL_CODE[collective], count, code,
+                                             self._max_scratch, ctypes.byref(need)),
+                   self._comm, "call_scratch")
+        have = self.scratch_bytes
+        if need.value > have:
+            if torch.cuda.is_current_stream_capturing():
+                raise InvalidArgument(
+                    f"{collective} of {count} elements needs a {need.value}-byte workspace "
+                    f"(have {have}): run it once outside CUDA-graph capture first")
+            target = have
+            while target < need.value:
+                target *= 2
+            self._grow_to(min(target, self._max_scratch))
+        self._scratch_ok.add(key)
+
+    def _grow_to(self, nbytes: int) -> None:
+        """Collective: every rank's collectives on this communicator have
+        completed (device sync + barrier) before the workspaces are
+        re-allocated, then handles are exchanged again."""
+        import torch.distributed as dist
+
+        torch.cuda.synchronize(self.device)
+        if self._group is not None:
+            dist.barrier(group=self._group)
+        _lib.check(self._lib.fc_comm_grow(self._comm, int(nbytes)), self._comm, "comm_grow")
+        self._connect()
 
     # -- NVLS (multicast) engine ----------------------------------------------
     def _setup_nvls(self, nbytes):
@@ -526,6 +587,7 @@ class ForestCollComm(_CommBase):
                 out.copy_(dst)
             return out
         self.plan(ALLGATHER)
+        self._ensure_scratch(ALLGATHER, count, code)
         self._ensure_registered(ALLGATHER, out, count, code)
         _lib.check(self._lib.fc_allgather(self._comm, inp.data_ptr(), out.data_ptr(), count, code,
                                           self._stream()), self._comm, "allgather")
@@ -559,6 +621,7 @@ class ForestCollComm(_CommBase):
             return out
         self._last_order = "tree"
         self.plan(REDUCE_SCATTER)
+        self._ensure_scratch(REDUCE_SCATTER, out.numel(), DTYPE_CODE[inp.dtype])
         _lib.check(self._lib.fc_reduce_scatter(self._comm, inp.data_ptr(), out.data_ptr(),
                                                out.numel(), DTYPE_CODE[inp.dtype], _op_code(op),
                                                self._stream()), self._comm, "reduce_scatter")
@@ -600,6 +663,7 @@ class ForestCollComm(_CommBase):
             out.copy_(tmp)
             return out
         self.plan(ALLREDUCE)
+        self._ensure_scratch(ALLREDUCE, buf.numel(), DTYPE_CODE[buf.dtype])
         self._ensure_registered(ALLREDUCE, out, buf.numel(), DTYPE_CODE[buf.dtype])
         _lib.check(self._lib.fc_allreduce(self._comm, buf.data_ptr(), out.data_ptr(), buf.numel(),
                                           DTYPE_CODE[buf.dtype], _op_code(op), self._stream()),

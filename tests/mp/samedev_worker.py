@@ -45,8 +45,11 @@ def main():
     rank, n = dist.get_rank(), dist.get_world_size()
     mode = sys.argv[1] if len(sys.argv) > 1 else "parity"
     comm = ForestCollComm(nvswitch_doc(n), rank=rank, world_size=n, device=0,
-                          scratch_bytes=64 << 20, options={"timeout_ms": 60000})
+                          scratch_bytes=None if mode == "grow" else 64 << 20,
+                          max_scratch_bytes=512 << 20, options={"timeout_ms": 60000})
     fails = []
+    if mode == "grow":
+        fails = grow(comm, rank, n, dev)
     if mode == "parity":
         fails = parity(comm, rank, n, dev)
     elif mode == "fresh_outputs":
@@ -123,6 +126,51 @@ def fresh_outputs(comm, rank, n, dev):
     nreg = comm.registration_count()
     if nreg > 4:
         fails.append(f"{nreg} registrations after 1000 calls")
+    return fails
+
+
+def grow(comm, rank, n, dev):
+    """The workspace starts small and grows collectively when a call's path
+    needs more (LL128 staging, reduce-scatter windows), up to the cap;
+    results stay bit-exact across re-allocations, and a capture that would
+    need growth fails loudly instead of re-allocating inside the graph."""
+    fails = []
+    s_ag, s_rs = comm.schedule("allgather"), comm.schedule("reduce_scatter")
+    start = comm.scratch_bytes
+    sizes = []
+    for S, dt, dname in ((1 << 12, torch.float32, "float32"), (12 << 20, torch.float32, "float32"),
+                         (1 << 12, torch.float32, "float32"), (20 << 20, torch.bfloat16, "bfloat16")):
+        ins = [seeded(S, torch.float32, 700 + r + S) for r in range(n)]
+        out = torch.empty(n * S, device=dev)
+        comm.all_gather(out, ins[rank].to(dev))
+        torch.cuda.synchronize()
+        _check(out.cpu().numpy(), fo.allgather(s_ag, [x.numpy() for x in ins])[rank],
+               f"allgather S={S}", fails)
+        rin = [seeded(n * S, dt, 900 + r + S) for r in range(n)]
+        rout = torch.empty(S, device=dev, dtype=dt)
+        comm.reduce_scatter(rout, rin[rank].to(dev))
+        torch.cuda.synchronize()
+        _check(host(rout), fo.reduce_scatter(s_rs, [host(x) for x in rin], dname)[rank],
+               f"reduce_scatter S={S} {dname}", fails)
+        sizes.append(comm.scratch_bytes)
+    if not (start == 64 << 20 and sizes[-1] > start and sizes[-1] <= 512 << 20):
+        fails.append(f"workspace did not grow as expected: start {start}, then {sizes}")
+    # a capture whose size needs a larger workspace raises instead of growing
+    S = comm.scratch_bytes // 8  # LL128 staging ~1.07 x the shard in each half: > scratch
+    a = torch.empty(S, device=dev)
+    b = torch.empty(n * S, device=dev)
+    g = torch.cuda.CUDAGraph()
+    raised = False
+    try:
+        with torch.cuda.graph(g):
+            comm.set_option("proto", 1)
+            comm.all_gather(b, a)
+    except Exception as e:  # noqa: BLE001
+        raised = "outside CUDA-graph capture" in str(e)
+    comm.set_option("proto", -1)
+    if not raised:
+        fails.append("capture needing a larger workspace did not raise")
+    torch.cuda.synchronize()
     return fails
 
 
