@@ -406,6 +406,10 @@ def run_multi(args):
     alg = gbs(M, ms)
     ingress = (n - 1) * M // n
     achieved = gbs(ingress, ms)
+    # kernel-issued peer bytes of one call (the NVLink traffic evidence)
+    issued, tinfo = issued_peer_bytes(comm, fn, dist)
+    if tinfo and tinfo["proto"] == "ce":
+        issued = S * 4 + 16  # one copy-engine transfer of the shard (+ two flag words)
     # NCCL on the same buffers
     nccl_out = torch.empty_like(out)
     nccl_ms = timed(lambda: dist.all_gather_into_tensor(nccl_out, inp), args.steps, args.warmup, dist)
@@ -452,7 +456,13 @@ def run_multi(args):
                          "peak_kind": "fallback: B200_PROFILING.md measured peer copy per direction",
                          "nominal": NVLINK_NOMINAL_GBS,
                          "algorithmic_bytes_per_launch": ingress,
-                         "traffic": None},
+                         "traffic": None,
+                         "traffic_note": ("NVML NVLink byte counters are NOT_SUPPORTED on this "
+                                          "pool and ncu must not wrap a multi-rank run; "
+                                          "issued_peer_bytes_per_launch is the executor's own "
+                                          "count of bytes stored into peers (item trace)"),
+                         "issued_peer_bytes_per_launch": issued,
+                         "issued_over_algorithmic": round(issued / ingress, 4)},
             "e2e": {"value": round(gbs(M, e2e_ms), 3), "unit": "GB/s",
                     "h2d_bytes_per_step": S * 4, "d2h_bytes_per_step": M,
                     "ms_per_step": round(e2e_ms, 3),
@@ -466,6 +476,33 @@ def run_multi(args):
         print(json.dumps(line), flush=True)
     comm.close()
     dist.destroy_process_group()
+
+
+def issued_peer_bytes(comm, fn, dist):
+    """Bytes the kernels of one call store into other ranks' memory (payload,
+    LL128 line tags, flag words), from the executor's item trace (the
+    trace's per-item peer_bytes); max over ranks.  The copy-engine path runs
+    no items: its bytes are the shard the copy engine moves.  NVML's NVLink
+    byte counters are NOT_SUPPORTED on this pool (profiles/
+    r02_nvlink_counters.md), so this software count stands in for them."""
+    import torch
+
+    info = None
+    comm.enable_trace(1 << 20)
+    try:
+        comm.reset_trace()
+        dist.barrier()
+        torch.cuda.synchronize()
+        fn()
+        torch.cuda.synchronize()
+        info = comm.last_call_info()
+        rec = comm.read_trace()
+        nb = int(rec["peer_bytes"].astype("int64").sum()) if rec.size else 0
+    finally:
+        comm.disable_trace()
+    x = torch.tensor([nb], dtype=torch.int64, device="cuda")
+    dist.all_reduce(x, op=dist.ReduceOp.MAX)
+    return int(x.item()), info
 
 
 def nccl_group(dist, algo):
@@ -506,11 +543,20 @@ def sweep_multi(comm, dist, n, dev, args):
         except Exception as exc:  # noqa: BLE001
             res[f"nccl_{algo.lower()}_error"] = f"{type(exc).__name__}: {exc}"[:200]
 
-    def rec(coll, M, ms, dtype, fn_nccl):
+    def rec(coll, M, ms, dtype, fn_nccl, fn_ours=None):
         t = comm.t_star(coll, M)
         r = {"collective": coll, "M_bytes": M, "dtype": dtype, "ms": round(ms, 4),
              "algbw_GBps": round(gbs(M, ms), 2), "frac_of_t_star": round(t * 1e3 / ms, 4),
              "proto": comm.last_call_info()["proto"]}
+        if fn_ours is not None and r["proto"] != "ce":
+            alg = (n - 1) * M // n * (2 if coll == "allreduce" else 1)
+            if r["proto"] == "oneshot":  # no item trace: LL128 lines of the input to every peer
+                src = M // n if coll == "allgather" else M
+                issued = -(-src // 120) * 128 * (n - 1)
+            else:
+                issued, _ = issued_peer_bytes(comm, fn_ours, dist)
+            r["issued_peer_bytes"] = issued
+            r["issued_over_algorithmic"] = round(issued / alg, 4)
         for name, g in groups.items():
             try:
                 nm = timed(lambda: fn_nccl(g), steps_for(M, max(5, args.steps)), warm, dist)
@@ -528,7 +574,8 @@ def sweep_multi(comm, dist, n, dev, args):
         o2 = torch.empty_like(out)
         ms = timed(lambda: comm.all_gather(out, inp), steps_for(M, max(5, args.steps)), warm, dist)
         rec("allgather", S * 4 * n, ms, "float32",
-            lambda g: dist.all_gather_into_tensor(o2, inp, group=g))
+            lambda g: dist.all_gather_into_tensor(o2, inp, group=g),
+            lambda: comm.all_gather(out, inp))
         comm.deregister(out)
     for mib, dt in ((256, torch.float32), (256, torch.bfloat16)):
         M = mib * MIB
@@ -537,14 +584,16 @@ def sweep_multi(comm, dist, n, dev, args):
         out = torch.empty(R, device=dev, dtype=dt)
         ms = timed(lambda: comm.reduce_scatter(out, inp), steps_for(M, max(5, args.steps)), warm, dist)
         rec("reduce_scatter", M, ms, str(dt).split(".")[-1],
-            lambda g: dist.reduce_scatter_tensor(out, inp, group=g))
+            lambda g: dist.reduce_scatter_tensor(out, inp, group=g),
+            lambda: comm.reduce_scatter(out, inp))
     for mib in (25, 1024):
         M = mib * MIB
         cnt = M // 2
         buf = comm.empty(cnt, dtype=torch.bfloat16)
         buf.normal_()
         ms = timed(lambda: comm.all_reduce(buf), steps_for(M, max(5, args.steps)), warm, dist)
-        rec("allreduce", M, ms, "bfloat16", lambda g: dist.all_reduce(buf, group=g))
+        rec("allreduce", M, ms, "bfloat16", lambda g: dist.all_reduce(buf, group=g),
+            lambda: comm.all_reduce(buf))
         comm.deregister(buf)
     comm.check()
     try:

@@ -637,7 +637,7 @@ template <int DT, int WW, bool AVG>
 __device__ void run_item(const FcParams& P, int me, FcCtl* ctl, const int* T, int c,
                          unsigned e, int w, int lane, unsigned& ready_mask, Ring& rg,
                          ItemShared* sh, ItemPtrs* ptrs, unsigned long long& t_ready,
-                         unsigned long long& t_moved) {
+                         unsigned long long& t_moved, unsigned long long& peer_bytes) {
   const int kind = __ldg(T + TW_KIND);
   const int t = __ldg(T + TW_TREE);
   const int root = __ldg(T + TW_ROOT);
@@ -740,7 +740,16 @@ __device__ void run_item(const FcParams& P, int me, FcCtl* ctl, const int* T, in
   // 3. publish: the CTA barrier orders every thread's stores (and the bulk
   //    completions above) before thread 0's cumulative .sys release.
   worker_sync<WW>(wk);
-  if (P.trace && leader) t_moved = globaltimer();
+  if (P.trace && leader) {
+    t_moved = globaltimer();
+    // bytes this item stored into other ranks: the chunk to every remote
+    // destination, plus one 4-byte flag per child / parent
+    int remote = 0;
+    if (kind == FC_K_RS_FWD) remote = (rs_parent != me);
+    else if (kind != FC_K_RS_ROOT)
+      for (int j = 0; j < n_ag; ++j) remote += (__ldg(T + TW_AG_CHILD + j) != me);
+    peer_bytes = (unsigned long long)(b1 - b0) * remote + 4ull * remote;
+  }
   if (kind == FC_K_RS_ROOT || !leader) return;
   if (kind == FC_K_RS_FWD) {
     st_release_sys(P.flags[rs_parent] + P.rs_flag_off + __ldg(T + TW_RS_PSLOT) * P.maxc + fi, e);
@@ -796,7 +805,8 @@ __device__ __forceinline__ bool ll_poll(const char* const* line, const bool* val
 template <int DT, int WW, bool AVG>
 __device__ void run_item_ll(const FcParams& P, int me, FcCtl* ctl, const int* T, int c,
                             unsigned e, int w, int lane, unsigned& ready_mask, ItemShared* sh,
-                            ItemPtrs* ptrs, unsigned long long& t_ready) {
+                            ItemPtrs* ptrs, unsigned long long& t_ready,
+                            unsigned long long& peer_bytes) {
   constexpr int U = FC_LL_UNROLL;
   const int kind = __ldg(T + TW_KIND);
   const int root = __ldg(T + TW_ROOT);
@@ -956,6 +966,13 @@ __device__ void run_item_ll(const FcParams& P, int me, FcCtl* ctl, const int* T,
   };
   const bool ok = (src_al && out_al) ? lines(std::true_type{}) : lines(std::false_type{});
   if (!ok) return;
+  if (P.trace && leader) {  // 128-byte lines of this chunk to every peer destination
+    int remote = 0;
+    if (kind == FC_K_RS_FWD) remote = (rs_parent != me);
+    else if (kind == FC_K_AG_ROOT || kind == FC_K_AG_FWD || kind == FC_K_AR_ROOT)
+      for (int j = 0; j < n_ag; ++j) remote += (__ldg(T + TW_AG_CHILD + j) != me);
+    peer_bytes = (unsigned long long)(l1 - l0) * 128ull * remote;
+  }
   worker_sync<WW>(wk);
 }
 
@@ -1031,13 +1048,13 @@ __global__ void __launch_bounds__(FC_BLOCK, 1) fc_forest_kernel(const __grid_con
       ti = nact + (int)(item - nA);
     }
     const unsigned long long t0 = trace ? globaltimer() : 0;
-    unsigned long long t_ready = t0, t_moved = t0;
+    unsigned long long t_ready = t0, t_moved = t0, peer_bytes = 0;
     if constexpr (PROTO == 1)
       run_item_ll<DT, WW, AVG>(P, me, ctl, tasks + (long long)ti * FC_TASK_WORDS, P.c0 + c, e, w,
-                          lane, ready_mask, &sh, &s_ptrs, t_ready);
+                          lane, ready_mask, &sh, &s_ptrs, t_ready, peer_bytes);
     else
       run_item<DT, WW, AVG>(P, me, ctl, tasks + (long long)ti * FC_TASK_WORDS, P.c0 + c, e, w, lane,
-                       ready_mask, rg, &sh, &s_ptrs, t_ready, t_moved);
+                       ready_mask, rg, &sh, &s_ptrs, t_ready, t_moved, peer_bytes);
     if (trace && lead) {
       const unsigned idx = atomicAdd(P.trace_count, 1u);
       if (idx < P.trace_cap) {
@@ -1046,7 +1063,7 @@ __global__ void __launch_bounds__(FC_BLOCK, 1) fc_forest_kernel(const __grid_con
         r.t_end = globaltimer();
         r.t_wait = (unsigned)(t_ready - t0);
         r.t_move = t_moved > t_ready ? (unsigned)(t_moved - t_ready) : 0u;
-        r.pad = 0;
+        r.peer_bytes = peer_bytes > 0xFFFFFFFFull ? 0xFFFFFFFFu : (unsigned)peer_bytes;
         r.chunk = P.c0 + c;
         r.rank = (short)me;
         r.task = (short)ti;

@@ -101,7 +101,8 @@ struct FcTraceRec {
   short rank, task;
   short worker;
   unsigned short launch;  // epoch (low 16 bits)
-  unsigned pad;
+  unsigned peer_bytes;    // bytes this item stored into other ranks' memory
+                          // (payload + LL128 line tags + flag words)
 };
 
 struct FcParams {

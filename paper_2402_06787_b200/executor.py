@@ -200,7 +200,7 @@ class _CommBase:
     TRACE_DTYPE = np.dtype([("t_start", "<u8"), ("t_end", "<u8"), ("t_wait", "<u4"),
                             ("t_move", "<u4"), ("chunk", "<i4"), ("rank", "<i2"),
                             ("task", "<i2"), ("worker", "<i2"), ("launch", "<u2"),
-                            ("pad", "<u4")])
+                            ("peer_bytes", "<u4")])
 
     def enable_trace(self, capacity: int = 1 << 20) -> None:
         """Record one (start, end, rank, task, chunk, worker, launch) row per

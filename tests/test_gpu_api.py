@@ -108,6 +108,10 @@ def test_trace_records(dev):
     assert rec.size > 0
     assert set(np.unique(rec["rank"])) == set(range(n))
     assert np.all(rec["t_end"] >= rec["t_start"])
+    # peer bytes: every rank receives (N-1) shards; LL128 adds 8 of 128 bytes
+    payload = (n - 1) * n * (1 << 16) * 4
+    total = int(rec["peer_bytes"].astype(np.int64).sum())
+    assert payload <= total <= payload * 1.08, (total, payload)
     comm.disable_trace()
 
 
