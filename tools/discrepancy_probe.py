@@ -52,6 +52,23 @@ def main():
     t("after NCCL NVLS all-gathers")
     timed(lambda: dist.all_gather_into_tensor(o2, inp), 50, 3, dist)
     t("after NCCL default all-gathers")
+    timed(lambda: comm.all_gather(big_o, big_i), 10, 3, dist, soak_s=1.0)
+    t("after a 1 s soak of 1 GiB allgathers")
+    from bench import pipelined_e2e
+
+    h_in = torch.empty(big_i.numel(), pin_memory=True)
+    h_out = torch.empty(big_o.numel(), pin_memory=True)
+    d_sets = [([big_i], [big_o]), ([torch.empty_like(big_i)], [comm.empty(big_o.numel())])]
+    pipelined_e2e([h_in], [h_out], d_sets, lambda o, i: comm.all_gather(o[0], i[0]), 5, 1, dist)
+    t("after the pipelined e2e phase")
+    small_i = torch.randn((1 << 20) // n // 4, device=dev)
+    small_o = comm.empty(n * small_i.numel())
+    timed(lambda: comm.all_gather(small_o, small_i), 100, 3, dist)
+    t("after 1 MiB one-hop allgathers")
+    comm.enable_trace(1 << 20)
+    comm.all_gather(big_o, big_i)
+    comm.disable_trace()
+    t("after a traced call")
     comm.check()
     comm.close()
     dist.destroy_process_group()
