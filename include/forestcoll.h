@@ -139,7 +139,7 @@ extern "C" {
 #define FC_OPT_CE_MIN 23       /* 2-rank single-switch forest: allgathers whose output is at
                                   least this many bytes move each shard with the copy engine
                                   (one cudaMemcpyAsync into the peer's registered output) and
-                                  the SMs only synchronise (default 128 MiB; 0 disables) */
+                                  the SMs only synchronise (default 24 MiB; 0 disables) */
 
 typedef struct fc_comm fc_comm_t;
 

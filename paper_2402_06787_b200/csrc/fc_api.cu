@@ -115,7 +115,7 @@ struct fc_comm {
   long long nvls_ll_red_max = -1;     // NVLS allreduce via LL multicast up to this many bytes
                                       // (-1: N x 64 KiB; reduce-scatter: 1/N of it)
   long long ce_min = -1;              // 2-rank forest: copy-engine allgather from this output
-                                      // size (-1: 128 MiB; 0: off)
+                                      // size (-1: 24 MiB; 0: off)
   int sm_count = 148;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   cudaEvent_t ev_last = nullptr;     // cross-stream ordering of this comm's collectives
@@ -492,9 +492,10 @@ int run(fc_comm* c, int coll, const void* const* sends, void* const* recvs, size
   // engine (fc_ce.cu) from ce_min output bytes (the peer's output must be
   // registered, as for the chunk-flag protocol)
   if (coll == FC_ALLGATHER && onehop && N == 2 && !c->virt && c->nlocal == 1 && c->ce_min != 0) {
-    // measured crossover vs the LL128 forest at N=2: equal at 64 MiB,
-    // +10 % at 256 MiB, +9 % at 1 GiB, +12 % at 4 GiB (0.855 of T*)
-    const long long lim = c->ce_min > 0 ? c->ce_min : (128LL << 20);
+    // measured vs the LL128 forest at N=2 (tools/exp_n2_ag_mid.sh): +3 % at
+    // 24 MiB, +11 % at 32 MiB, +4 % at 96 MiB, +9 % at 1 GiB, +12 % at 4 GiB
+    // (0.856 of T*); below 24 MiB the one-hop path or the forest wins
+    const long long lim = c->ce_min > 0 ? c->ce_min : (24LL << 20);
     if (total * es >= lim) {
       if (path_out) return decided(5, 0);
       return run_ce_ag(c, sends[0], recvs[0], S * es, stream);
@@ -1222,7 +1223,7 @@ int fc_comm_get_option(fc_comm_t* c, int option, long long* v) {
       *v = c->oneshot_ag_max >= 0 ? c->oneshot_ag_max : (16LL << 20);
       return FC_SUCCESS;
     case FC_OPT_CE_MIN:
-      *v = c->ce_min >= 0 ? c->ce_min : (128LL << 20);
+      *v = c->ce_min >= 0 ? c->ce_min : (24LL << 20);
       return FC_SUCCESS;
     case FC_OPT_LL_WORKER_WARPS: *v = c->ll_worker_warps; return FC_SUCCESS;
     case FC_OPT_MAX_CTAS_PER_RANK: {
