@@ -18,9 +18,12 @@ def samedev() -> bool:
 
 
 def init():
-    """Initialise the default process group; returns the local device index."""
-    if samedev():
-        local = 0
+    """Initialise the default process group; returns the local device index.
+    FC_RANKS_PER_GPU=k packs k rank processes per GPU (gloo), e.g. the
+    8-rank forest on a 4-GPU box."""
+    k = int(os.environ.get("FC_RANKS_PER_GPU", "0"))
+    if samedev() or k > 1:
+        local = 0 if samedev() else int(os.environ["LOCAL_RANK"]) // k
         torch.cuda.set_device(local)
         dist.init_process_group("gloo")
     else:

@@ -110,3 +110,4 @@ def test_eight_rank_forests_over_nvlink(n):
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=1200)
     out = r.stdout + r.stderr
     assert r.returncode == 0 and out.count(" OK") >= n, out[-4000:]
+
