@@ -179,7 +179,8 @@ int fc_buffer_register_multi(fc_comm_t* comm, const void* const* ptrs,
 int fc_buffer_query(fc_comm_t* comm, const void* ptr, size_t bytes, int* registered);
 int fc_buffer_count(const fc_comm_t* comm);
 /* The path the next collective of this size would take: 0 chunk flags,
- * 1 LL128, 4 one-hop / one-shot, 5 copy engine (2-rank allgather), -1 empty.
+ * 1 LL128, 4 one-hop / one-shot, 5 copy engine (2-rank allgather), 6 the 1-rank
+ * forest's local copy, -1 empty.
  * Paths 0 and 5 store into peers' outputs: allgather / allreduce outputs
  * must then be registered.  The
  * choice depends only on values equal on every rank (count, dtype, plan,

@@ -474,6 +474,28 @@ int run(fc_comm* c, int coll, const void* const* sends, void* const* recvs, size
   for (int i = 0; i < c->nlocal && !path_out; ++i)
     if (!sends[i] || !recvs[i]) return fail(c, FC_ERR_INVALID_ARG, "null buffer");
 
+  // The 1-rank forest (N=1 is outside the reference's API, topology.py:263-266)
+  // is its root's copy send -> recv: one full-GPU vector copy kernel
+  if (N == 1 && coll == FC_ALLGATHER && c->nlocal == 1) {
+    if (path_out) return *path_out = 6, FC_SUCCESS;
+    {
+      const int st = order_begin(c, (cudaStream_t)stream);
+      if (st) return st;
+    }
+    const bool copy = recvs[0] != sends[0];
+    if (copy)
+      FC_CUDA(c, (cudaError_t)fc_ce_copy_launch(recvs[0], sends[0], total * es, 2 * c->sm_count,
+                                                stream));
+    {
+      const int st = order_end(c, (cudaStream_t)stream);
+      if (st) return st;
+    }
+    c->info[0] = copy ? 1 : 0;
+    c->info[1] = c->info[2] = 1;
+    c->info[3] = 2 * c->sm_count;
+    c->info[5] = 6;  // local copy
+    return FC_SUCCESS;
+  }
   // Every choice below depends only on values that are equal on every rank
   // (sizes, dtype, plan, options): ranks must run the same kernel.  Local
   // buffer alignment is handled inside the kernels (ld_u64_any/st_u64_any).

@@ -320,3 +320,26 @@ def test_staging_shared_by_all_ll128_writers(dev):
             assert np.array_equal(ari[r].cpu().numpy(), ref[r]), (it, "ar", r)
     comm.check()
     comm.close()
+
+
+@pytest.mark.parametrize("n_el,offset", [(1, 0), (1000, 1), (1 << 20, 0), ((1 << 22) + 3, 3)])
+def test_one_rank_forest_is_a_local_copy(dev, n_el, offset):
+    """The 1-rank forest (bench.py's local-copy sanity point) runs as one
+    full-GPU copy kernel; any size and alignment."""
+    from fractions import Fraction
+
+    from paper_2402_06787_b200 import VirtualComm
+    from paper_2402_06787_b200._refpath import require_collsched
+
+    cs = require_collsched()
+    s = cs.Schedule(collective="allgather", num_compute=1, k=1, U=Fraction(1), y=Fraction(1),
+                    inv_x_star=Fraction(0),
+                    roots=(cs.RootTrees("g0", (cs.ScheduleBatch(1, ()),)),))
+    comm = VirtualComm(schedules={"allgather": s}, device=0)
+    src = torch.randn(n_el + offset, device=dev)[offset:]
+    dst = torch.zeros(n_el + offset, device=dev)[offset:]
+    comm.all_gather([dst], [src])
+    comm.check()
+    assert comm.last_call_info()["proto"] == "local"
+    assert torch.equal(dst, src)
+    comm.close()
