@@ -140,6 +140,12 @@ extern "C" {
                                   least this many bytes move each shard with the copy engine
                                   (one cudaMemcpyAsync into the peer's registered output) and
                                   the SMs only synchronise (default 24 MiB; 0 disables) */
+#define FC_OPT_TWOHOP_MAX 25   /* tree engine, single-switch forest: reduce-scatters /
+                                  allreduces above the one-shot limit and up to this many
+                                  input bytes per rank run in two hops (shards to their
+                                  roots, in-tree evaluated there, reduced shards to every
+                                  rank; default 6 MiB at N=2, 12 MiB above, reduce-scatter
+                                  2/3 of it; 0 disables) */
 
 typedef struct fc_comm fc_comm_t;
 
@@ -180,7 +186,7 @@ int fc_buffer_query(fc_comm_t* comm, const void* ptr, size_t bytes, int* registe
 int fc_buffer_count(const fc_comm_t* comm);
 /* The path the next collective of this size would take: 0 chunk flags,
  * 1 LL128, 4 one-hop / one-shot, 5 copy engine (2-rank allgather), 6 the 1-rank
- * forest's local copy, -1 empty.
+ * forest's local copy, 7 two-hop reduction, -1 empty.
  * Paths 0 and 5 store into peers' outputs: allgather / allreduce outputs
  * must then be registered.  The
  * choice depends only on values equal on every rank (count, dtype, plan,

@@ -22,7 +22,7 @@ OPT_LAG, OPT_COPY_MODE, OPT_DMA_ROOT_COPY, OPT_WORKER_WARPS = 6, 7, 8, 9
 OPT_PROTO, OPT_LL_MAX, OPT_LL_CHUNK_MAX, OPT_LL_WORKER_WARPS, OPT_NVLS_CTAS = 10, 11, 12, 13, 14
 OPT_PDL, OPT_CHUNK_TAIL, OPT_NVLS_LL_MAX, OPT_NVLS_LL_HALF, OPT_NVLS_LL_RED_MAX = 15, 16, 17, 18, 19
 OPT_ONESHOT_MAX, OPT_ONESHOT_AG_MAX, OPT_MAX_CTAS_PER_RANK = 20, 21, 22
-OPT_CE_MIN = 23
+OPT_CE_MIN, OPT_TWOHOP_MAX = 23, 25
 OPTIONS = {
     "ctas_per_rank": OPT_CTAS_PER_RANK,
     "chunk_max": OPT_CHUNK_MAX,
@@ -47,6 +47,7 @@ OPTIONS = {
     "oneshot_ag_max": OPT_ONESHOT_AG_MAX,
     "max_ctas_per_rank": OPT_MAX_CTAS_PER_RANK,
     "ce_min": OPT_CE_MIN,
+    "twohop_max": OPT_TWOHOP_MAX,
 }
 
 # symbol -> (restype, argtypes)

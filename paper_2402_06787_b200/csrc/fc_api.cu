@@ -114,6 +114,8 @@ struct fc_comm {
                                       // (-1: 2 MiB; reduce-scatter 2/N of it; 0: off)
   long long nvls_ll_red_max = -1;     // NVLS allreduce via LL multicast up to this many bytes
                                       // (-1: N x 64 KiB; reduce-scatter: 1/N of it)
+  long long twohop_max = -1;          // tree engine: two-hop reductions up to this many input
+                                      // bytes per rank (-1: default; 0: off)
   long long ce_min = -1;              // 2-rank forest: copy-engine allgather from this output
                                       // size (-1: 24 MiB; 0: off)
   int sm_count = 148;
@@ -347,7 +349,7 @@ int oneshot_common(fc_comm* c, FcNvlsParams& P, int mode, int rd, const void* co
 // AG depth.
 int run_oneshot(fc_comm* c, int coll, const Plan& pl, const void* const* sends,
                 void* const* recvs, long long S, long long total, int es, int rd, int op,
-                long long half, void* stream) {
+                long long half, void* stream, bool twohop = false) {
   FcNvlsParams P;
   memset(&P, 0, sizeof(P));
   P.op = op;
@@ -357,7 +359,10 @@ int run_oneshot(fc_comm* c, int coll, const Plan& pl, const void* const* sends,
   P.buf_bytes = total * es;
   P.count = total;
   P.shard_elems = S;
-  return oneshot_common(c, P, coll == FC_REDUCE_SCATTER ? 6 : 7, rd, sends, recvs, half, stream);
+  const int mode = twohop ? (coll == FC_REDUCE_SCATTER ? 10 : 9) : (coll == FC_REDUCE_SCATTER ? 6 : 7);
+  const int st = oneshot_common(c, P, mode, rd, sends, recvs, half, stream);
+  if (!st && twohop) c->info[5] = 7;  // two-hop
+  return st;
 }
 
 // One-hop allgather (fc_oneshot_ag128_kernel): outputs are written locally
@@ -547,6 +552,22 @@ int run(fc_comm* c, int coll, const void* const* sends, void* const* recvs, size
         (S * es) % 8 == 0 && (long long)N * lines * 128 <= half) {
       if (path_out) return decided(4, 2 * (long long)N * lines * 128);
       return run_oneshot(c, coll, pl, sends, recvs, S, total, es, rd, op, half, stream);
+    }
+  }
+  // mid-size reductions: two hops (shards to their roots, reduced shards to
+  // everyone; fc_nvls.cu fc_twohop128_kernel) -- the forest's link loads,
+  // two hops instead of the in-trees' plus out-trees' depths
+  if (coll != FC_ALLGATHER && onehop && pl.d_os && c->twohop_max != 0) {
+    const long long bytes = total * es;
+    // measured crossover vs the LL128 forest (tools/exp_twohop_r02.sh): N=4
+    // allreduce 4 MiB +56 %, 8 MiB +17 %, 16 MiB even; N=2 4 MiB +15 %, 8 MiB
+    // -6 %.  Reduce-scatter (input bytes) crosses over at 2/3 of that.
+    const long long lim = c->twohop_max > 0 ? c->twohop_max : (N <= 2 ? (6LL << 20) : (12LL << 20));
+    const long long need = 2LL * N * ((S * es + 119) / 120) * 128;  // hop-1 + hop-2 lines
+    if (bytes <= (coll == FC_REDUCE_SCATTER ? 2 * lim / 3 : lim) && bytes % 8 == 0 &&
+        (S * es) % 8 == 0 && need <= half) {
+      if (path_out) return decided(7, 2 * need);
+      return run_oneshot(c, coll, pl, sends, recvs, S, total, es, rd, op, half, stream, true);
     }
   }
   FcParams P;
@@ -1194,6 +1215,10 @@ int fc_comm_set_option(fc_comm_t* c, int option, long long v) {
       if (v < 0) return fail(c, FC_ERR_INVALID_ARG, "ce_min < 0");
       c->ce_min = v;
       return FC_SUCCESS;
+    case FC_OPT_TWOHOP_MAX:
+      if (v < 0) return fail(c, FC_ERR_INVALID_ARG, "twohop_max < 0");
+      c->twohop_max = v;
+      return FC_SUCCESS;
     case FC_OPT_NVLS_CTAS:
       if (v < 1 || v > 1024) return fail(c, FC_ERR_INVALID_ARG, "nvls_ctas out of range");
       c->nvls_ctas = (int)v;
@@ -1246,6 +1271,9 @@ int fc_comm_get_option(fc_comm_t* c, int option, long long* v) {
       return FC_SUCCESS;
     case FC_OPT_CE_MIN:
       *v = c->ce_min >= 0 ? c->ce_min : (24LL << 20);
+      return FC_SUCCESS;
+    case FC_OPT_TWOHOP_MAX:
+      *v = c->twohop_max >= 0 ? c->twohop_max : (c->nranks <= 2 ? (6LL << 20) : (12LL << 20));
       return FC_SUCCESS;
     case FC_OPT_LL_WORKER_WARPS: *v = c->ll_worker_warps; return FC_SUCCESS;
     case FC_OPT_MAX_CTAS_PER_RANK: {

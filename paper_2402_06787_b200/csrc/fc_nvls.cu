@@ -648,11 +648,128 @@ __global__ void __launch_bounds__(FC_NVLS_THREADS) fc_oneshot_ag128_kernel(const
   oneshot_finish(V, P, e);
 }
 
+// Two-hop allreduce (mode 9) / reduce-scatter (mode 10) for mid-size buffers
+// on a single-switch forest (FC_PLAN_ONEHOP).  Hop 1: every rank stores its
+// input's shard q, as LL128 lines in shard coordinates (line l = shard bytes
+// [120 l, 120 l + 120)), into rank q's staging -- (N-1)/N of the input, the
+// forest's reduce-scatter load.  Rank q then evaluates shard q over the
+// forest's in-tree locally (tree_word: the forest kernel's order, bit-exact)
+// and writes it to its output.  Hop 2 (allreduce): it stores the reduced
+// lines into every peer's staging, and every rank copies the other roots'
+// arrived lines to its output -- the forest's allgather load.  Two hops in
+// place of the in-trees' and out-trees' depths; staging halves alternate by
+// epoch parity as for every LL128 writer.
+template <int DT>
+__global__ void __launch_bounds__(FC_NVLS_THREADS) fc_twohop128_kernel(const __grid_constant__ FcNvlsParams P) {
+  using E = typename Red<DT>::E;
+  const OneshotView V = oneshot_view(P);
+  __shared__ unsigned s_e;
+  if (threadIdx.x == 0) s_e = *reinterpret_cast<volatile unsigned*>(&V.ctl->epoch) + 1;
+  __syncthreads();
+  const unsigned e = s_e;
+  const unsigned long long flag = e;
+  const bool ar = P.mode == 9;
+  const int N = P.nranks, me = V.rank;
+  const long long es = (long long)sizeof(E);
+  const long long S = P.shard_elems;
+  const long long total = ar ? P.count : S * N;  // elements of the input buffer
+  auto shard_bytes = [&](int q) -> long long {
+    const long long lo = (long long)q * S, hi = (long long)(q + 1) * S < total ? (long long)(q + 1) * S : total;
+    return hi > lo ? (hi - lo) * es : 0;
+  };
+  const long long Lmax = (S * es + 119) / 120;
+  const long long slot = Lmax * 128;
+  const long long half = (long long)(e & 1u) * P.ll_half;
+  const long long rs_area = half;                           // [sender][line]
+  const long long ag_area = half + (long long)N * slot;     // [root][line]
+  const int lane = threadIdx.x & 31, gl = lane & 7;
+  const long long gid = (V.cta * blockDim.x + threadIdx.x) >> 3;
+  const long long ngrp = (V.nctas * blockDim.x) >> 3;
+  const long long p_lane = 16LL * gl;
+  // hop 1: shard q of the own input -> rank q's staging (the own shard too)
+  for (long long j = gid; j < (long long)N * Lmax; j += ngrp) {
+    const int q = (int)(j / Lmax);
+    const long long l = j - (long long)q * Lmax;
+    const long long Bq = shard_bytes(q);
+    if (120 * l >= Bq) continue;
+    const char* src = V.send + (long long)q * S * es;
+    const long long pb = 120 * l + p_lane;  // shard-relative byte
+    unsigned long long w0 = 0, w1 = flag;
+    if (pb + 8 <= Bq) w0 = ld_u64_any(src + pb);
+    if (gl < 7) w1 = (pb + 16 <= Bq) ? ld_u64_any(src + pb + 8) : 0ull;
+    asm volatile("st.volatile.global.v2.u64 [%0], {%1, %2};" ::"l"(P.peer_stage[q] + rs_area + (long long)me * slot + 128 * l + 16 * gl),
+                 "l"(w0), "l"(w1)
+                 : "memory");
+  }
+  // reduce the own shard as its lines arrive: warp-uniform, 4 lines per warp step
+  const unsigned long long t0 = globaltimer();
+  const long long wid = gid >> 2, nw = ngrp >> 2;
+  const long long Bme = shard_bytes(me);
+  const long long Lme = (Bme + 119) / 120;
+  const long long base_me = (long long)me * S * es;  // global byte offset of the own shard
+  char* out_me = ar ? V.out + base_me : V.out;
+  bool ok = true;
+  for (long long lb = 4 * wid; lb < Lme && ok; lb += 4 * nw) {
+    const long long l = lb + (lane >> 3);
+    const bool valid = l < Lme;
+    unsigned long long x0[FC_MAXR], x1[FC_MAXR];
+    for (int q = 0; q < N && ok; ++q)
+      ok = poll_line(V.stage + rs_area + (long long)q * slot + 128 * l + 16 * gl, valid, flag, lane,
+                     x0[q], x1[q], V.ctl, t0, P.timeout_ns, FC_DEVERR_TIMEOUT_RS);
+    if (!ok) break;
+    const long long pb = 120 * l + p_lane;
+    unsigned long long r0 = 0, r1 = gl < 7 ? 0ull : flag;
+    if (valid && pb + 8 <= Bme) {
+      r0 = tree_word<DT>(P, !ar, me, base_me + pb, x0);
+      st_u64_any(out_me + pb, r0);
+    }
+    if (valid && gl < 7 && pb + 16 <= Bme) {
+      r1 = tree_word<DT>(P, !ar, me, base_me + pb + 8, x1);
+      st_u64_any(out_me + pb + 8, r1);
+    }
+    if (ar && valid) {  // hop 2: the reduced line to every peer
+      for (int q = 0; q < N; ++q)
+        if (q != me)
+          asm volatile("st.volatile.global.v2.u64 [%0], {%1, %2};" ::"l"(P.peer_stage[q] + ag_area + (long long)me * slot + 128 * l + 16 * gl),
+                       "l"(r0), "l"(r1)
+                       : "memory");
+    }
+  }
+  // allreduce: copy the other roots' reduced lines to the output
+  if (ar && ok) {
+    for (long long jb = 4 * wid; jb < (long long)N * Lmax; jb += 4 * nw) {
+      const long long j = jb + (lane >> 3);
+      const int q = (int)((j < (long long)N * Lmax ? j : 0) / Lmax);
+      const long long l = j - (long long)q * Lmax;
+      const long long Bq = shard_bytes(q);
+      const bool valid = j < (long long)N * Lmax && q != me && 120 * l < Bq;
+      unsigned long long a, b;
+      if (!poll_line(V.stage + ag_area + (long long)q * slot + 128 * l + 16 * gl, valid, flag, lane, a,
+                     b, V.ctl, t0, P.timeout_ns, FC_DEVERR_TIMEOUT_AG))
+        break;
+      if (!valid) continue;
+      char* dst = V.out + (long long)q * S * es;
+      const long long pb = 120 * l + p_lane;
+      if (pb + 8 <= Bq) st_u64_any(dst + pb, a);
+      if (gl < 7 && pb + 16 <= Bq) st_u64_any(dst + pb + 8, b);
+    }
+  }
+  oneshot_finish(V, P, e);
+}
+
 }  // namespace
 
 namespace {
 const void* oneshot_fn(int mode, int dtype) {
   if (mode == 8) return (const void*)fc_oneshot_ag128_kernel;
+  if (mode == 9 || mode == 10) {
+    switch (dtype) {
+      case FC_BFLOAT16: return (const void*)fc_twohop128_kernel<FC_BFLOAT16>;
+      case FC_FLOAT16: return (const void*)fc_twohop128_kernel<FC_FLOAT16>;
+      case FC_INT32: return (const void*)fc_twohop128_kernel<FC_INT32>;
+      default: return (const void*)fc_twohop128_kernel<FC_FLOAT32>;
+    }
+  }
   switch (dtype) {
     case FC_BFLOAT16: return (const void*)fc_oneshot128_kernel<FC_BFLOAT16>;
     case FC_FLOAT16: return (const void*)fc_oneshot128_kernel<FC_FLOAT16>;

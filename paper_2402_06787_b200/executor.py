@@ -190,7 +190,7 @@ class _CommBase:
         info = {"launches": buf[0], "nchunks": buf[1], "window": buf[2], "grid": buf[3],
                 "unit_bytes": buf[4],
                 "proto": {0: "flags", 1: "ll128", 2: "nvls", 3: "nvls_ll", 4: "oneshot",
-                          5: "ce", 6: "local"}[buf[5]]}
+                          5: "ce", 6: "local", 7: "twohop"}[buf[5]]}
         # floating-point summation order of the last reduction: "tree" (the
         # forest's order, bit-exact vs the oracle) or "switch" (in-NVSwitch)
         info["order"] = getattr(self, "_last_order", None)

@@ -343,3 +343,26 @@ def test_one_rank_forest_is_a_local_copy(dev, n_el, offset):
     assert comm.last_call_info()["proto"] == "local"
     assert torch.equal(dst, src)
     comm.close()
+
+
+@pytest.mark.parametrize("base", ["nvs2", "nvs4", "nvs8"])
+@pytest.mark.parametrize("dtype", ["float32", "bfloat16", "float16", "int32"])
+@pytest.mark.parametrize("mib", [3, 5])
+@pytest.mark.parametrize("offset", [0, 1])
+def test_twohop_reductions(dev, base, dtype, mib, offset):
+    """Mid-size reduce-scatter / allreduce in two hops (shards to their
+    roots, the in-tree evaluated there, reduced shards to every rank),
+    bit-exact with the forest kernel's order; SUM and AVG; unaligned views."""
+    es = 2 if dtype in ("bfloat16", "float16") else 4
+    for coll in ("allreduce", "reduce_scatter"):
+        comm, s = _comm(f"{base}_{coll}")
+        comm.set_option("twohop_max", 16 << 20)
+        n = comm.nranks
+        count = mib * (1 << 20) // es
+        S = count if coll == "allreduce" else count // n
+        S -= S % 64
+        for op in (("sum", "avg") if dtype != "int32" else ("sum",)):
+            ins, outs = _run(comm, coll, S, dtype, dev, seed=mib * 7 + offset, op=op, offset=offset)
+            assert comm.last_call_info()["proto"] == "twohop", comm.last_call_info()
+            _assert_exact(s, coll, ins, outs, dtype, op=op)
+        comm.close()
