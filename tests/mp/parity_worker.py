@@ -49,10 +49,12 @@ def main():
     # auto (one-hop / one-shot, else LL128 where aligned), auto with the
     # one-hop paths off (the forest's LL128 lines), the chunk-flag protocol,
     # and (N=2) every allgather through the copy-engine path (ce_min=1)
+    twohop_default = comm.get_option("twohop_max")
     for proto, onehop, ce in ((-1, True, 0), (-1, False, 0), (0, True, 0), (-1, True, 1)):
         comm.set_option("proto", proto)
         comm.set_option("oneshot_ag_max", (16 << 20) if onehop else 0)
         comm.set_option("oneshot_max", (2 << 20) if onehop else 0)
+        comm.set_option("twohop_max", twohop_default if onehop else 0)
         comm.set_option("ce_min", ce)
         fails += [f"proto={proto} onehop={onehop} ce={ce}: {f}" for f in run_all(comm, rank, n, dev)]
         if ce and n == 2 and comm.last_call_info()["proto"] not in ("ce", "oneshot", "flags", "ll128"):
@@ -129,6 +131,28 @@ def run_all(comm, rank, n, dev):
             ref = fo.reduce_scatter(comm.schedule("reduce_scatter"), [host(x) for x in ins], name)[rank]
             if not np.array_equal(host(out).view(np.uint8), ref.view(np.uint8)):
                 fails.append(f"one-shot reduce_scatter {name} S={S}")
+    # two-hop path (mid sizes: shards to their roots, in-tree evaluated at the
+    # root, reduced shards to everyone): bit-identical as well
+    for dtype, name in ((torch.float32, "float32"), (torch.bfloat16, "bfloat16"), (torch.int32, "int32")):
+        es = torch.tensor([], dtype=dtype).element_size()
+        count = (3 << 20) // es // (64 * n) * (64 * n)  # 3 MiB, equal 256-byte-aligned shards
+        ins = [seeded(count, dtype, 2300 + r) for r in range(n)]
+        buf = comm.empty(count, dtype=dtype)
+        buf.copy_(ins[rank].to(dev))
+        comm.all_reduce(buf)
+        torch.cuda.synchronize()
+        got = comm.last_call_info()["proto"]
+        if comm.get_option("proto") < 0 and comm.get_option("oneshot_max") > 0 and got not in ("twohop", "ce"):
+            fails.append(f"allreduce {name} count={count} took {got}, expected the two-hop path")
+        ref = fo.allreduce(comm.schedule("allreduce"), [host(x) for x in ins], name)[rank]
+        if not np.array_equal(host(buf).view(np.uint8), ref.view(np.uint8)):
+            fails.append(f"two-hop allreduce {name} count={count}")
+        out = torch.zeros(count // n, dtype=dtype, device=dev)
+        comm.reduce_scatter(out, ins[rank].to(dev))
+        torch.cuda.synchronize()
+        ref = fo.reduce_scatter(comm.schedule("reduce_scatter"), [host(x) for x in ins], name)[rank]
+        if not np.array_equal(host(out).view(np.uint8), ref.view(np.uint8)):
+            fails.append(f"two-hop reduce_scatter {name} S={count // n}")
     # op avg (fp dtypes): the root scales its fp32 sum by fp32(1/N) once
     for dtype, name in ((torch.bfloat16, "bfloat16"), (torch.float32, "float32")):
         for S in (999, (1 << 19) + 8):
