@@ -320,7 +320,7 @@ int oneshot_common(fc_comm* c, FcNvlsParams& P, int mode, int rd, const void* co
     P.ctas_per_rank = c->sm_count;  // one CTA per SM: polls and tree evaluation
   } else {
     int maxc = 0;
-    FC_CUDA(c, (cudaError_t)fc_oneshot_max_ctas(mode, rd, &maxc));
+    FC_CUDA(c, (cudaError_t)fc_oneshot_max_ctas(mode, rd, c->nranks, &maxc));
     P.ctas_per_rank = std::min(c->sm_count, maxc / c->nlocal);
     if (P.ctas_per_rank < 1)
       return fail(c, FC_ERR_UNSUPPORTED, "device cannot co-schedule %d one-shot ranks", c->nlocal);

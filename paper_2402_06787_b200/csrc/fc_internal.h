@@ -207,7 +207,7 @@ int fc_max_ctas_per_sm(int reduce_dtype, int* out);
 int fc_warps_per_cta();
 int fc_nvls_launch(const FcNvlsParams& p, int ctas, void* stream);
 // grid size for the one-shot kernels (modes 6/7/8): every CTA co-resident
-int fc_oneshot_max_ctas(int mode, int dtype, int* out);
+int fc_oneshot_max_ctas(int mode, int dtype, int nranks, int* out);
 
 // Copy-engine path of the 2-rank forest (fc_ce.cu).  Its flag slots are
 // 64-bit words at the end of each rank's flag area: FC_CE_READY + r holds

@@ -648,6 +648,34 @@ __global__ void __launch_bounds__(FC_NVLS_THREADS) fc_oneshot_ag128_kernel(const
   oneshot_finish(V, P, e);
 }
 
+// A chain in-tree over one 8-byte word, operands in post-order (leaf first):
+// the leaf forwards its raw value, every later node adds its own value to
+// the partial below and rounds once; AVG scales at the root (the last).
+template <int DT, int NR>
+__device__ __forceinline__ unsigned long long chain_eval(const FcNvlsParams& P,
+                                                         const unsigned long long* x, int n) {
+  using R = Red<DT>;
+  using E = typename R::E;
+  constexpr int EPU = 8 / (int)sizeof(E);
+  unsigned long long part = x[0];
+#pragma unroll
+  for (int i = 1; i < NR; ++i) {
+    if (i >= n) break;
+    const E* xv = reinterpret_cast<const E*>(&x[i]);
+    const E* pv = reinterpret_cast<const E*>(&part);
+    unsigned long long o;
+    E* oe = reinterpret_cast<E*>(&o);
+#pragma unroll
+    for (int m = 0; m < EPU; ++m) {
+      typename R::A acc = R::add(R::to(xv[m]), R::to(pv[m]));
+      if (P.op == FC_AVG && i == n - 1) acc = R::mul(acc, P.scale);
+      oe[m] = R::from(acc);
+    }
+    part = o;
+  }
+  return part;
+}
+
 // Two-hop allreduce (mode 9) / reduce-scatter (mode 10) for mid-size buffers
 // on a single-switch forest (FC_PLAN_ONEHOP).  Hop 1: every rank stores its
 // input's shard q, as LL128 lines in shard coordinates (line l = shard bytes
@@ -659,7 +687,7 @@ __global__ void __launch_bounds__(FC_NVLS_THREADS) fc_oneshot_ag128_kernel(const
 // arrived lines to its output -- the forest's allgather load.  Two hops in
 // place of the in-trees' and out-trees' depths; staging halves alternate by
 // epoch parity as for every LL128 writer.
-template <int DT>
+template <int DT, int NR>
 __global__ void __launch_bounds__(FC_NVLS_THREADS) fc_twohop128_kernel(const __grid_constant__ FcNvlsParams P) {
   using E = typename Red<DT>::E;
   const OneshotView V = oneshot_view(P);
@@ -670,6 +698,29 @@ __global__ void __launch_bounds__(FC_NVLS_THREADS) fc_twohop128_kernel(const __g
   const unsigned long long flag = e;
   const bool ar = P.mode == 9;
   const int N = P.nranks, me = V.rank;
+  // k = 1 with a chain in-tree (every node at most one child: the
+  // single-switch forests): senders are polled in the chain's post-order, so
+  // the evaluation below runs in registers, leaf to root
+  __shared__ int s_chain[FC_MAXR];
+  __shared__ int s_is_chain;
+  if (threadIdx.x == 0) {
+    s_is_chain = 0;
+    if (P.k == 1)
+      for (int ti = 0; ti < P.os_ntrees; ++ti) {
+        const int* T = P.os_trees + (long long)ti * FC_OS_TREE_WORDS;
+        if (__ldg(T + OS_ROOT) != me) continue;
+        int chain = __ldg(T + OS_NPOST) == N;
+        for (int a = 0; a < N && chain; ++a) {
+          const int v = __ldg(T + OS_POST + a);
+          s_chain[a] = v;
+          chain = __ldg(T + OS_NCH + v) == (a == 0 ? 0 : 1) &&
+                  (a == 0 || __ldg(T + OS_CH + v * FC_MAXR) == s_chain[a - 1]);
+        }
+        s_is_chain = chain;
+      }
+  }
+  __syncthreads();
+  const bool is_chain = s_is_chain != 0;
   const long long es = (long long)sizeof(E);
   const long long S = P.shard_elems;
   const long long total = ar ? P.count : S * N;  // elements of the input buffer
@@ -686,10 +737,13 @@ __global__ void __launch_bounds__(FC_NVLS_THREADS) fc_twohop128_kernel(const __g
   const long long gid = (V.cta * blockDim.x + threadIdx.x) >> 3;
   const long long ngrp = (V.nctas * blockDim.x) >> 3;
   const long long p_lane = 16LL * gl;
-  // hop 1: shard q of the own input -> rank q's staging (the own shard too)
+  // hop 1: shard q of the own input -> rank q's staging (the own shard too).
+  // Line-major with destinations rotated by the sender's rank: at any moment
+  // every rank receives from every sender alike (a destination-major order
+  // makes all senders hit one rank's ingress link at a time)
   for (long long j = gid; j < (long long)N * Lmax; j += ngrp) {
-    const int q = (int)(j / Lmax);
-    const long long l = j - (long long)q * Lmax;
+    const long long l = j / N;
+    const int q = (int)((j - l * N + me) % N);
     const long long Bq = shard_bytes(q);
     if (120 * l >= Bq) continue;
     const char* src = V.send + (long long)q * S * es;
@@ -712,19 +766,60 @@ __global__ void __launch_bounds__(FC_NVLS_THREADS) fc_twohop128_kernel(const __g
   for (long long lb = 4 * wid; lb < Lme && ok; lb += 4 * nw) {
     const long long l = lb + (lane >> 3);
     const bool valid = l < Lme;
+    // every sender's line at once: NR loads in flight, one flag check
     unsigned long long x0[FC_MAXR], x1[FC_MAXR];
-    for (int q = 0; q < N && ok; ++q)
-      ok = poll_line(V.stage + rs_area + (long long)q * slot + 128 * l + 16 * gl, valid, flag, lane,
-                     x0[q], x1[q], V.ctl, t0, P.timeout_ns, FC_DEVERR_TIMEOUT_RS);
+    unsigned long long c0 = 0, c1 = 0;  // chain: the evaluated words
+    for (unsigned it = 0;; ++it) {
+      unsigned long long a[NR], b[NR];
+      int mine_ok = 1;
+#pragma unroll
+      for (int q = 0; q < NR; ++q) {
+        a[q] = 0;
+        b[q] = flag;
+        const int src = is_chain ? s_chain[q < N ? q : 0] : q;  // chain: post-order
+        if (q < N && valid)
+          asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];"
+                       : "=l"(a[q]), "=l"(b[q])
+                       : "l"(V.stage + rs_area + (long long)src * slot + 128 * l + 16 * gl)
+                       : "memory");
+        mine_ok &= (gl != 7 || b[q] == flag) ? 1 : 0;
+      }
+      const int grp_ok = __shfl_sync(0xffffffffu, mine_ok, (lane & ~7) | 7);
+      if (__all_sync(0xffffffffu, grp_ok)) {
+        if (is_chain) {  // leaf to root in registers: one rounding per hop
+          c0 = chain_eval<DT, NR>(P, a, N);
+          c1 = chain_eval<DT, NR>(P, b, N);
+        } else {
+#pragma unroll
+          for (int q = 0; q < NR; ++q) {
+            x0[q] = a[q];
+            x1[q] = b[q];
+          }
+        }
+        break;
+      }
+      if ((it & 1023u) == 1023u) {
+        int bad = 0;
+        if (lane == 0 && (*reinterpret_cast<volatile unsigned*>(&V.ctl->error) != 0 ||
+                          (long long)(globaltimer() - t0) > P.timeout_ns)) {
+          atomicCAS(&V.ctl->error, 0u, (unsigned)FC_DEVERR_TIMEOUT_RS);
+          bad = 1;
+        }
+        if (__shfl_sync(0xffffffffu, bad, 0)) {
+          ok = false;
+          break;
+        }
+      }
+    }
     if (!ok) break;
     const long long pb = 120 * l + p_lane;
     unsigned long long r0 = 0, r1 = gl < 7 ? 0ull : flag;
     if (valid && pb + 8 <= Bme) {
-      r0 = tree_word<DT>(P, !ar, me, base_me + pb, x0);
+      r0 = is_chain ? c0 : tree_word<DT>(P, !ar, me, base_me + pb, x0);
       st_u64_any(out_me + pb, r0);
     }
     if (valid && gl < 7 && pb + 16 <= Bme) {
-      r1 = tree_word<DT>(P, !ar, me, base_me + pb + 8, x1);
+      r1 = is_chain ? c1 : tree_word<DT>(P, !ar, me, base_me + pb + 8, x1);
       st_u64_any(out_me + pb + 8, r1);
     }
     if (ar && valid) {  // hop 2: the reduced line to every peer
@@ -760,15 +855,21 @@ __global__ void __launch_bounds__(FC_NVLS_THREADS) fc_twohop128_kernel(const __g
 }  // namespace
 
 namespace {
-const void* oneshot_fn(int mode, int dtype) {
+const void* oneshot_fn(int mode, int dtype, int nranks) {
   if (mode == 8) return (const void*)fc_oneshot_ag128_kernel;
   if (mode == 9 || mode == 10) {
-    switch (dtype) {
-      case FC_BFLOAT16: return (const void*)fc_twohop128_kernel<FC_BFLOAT16>;
-      case FC_FLOAT16: return (const void*)fc_twohop128_kernel<FC_FLOAT16>;
-      case FC_INT32: return (const void*)fc_twohop128_kernel<FC_INT32>;
-      default: return (const void*)fc_twohop128_kernel<FC_FLOAT32>;
-    }
+#define FC_TWOHOP(NR)                                                             \
+  switch (dtype) {                                                                \
+    case FC_BFLOAT16: return (const void*)fc_twohop128_kernel<FC_BFLOAT16, NR>;   \
+    case FC_FLOAT16: return (const void*)fc_twohop128_kernel<FC_FLOAT16, NR>;     \
+    case FC_INT32: return (const void*)fc_twohop128_kernel<FC_INT32, NR>;         \
+    default: return (const void*)fc_twohop128_kernel<FC_FLOAT32, NR>;             \
+  }
+    if (nranks <= 2) FC_TWOHOP(2)
+    if (nranks <= 4) FC_TWOHOP(4)
+    if (nranks <= 8) FC_TWOHOP(8)
+    FC_TWOHOP(16)
+#undef FC_TWOHOP
   }
   switch (dtype) {
     case FC_BFLOAT16: return (const void*)fc_oneshot128_kernel<FC_BFLOAT16>;
@@ -779,9 +880,9 @@ const void* oneshot_fn(int mode, int dtype) {
 }
 }  // namespace
 
-int fc_oneshot_max_ctas(int mode, int dtype, int* out) {
+int fc_oneshot_max_ctas(int mode, int dtype, int nranks, int* out) {
   int per_sm = 0, dev = 0, sms = 0;
-  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, oneshot_fn(mode, dtype),
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, oneshot_fn(mode, dtype, nranks),
                                                                 FC_NVLS_THREADS, 0);
   if (e == cudaSuccess) e = cudaGetDevice(&dev);
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -798,7 +899,7 @@ int fc_nvls_launch(const FcNvlsParams& p, int ctas, void* stream) {
   if (p.mode >= 6) {
     // tree-engine one-shot: ctas_per_rank CTAs per local rank; ranks of one
     // grid wait on each other, so several local ranks need co-residency
-    fn = oneshot_fn(p.mode, p.dtype);
+    fn = oneshot_fn(p.mode, p.dtype, p.nranks);
     const dim3 grid(p.nlocal * p.ctas_per_rank);
     if (p.nlocal > 1)
       return (int)cudaLaunchCooperativeKernel(fn, grid, dim3(FC_NVLS_THREADS), args, 0,
