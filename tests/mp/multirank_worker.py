@@ -39,7 +39,7 @@ def main():
                              options={"timeout_ms": 20000})
         for proto in (-1, 0):
             comm.set_option("proto", proto)
-            for S in (1000, 1 << 18):
+            for S in (1000, 1 << 18, 1 << 20):  # one-hop / one-shot, two-hop, LL128 / flags
                 g = torch.Generator().manual_seed(S + proto)
                 sends = [torch.randn(S, generator=g) for _ in range(N)]
                 outs = [torch.empty(N * S, device=dev) for _ in mine]
