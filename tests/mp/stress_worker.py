@@ -28,14 +28,15 @@ def main():
                           scratch_bytes=256 << 20, options={"timeout_ms": 20000})
     rng = random.Random(1234)  # same sequence on every rank
     # a few persistent (registered) output buffers, reused across calls
-    pools = {dt: comm.empty(n * (1 << 21), dtype=dt) for dt in (torch.float32, torch.int32)}
+    pools = {dt: comm.empty(n * (1 << 22), dtype=dt) for dt in (torch.float32, torch.int32)}
     fails = 0
     for it in range(iters):
         coll = rng.choice(["allgather", "reduce_scatter", "allreduce"])
         proto = rng.choice([-1, 0])
         comm.set_option("proto", proto)
         comm.set_option("chunk_max", rng.choice([16 << 10, 64 << 10, 256 << 10]))
-        S = rng.choice([1, 17, 256, 4096, 65536 + 8, 1 << 20, (1 << 21) - 4])
+        # up to the copy-engine (N=2, >= 24 MiB output) and two-hop (2-12 MiB) ranges
+        S = rng.choice([1, 17, 256, 4096, 65536 + 8, 1 << 18, 1 << 20, (1 << 21) - 4, 1 << 22])
         g = torch.Generator().manual_seed(it)
         if coll == "allgather":
             allin = torch.randint(-2**31, 2**31 - 1, (n, S), generator=g, dtype=torch.int32)
