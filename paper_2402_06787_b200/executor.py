@@ -342,6 +342,8 @@ class ForestCollComm(_CommBase):
             while target < need.value:
                 target *= 2
             self._grow_to(min(target, self._max_scratch))
+        if len(self._scratch_ok) > 4096:  # many distinct sizes: keep the memo bounded
+            self._scratch_ok.clear()
         self._scratch_ok.add(key)
 
     def _grow_to(self, nbytes: int) -> None:
