@@ -27,13 +27,23 @@ def timeline(rec):
 
 
 def main():
+    import argparse
+
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--sizes", default="64,65536", help="elements per rank (fp32)")
+    ap.add_argument("--opt", action="append", default=[])
+    ap.add_argument("--reps", type=int, default=300)
+    args = ap.parse_args()
     local = int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
     dev = torch.device(f"cuda:{local}")
     dist.init_process_group("nccl", device_id=dev)
     rank, n = dist.get_rank(), dist.get_world_size()
     comm = ForestCollComm(nvswitch_doc(n), rank=rank, world_size=n, device=local)
-    for S in (64, 1 << 16):
+    for o in args.opt:
+        k, v = o.split("=")
+        comm.set_option(k, int(v))
+    for S in [int(x) for x in args.sizes.split(",")]:
         inp = torch.randn(S, device=dev)
         out = comm.empty(n * S)
         f = lambda: comm.all_gather(out, inp)  # noqa: E731
@@ -45,7 +55,7 @@ def main():
             if mode == "eager":
                 dist.barrier()
                 torch.cuda.synchronize()
-                for _ in range(300):
+                for _ in range(args.reps):
                     f()
             else:
                 s = torch.cuda.Stream()
