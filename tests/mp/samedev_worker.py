@@ -56,7 +56,9 @@ def main():
         fails = fresh_outputs(comm, rank, n, dev)
     elif mode == "mismatch":
         fails = mismatch(comm, rank, n, dev)
-    comm.check() if mode != "mismatch" else None
+    elif mode == "mismatch_ce":
+        fails = mismatch(comm, rank, n, dev, ce=True)
+    comm.check() if not mode.startswith("mismatch") else None
     print(f"RANK {rank} {'OK' if not fails else 'FAIL ' + '; '.join(fails)}", flush=True)
     comm.close()
     dist.destroy_process_group()
@@ -174,12 +176,15 @@ def grow(comm, rank, n, dev):
     return fails
 
 
-def mismatch(comm, rank, n, dev):
+def mismatch(comm, rank, n, dev, ce=False):
     """Rank 0 passes a different (registered) output than its peers: the
-    device check fails loudly instead of receiving misplaced stores."""
+    device check fails loudly instead of receiving misplaced stores (chunk
+    flags), or right after them (copy engine: the tag check runs beside the
+    copy, which stays inside the peer's registered segment)."""
     from paper_2402_06787_b200 import DeviceError
 
-    comm.set_option("proto", 0)
+    comm.set_option("proto", -1 if ce else 0)
+    comm.set_option("ce_min", 1 if ce else 0)
     comm.set_option("timeout_ms", 4000)
     S = 1 << 12
     a = torch.empty(n * S, device=dev)
@@ -189,6 +194,8 @@ def mismatch(comm, rank, n, dev):
     comm.all_gather(b, inp)
     torch.cuda.synchronize()
     comm.all_gather(b if rank == 0 else a, inp)
+    if ce and comm.last_call_info()["proto"] != "ce":
+        return [f"took {comm.last_call_info()['proto']}, not the copy-engine path"]
     try:
         comm.check()
     except DeviceError as e:

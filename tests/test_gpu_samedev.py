@@ -48,6 +48,12 @@ def test_fresh_outputs_do_not_grow_registrations():
     assert rc == 0 and out.count(" OK") >= 2, out[-4000:]
 
 
+def test_mismatched_outputs_fail_loudly_copy_engine_one_gpu():
+    rc, out = _launch("mismatch_ce", port=29655)
+    assert rc == 0 and out.count(" OK") >= 2, out[-4000:]
+    assert "different output buffer" in out, out[-4000:]
+
+
 def test_workspace_grows_on_demand_one_gpu():
     rc, out = _launch("grow", port=29654)
     assert rc == 0 and out.count(" OK") >= 2, out[-4000:]
