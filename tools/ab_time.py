@@ -78,7 +78,8 @@ def main():
             try:
                 comm.set_option(k, {"ce_min": 24 << 20, "twohop_max": 12 << 20, "oneshot_ag_max": 16 << 20,
                                     "ctas_per_rank": 128, "ll_worker_warps": 4,
-                                    "ll_chunk_max": 64 << 10, "lag": 64}.get(k, -1))
+                                    "ll_chunk_max": 64 << 10, "lag": 64, "worker_warps": 8,
+                                    "copy_mode": 1, "pdl": 1}.get(k, -1))
             except Exception:  # noqa: BLE001
                 pass
     comm.check()
