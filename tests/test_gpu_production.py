@@ -366,3 +366,41 @@ def test_twohop_reductions(dev, base, dtype, mib, offset):
             assert comm.last_call_info()["proto"] == "twohop", comm.last_call_info()
             _assert_exact(s, coll, ins, outs, dtype, op=op)
         comm.close()
+
+
+@pytest.mark.parametrize("coll,S,opts,want", [
+    ("allgather", 4096 + 2, {}, "oneshot"),
+    ("allgather", 3 * 65536, {"oneshot_ag_max": 0}, "ll128"),
+    ("allgather", 3 * 65536 + 1, {"proto": 0}, "flags"),
+    ("reduce_scatter", 2000, {}, "oneshot"),
+    ("reduce_scatter", 98304, {}, "twohop"),
+    ("reduce_scatter", 98304 + 3, {"proto": 0}, "flags"),
+    ("allreduce", 1000 * 8, {}, "oneshot"),
+    ("allreduce", 1 << 20, {}, "twohop"),
+    ("allreduce", (1 << 20) + 8, {"twohop_max": 0}, "ll128"),
+    ("allreduce", (1 << 20) + 5, {"proto": 0}, "flags"),
+])
+def test_no_writes_outside_the_output(dev, coll, S, opts, want):
+    """Guard words around every output (before and after, same allocation)
+    stay untouched on every path: no kernel writes past its buffer."""
+    comm, s = _comm(f"nvs4_{coll}", **opts)
+    n = comm.nranks
+    G = 4096  # guard elements on each side
+    gen = torch.Generator().manual_seed(S)
+    count = {"allgather": S, "reduce_scatter": n * S, "allreduce": S}[coll]
+    out_n = {"allgather": n * S, "reduce_scatter": S, "allreduce": S}[coll]
+    ins = [_rand(count, "float32", gen, dev) for _ in range(n)]
+    bigs = [torch.full((out_n + 2 * G,), -12345.0, device=dev) for _ in range(n)]
+    outs = [b[G:G + out_n] for b in bigs]
+    if coll == "allgather":
+        comm.all_gather(outs, ins)
+    elif coll == "reduce_scatter":
+        comm.reduce_scatter(outs, ins)
+    else:
+        comm.all_reduce(ins, outs=outs)
+    comm.check()
+    assert comm.last_call_info()["proto"] == want, comm.last_call_info()
+    for b in bigs:
+        assert torch.all(b[:G] == -12345.0) and torch.all(b[G + out_n:] == -12345.0)
+    _assert_exact(s, coll, ins, outs, "float32")
+    comm.close()
