@@ -56,6 +56,8 @@ def main():
         fails = fresh_outputs(comm, rank, n, dev)
     elif mode == "mismatch":
         fails = mismatch(comm, rank, n, dev)
+    elif mode == "guards":
+        fails = guards(comm, rank, n, dev)
     elif mode == "mismatch_ce":
         fails = mismatch(comm, rank, n, dev, ce=True)
     comm.check() if not mode.startswith("mismatch") else None
@@ -173,6 +175,44 @@ def grow(comm, rank, n, dev):
     if not raised:
         fails.append("capture needing a larger workspace did not raise")
     torch.cuda.synchronize()
+    return fails
+
+
+def guards(comm, rank, n, dev):
+    """Peer stores land only inside each peer's output: guard words around
+    the outputs (same allocation, so inside the registered segment) stay
+    untouched on the copy-engine, chunk-flag and LL128 paths, allgather and
+    allreduce."""
+    fails = []
+    G = 8192
+    s_ag, s_ar = comm.schedule("allgather"), comm.schedule("allreduce")
+    for label, opts in (("ce", {"ce_min": 1, "proto": -1}), ("flags", {"ce_min": 0, "proto": 0}),
+                        ("ll128", {"ce_min": 0, "proto": 1})):
+        for k, v in opts.items():
+            comm.set_option(k, v)
+        S = 3 * 65536
+        ins = [seeded(S, torch.float32, 4000 + r) for r in range(n)]
+        big = torch.full((n * S + 2 * G,), -7.0, device=dev)
+        out = big[G:G + n * S]
+        comm.all_gather(out, ins[rank].to(dev))
+        torch.cuda.synchronize()
+        if not (torch.all(big[:G] == -7.0) and torch.all(big[G + n * S:] == -7.0)):
+            fails.append(f"{label} allgather wrote outside its output")
+        _check(out.cpu().numpy(), fo.allgather(s_ag, [x.numpy() for x in ins])[rank],
+               f"{label} allgather", fails)
+        if label != "ce":
+            cnt = n * S
+            ains = [seeded(cnt, torch.float32, 5000 + r) for r in range(n)]
+            big = torch.full((cnt + 2 * G,), -7.0, device=dev)
+            buf = big[G:G + cnt]
+            buf.copy_(ains[rank].to(dev))
+            comm.all_reduce(buf)
+            torch.cuda.synchronize()
+            if not (torch.all(big[:G] == -7.0) and torch.all(big[G + cnt:] == -7.0)):
+                fails.append(f"{label} allreduce wrote outside its buffer")
+            _check(buf.cpu().numpy(), fo.allreduce(s_ar, [x.numpy() for x in ains], "float32")[rank],
+                   f"{label} allreduce", fails)
+    comm.set_option("proto", -1)
     return fails
 
 

@@ -54,6 +54,11 @@ def test_mismatched_outputs_fail_loudly_copy_engine_one_gpu():
     assert "different output buffer" in out, out[-4000:]
 
 
+def test_peer_stores_stay_inside_outputs_one_gpu():
+    rc, out = _launch("guards", port=29656)
+    assert rc == 0 and out.count(" OK") >= 2, out[-4000:]
+
+
 def test_workspace_grows_on_demand_one_gpu():
     rc, out = _launch("grow", port=29654)
     assert rc == 0 and out.count(" OK") >= 2, out[-4000:]
