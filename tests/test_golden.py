@@ -85,3 +85,26 @@ def test_appendix_a_forest_shape():
     rows = {rt.root: " ".join(f"{e.src[1:]}>{e.dst[1:]}" for e in rt.batches[0].edges) for rt in s.roots}
     assert rows["g0"] == "0>1 0>2 0>3 0>4 4>7 7>6 6>5"
     assert rows["g7"] == "7>6 6>5 5>4 4>3 3>2 2>1 1>0"
+
+
+@pytest.mark.parametrize("beta,fixed_k", [(450, 1), (450, 3), (100, 2)])
+def test_t_star_uses_congestion_time_for_fixed_k(beta, fixed_k):
+    """fixed_k schedules are not marked exact (schedule.py:78-81): T* comes
+    from the reference's own congestion_time over the topology
+    (verify.py:537-562), allreduce summing its two phases."""
+    import json
+    from fractions import Fraction
+
+    from paper_2402_06787_b200._refpath import require_collsched
+    from paper_2402_06787_b200.schedule_io import t_star_seconds
+    from paper_2402_06787_b200.topology import groups_switch_doc
+
+    cs = require_collsched()
+    doc = groups_switch_doc(beta)
+    t = cs.parse_topology(json.dumps(doc))
+    M = 1 << 30
+    for coll in ("allgather", "allreduce"):
+        s, _ = cs.generate(t, coll, fixed_k=fixed_k)
+        assert not s.exact
+        want = float(Fraction(cs.congestion_time(s, t))) * M / 1e9
+        assert t_star_seconds(s, M, coll, doc) == pytest.approx(want, rel=1e-12)
