@@ -353,6 +353,7 @@ class ForestCollComm(_CommBase):
         import torch.distributed as dist
 
         torch.cuda.synchronize(self.device)
+        self.check()  # a sticky device error must surface, not vanish with the old workspace
         if self._group is not None:
             dist.barrier(group=self._group)
         _lib.check(self._lib.fc_comm_grow(self._comm, int(nbytes)), self._comm, "comm_grow")
