@@ -335,7 +335,8 @@ def run_single(args):
         "config": {"workload": workload, "topology": "nvswitch(8) forest from collsched.generate",
                    "ranks": "8 virtual ranks on cuda:0", "M_bytes": M, "shard_bytes": S_bytes,
                    "l2": "inputs+outputs (4.5 GiB) larger than L2; no flush",
-                   "chunks_per_tree": info["nchunks"], "ctas_per_rank": comm.get_option("ctas_per_rank")},
+                   "chunks_per_tree": info["nchunks"], "ctas_per_rank": comm.get_option("ctas_per_rank"),
+                   "path": info["proto"]},
         "t_star_ms_nvlink_model": round(tstar * 1e3, 4),
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "peak_kind": peak_kind,
@@ -447,6 +448,9 @@ def run_multi(args):
                        "topology": f"nvswitch({n}) from {topo_kind} ingestion, collsched forest",
                        "M_bytes": M, "shard_bytes": S * 4, "parallelism": f"{n} ranks, 1 per GPU",
                        "l2": "M larger than L2; no flush", "chunks_per_tree": info["nchunks"],
+                       "path": info["proto"] + (" (copy engine moves each tree edge; SM kernels "
+                                                "synchronise and place the own shard)"
+                                                if info["proto"] == "ce" else ""),
                        "ctas_per_rank": comm.get_option("ctas_per_rank")},
             "frac_of_t_star": round(tstar * 1e3 / ms, 4),
             "t_star_ms": round(tstar * 1e3, 4),
