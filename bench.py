@@ -407,6 +407,15 @@ def run_multi(args):
     alg = gbs(M, ms)
     ingress = (n - 1) * M // n
     achieved = gbs(ingress, ms)
+    # the SM kernel on the same call when the copy engine carried the headline
+    sm_alt = None
+    if info["proto"] == "ce":
+        comm.set_option("ce_min", 0)
+        ms_sm = timed(fn, args.steps, args.warmup, dist)
+        sm_alt = {"path": comm.last_call_info()["proto"], "ms": round(ms_sm, 4),
+                  "algbw_GBps": round(gbs(M, ms_sm), 2),
+                  "frac_of_t_star": round(tstar * 1e3 / ms_sm, 4)}
+        comm.set_option("ce_min", 24 << 20)
     # kernel-issued peer bytes of one call (the NVLink traffic evidence)
     issued, tinfo = issued_peer_bytes(comm, fn, dist)
     if tinfo and tinfo["proto"] == "ce":
@@ -476,6 +485,8 @@ def run_multi(args):
             "nccl": {"ms": round(nccl_ms, 4), "algbw_GBps": round(gbs(M, nccl_ms), 2),
                      "bitexact_vs_forestcoll": ok},
         }
+        if sm_alt is not None:
+            line["sm_kernel_path"] = sm_alt
         line.update(extra)
         print(json.dumps(line), flush=True)
     comm.close()
