@@ -17,6 +17,17 @@ def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200, sm_100a)")
 
 
+def pytest_collection_modifyitems(config, items):
+    """A hung device wait must not hang the run: every GPU test gets a
+    generous wall-clock limit (pytest-timeout) unless it sets its own; the
+    kernels' own flag-wait timeouts fire well before it."""
+    if not config.pluginmanager.hasplugin("timeout"):
+        return
+    for item in items:
+        if item.get_closest_marker("gpu") and not item.get_closest_marker("timeout"):
+            item.add_marker(pytest.mark.timeout(1800))
+
+
 def golden_names(collective=None):
     names = []
     for p in sorted(glob.glob(os.path.join(GOLDEN, "schedules", "*.json"))):
