@@ -217,3 +217,23 @@ def test_cli_run_subcommand(dev, tmp_path):
         assert r.returncode == 0, r.stderr[-2000:]
         line = json.loads(r.stdout.strip().splitlines()[-1])
         assert line["collective"] == coll and line["ranks"] == 4 and line["ms"] > 0
+
+
+def test_cli_run_executes_a_schedule_json(dev):
+    """`run -s` executes a schedule given in the reference's wire format
+    (parse_schedule, schedule.py:439-448), here the sparse groups forest."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    from conftest import GOLDEN, REPO
+
+    for name, coll in (("groups300_allgather", "allgather"), ("nvs4_allreduce", "allreduce")):
+        path = os.path.join(GOLDEN, "schedules", name + ".json")
+        r = subprocess.run([sys.executable, "-m", "paper_2402_06787_b200", "run", "-s", path,
+                            "--collective", coll, "--mib", "8", "--steps", "3"],
+                           cwd=REPO, capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0, r.stderr[-2000:]
+        line = json.loads(r.stdout.strip().splitlines()[-1])
+        assert line["collective"] == coll and line["ms"] > 0
