@@ -47,6 +47,32 @@ def main():
     rep = cs.validate_schedule(star, t, meta)
     if rank == 0:
         print(f"star valid: {rep.ok} {[v.kind for v in rep.violations][:3]}", flush=True)
+    import collsched.schedule as CS
+
+    star_rs = CS.reverse_for_reduce_scatter(star)
+    star_ar = CS.combine_allreduce(star_rs, star)
+    if "--ar" in sys.argv:  # allreduce / reduce-scatter, star vs chain, LL128
+        for name, scheds in (("chain", {"allreduce": get_schedule(doc, "allreduce", validate=False),
+                                        "reduce_scatter": get_schedule(doc, "reduce_scatter",
+                                                                       validate=False)}),
+                             ("star", {"allreduce": star_ar, "reduce_scatter": star_rs})):
+            comm = ForestCollComm(doc, schedules=scheds, device=local,
+                                  options={"oneshot_max": 0, "twohop_max": 0})
+            for mib in (4, 8, 16, 25, 64, 256):
+                M = mib * MIB
+                buf = comm.empty(M // 2, dtype=torch.bfloat16)
+                buf.normal_()
+                ms = timed(lambda: comm.all_reduce(buf), max(5, int(0.03 / (M / 3e11))), 3, dist)
+                rin = torch.randn(M // 2, device=dev).to(torch.bfloat16)
+                rout = torch.empty(M // 2 // n, device=dev, dtype=torch.bfloat16)
+                ms2 = timed(lambda: comm.reduce_scatter(rout, rin), max(5, int(0.03 / (M / 6e11))), 3, dist)
+                if rank == 0:
+                    print(f"{name:5s} AR {mib:4d} MiB {comm.last_call_info()['proto']:6s} "
+                          f"{gbs(M, ms):7.1f} GB/s | RS {gbs(M, ms2):7.1f} GB/s", flush=True)
+                comm.deregister(buf)
+            comm.close()
+        dist.destroy_process_group()
+        return
     for name, sched in (("chain", chain), ("star", star)):
         comm = ForestCollComm(doc, schedules={"allgather": sched}, device=local,
                               options={"oneshot_ag_max": 0, "ce_min": 0})
