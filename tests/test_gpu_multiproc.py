@@ -111,3 +111,26 @@ def test_eight_rank_forests_over_nvlink(n):
     out = r.stdout + r.stderr
     assert r.returncode == 0 and out.count(" OK") >= n, out[-4000:]
 
+
+
+def test_cli_run_one_rank_per_gpu(tmp_path):
+    """`torchrun ... -m paper_2402_06787_b200 run` times the forest with one
+    rank per GPU and reports the fraction of T*."""
+    if _ngpus() < 2:
+        pytest.skip("needs 2 GPUs")
+    import json
+
+    from paper_2402_06787_b200.topology import nvswitch_doc
+
+    topo = tmp_path / "nvs2.json"
+    topo.write_text(json.dumps(nvswitch_doc(2)))
+    for coll in ("allgather", "allreduce"):
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+               "--master-addr", "127.0.0.1", "--master-port", "29721", "-m", "paper_2402_06787_b200",
+               "run", "-t", str(topo), "--collective", coll, "--mib", "64", "--steps", "5"]
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=600,
+                           cwd=os.path.dirname(HERE))
+        assert r.returncode == 0, (r.stdout + r.stderr)[-3000:]
+        line = json.loads([x for x in r.stdout.splitlines() if x.startswith("{")][-1])
+        assert line["ranks"] == 2 and line["mode"] == "2 ranks, one per GPU"
+        assert 0 < line["frac_of_t_star"] < 1.0
