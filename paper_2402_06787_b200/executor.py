@@ -168,6 +168,8 @@ class _CommBase:
                    self._comm, f"set_option({name})")
         if hasattr(self, "_scratch_ok"):
             self._scratch_ok.clear()  # options change paths (and their workspace needs)
+        if hasattr(self, "_paths"):
+            self._paths.clear()
         if name == "nvls_ll_max":
             self._nvls_ll_max = int(value)
         if name == "nvls_ll_red_max":
@@ -290,6 +292,7 @@ class ForestCollComm(_CommBase):
         self._grow = scratch_bytes is None
         self._max_scratch = int(max_scratch_bytes)
         self._scratch_ok = set()  # (collective, count, dtype) needing no growth
+        self._paths = {}  # (collective, count, dtype) -> fc_call_path
         comm = ctypes.c_void_p()
         init = INITIAL_SCRATCH if scratch_bytes is None else int(scratch_bytes)
         _lib.check(self._lib.fc_comm_init(rank, world_size, device, init, ctypes.byref(comm)),
@@ -357,6 +360,7 @@ class ForestCollComm(_CommBase):
         if self._group is not None:
             dist.barrier(group=self._group)
         _lib.check(self._lib.fc_comm_grow(self._comm, int(nbytes)), self._comm, "comm_grow")
+        self._paths.clear()  # staging-dependent choices may change with the size
         self._connect()
 
     # -- NVLS (multicast) engine ----------------------------------------------
@@ -543,12 +547,21 @@ class ForestCollComm(_CommBase):
 
     def _call_path(self, collective: str, count: int, code: int) -> int:
         """fc_call_path: 0 chunk flags, 1 LL128, 4 one-hop / one-shot, 5 copy
-        engine, -1 empty."""
+        engine, 7 two-hop, -1 empty.  Memoised per (collective, count, dtype):
+        the answer changes only with the options or the workspace size, which
+        clear the memo."""
+        key = (collective, count, code)
+        path = self._paths.get(key)
+        if path is not None:
+            return path
         self.plan(collective)
-        path = ctypes.c_int()
+        out = ctypes.c_int()
         _lib.check(self._lib.fc_call_path(self._comm, COLL_CODE[collective], count, code,
-                                          ctypes.byref(path)), self._comm, "call_path")
-        return path.value
+                                          ctypes.byref(out)), self._comm, "call_path")
+        if len(self._paths) > 4096:
+            self._paths.clear()
+        self._paths[key] = out.value
+        return out.value
 
     def _switch_order(self, order) -> bool:
         order = self.reduction_order if order is None else order
