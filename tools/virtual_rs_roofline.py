@@ -49,10 +49,15 @@ def main():
     ap.add_argument("--dtype", default="bfloat16")
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--opt", action="append", default=[], help="option=value")
     args = ap.parse_args()
     dev = torch.device("cuda:0")
     n = args.n
-    comm = VirtualComm(nvswitch_doc(n), device=0, options={"proto": 0})
+    opts = {"proto": 0}
+    for o in args.opt:
+        k, v = o.split("=")
+        opts[k] = int(v)
+    comm = VirtualComm(nvswitch_doc(n), device=0, options=opts)
     dt = getattr(torch, args.dtype)
     es = torch.tensor([], dtype=dt).element_size()
     S = args.mib * MIB // es
@@ -70,7 +75,7 @@ def main():
                       "achieved_GBps": round(gbs(nbytes, ms), 1), "peak_GBps": peak,
                       "peak_kind": kind, "frac": round(gbs(nbytes, ms) / peak, 4),
                       "proto": info["proto"], "launches": info["launches"],
-                      "grid": info["grid"]}), flush=True)
+                      "grid": info["grid"], "options": opts}), flush=True)
     comm.close()
 
 
