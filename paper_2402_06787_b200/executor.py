@@ -885,9 +885,11 @@ class Executor:
     """§8b surface: ``Executor(schedule_or_path, topology, rank, world, device)``.
 
     Accepts a reference ``Schedule``, its JSON text, or a path to the JSON
-    (``parse_schedule``, schedule.py:439-448); validates it against the
-    topology when the reference is importable (verify.py:478-534) before
-    lowering.  ``virtual=True`` executes all ranks on one device.
+    (``parse_schedule``, schedule.py:439-448); with a topology it validates
+    the schedule against it (``validate_schedule``, verify.py:478-534) before
+    lowering, as the reference CLI does.  ``virtual=True`` executes all ranks
+    on one device; other keywords (options, reduction_order, ...) go to the
+    communicator.
     """
 
     def __init__(self, schedule_or_path, topology=None, rank=None, world=None, device=None,
