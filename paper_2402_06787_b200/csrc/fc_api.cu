@@ -793,13 +793,17 @@ int default_ctas(fc_comm* c) {
   c->sm_count = sms;
   const int cap = per_sm * sms / c->nlocal;
   if (cap < 1) return fail(c, FC_ERR_UNSUPPORTED, "device cannot co-schedule %d ranks", c->nlocal);
-  c->ctas_per_rank = std::min(c->virt ? std::max(1, 128 / c->nlocal) : 128, cap);
+  // virtual mode: every SM (one co-resident grid; 18 CTAs per rank at N=8 measured +2 %
+  // over 16 on the N=1 bench workload, tools/exp_n1_r02.sh)
+  c->ctas_per_rank = std::min(c->virt ? std::max(1, sms / c->nlocal) : 128, cap);
   c->worker_warps = c->virt ? 1 : 8;
   c->ll_worker_warps = c->virt ? 1 : 4;
   // virtual ranks share one HBM: LL staging doubles the traffic, so keep it for small calls
   if (c->virt) c->ll_max = 16LL << 20;
   // all ranks share one HBM and one grid: no drain to shorten (measured -1 % with tail 4)
   if (c->virt) c->chunk_tail = 0;
+  // and finer chunks keep the depth-7 chains' fill and drain short (128 KiB: +1.5 %)
+  if (c->virt) c->chunk_max = 128 << 10;
   return make_side_stream(c);
 }
 
