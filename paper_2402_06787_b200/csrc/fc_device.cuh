@@ -50,6 +50,9 @@
 #define FC_STAGE (8 * 1024)                // bytes per stage
 #define FC_SMEM (FC_WPC * FC_NST * FC_STAGE)
 #define FC_MAXS 17                         // max sources / destinations per item
+#ifndef FC_RED_U
+#define FC_RED_U 2                         // vectors per lane in flight in bulk_reduce
+#endif
 
 namespace {
 
@@ -513,16 +516,31 @@ __device__ void bulk_reduce(Ring& rg, const char* const* src, int nsrc, char* co
     mbar_wait(&rg.bar[q % FC_NST], (q / FC_NST) & 1u);
     const char* sb = rg.buf + (q % FC_NST) * FC_STAGE;
     const long long off = i * seg;
-    const long long len = (nbytes - off) < seg ? (nbytes - off) : seg;
-    for (long long j = lane; j < len / 16; j += 32) {
-      Acc16<DT> acc;
-      acc.init(reinterpret_cast<const uint4*>(sb)[j]);
-      for (int s = 1; s < nsrc; ++s) acc.add(reinterpret_cast<const uint4*>(sb + s * seg)[j]);
-      if constexpr (SC) {
-        if (scaled) acc.scale(sc);
+    const int nv = (int)(((nbytes - off) < seg ? (nbytes - off) : seg) / 16);
+    // RU vectors per lane in flight: 4-byte types gain from overlapping
+    // independent smem loads (fp32 virtual reduce-scatter 0.92 -> 0.95 of
+    // HBM); 2-byte types lose 2-3 % (tools/exp_redu_r02.sh)
+    constexpr int RU = sizeof(typename Red<DT>::E) == 2 ? 1 : FC_RED_U;
+    for (int j0 = lane; j0 < nv; j0 += 32 * RU) {
+      Acc16<DT> acc[RU];
+#pragma unroll
+      for (int u = 0; u < RU; ++u)
+        if (j0 + 32 * u < nv) acc[u].init(reinterpret_cast<const uint4*>(sb)[j0 + 32 * u]);
+      for (int s = 1; s < nsrc; ++s) {
+        const uint4* ss = reinterpret_cast<const uint4*>(sb + s * seg);
+#pragma unroll
+        for (int u = 0; u < RU; ++u)
+          if (j0 + 32 * u < nv) acc[u].add(ss[j0 + 32 * u]);
       }
-      const uint4 out = acc.pack();
-      for (int d = 0; d < ndst; ++d) reinterpret_cast<uint4*>(dst[d] + off0 + off)[j] = out;
+#pragma unroll
+      for (int u = 0; u < RU; ++u) {
+        if (j0 + 32 * u >= nv) break;
+        if constexpr (SC) {
+          if (scaled) acc[u].scale(sc);
+        }
+        const uint4 out = acc[u].pack();
+        for (int d = 0; d < ndst; ++d) reinterpret_cast<uint4*>(dst[d] + off0 + off)[j0 + 32 * u] = out;
+      }
     }
     __syncwarp();
     // refill the stage consumed in iteration i-1 (all lanes passed its __syncwarp)
