@@ -53,6 +53,9 @@
 #ifndef FC_RED_U
 #define FC_RED_U 2                         // vectors per lane in flight in bulk_reduce
 #endif
+#ifndef FC_RED_U2
+#define FC_RED_U2 1                        // the same for 2-byte types
+#endif
 
 namespace {
 
@@ -208,6 +211,19 @@ __device__ bool wait_ready(const FcParams& P, int me, int x, unsigned e, FcCtl* 
   return false;
 }
 
+// Element q (a compile-time constant after unrolling) of a packed vector in
+// the accumulator type.  bf16 unpacks word-wise: the low half shifted up,
+// the high half masked in place (one ALU op per element).
+template <int DT>
+__device__ __forceinline__ typename Red<DT>::A elem(const void* v, int q) {
+  if constexpr (DT == FC_BFLOAT16) {
+    const unsigned w = reinterpret_cast<const unsigned*>(v)[q >> 1];
+    return __uint_as_float((q & 1) ? (w & 0xffff0000u) : (w << 16));
+  } else {
+    return Red<DT>::to(reinterpret_cast<const typename Red<DT>::E*>(v)[q]);
+  }
+}
+
 // acc (accumulator lanes of one 16-byte vector) <- first source
 template <int DT>
 struct Acc16 {
@@ -216,14 +232,12 @@ struct Acc16 {
   static constexpr int NE = 16 / sizeof(E);
   typename R::A a[NE];
   __device__ __forceinline__ void init(const uint4& v) {
-    const E* e = reinterpret_cast<const E*>(&v);
 #pragma unroll
-    for (int q = 0; q < NE; ++q) a[q] = R::to(e[q]);
+    for (int q = 0; q < NE; ++q) a[q] = elem<DT>(&v, q);
   }
   __device__ __forceinline__ void add(const uint4& v) {
-    const E* e = reinterpret_cast<const E*>(&v);
 #pragma unroll
-    for (int q = 0; q < NE; ++q) a[q] = R::add(a[q], R::to(e[q]));
+    for (int q = 0; q < NE; ++q) a[q] = R::add(a[q], elem<DT>(&v, q));
   }
   __device__ __forceinline__ void scale(float s) {
 #pragma unroll
@@ -252,14 +266,12 @@ struct Acc8 {
   static constexpr int NE = 8 / sizeof(E);
   typename R::A a[NE];
   __device__ __forceinline__ void init(unsigned long long v) {
-    const E* e = reinterpret_cast<const E*>(&v);
 #pragma unroll
-    for (int q = 0; q < NE; ++q) a[q] = R::to(e[q]);
+    for (int q = 0; q < NE; ++q) a[q] = elem<DT>(&v, q);
   }
   __device__ __forceinline__ void add(unsigned long long v) {
-    const E* e = reinterpret_cast<const E*>(&v);
 #pragma unroll
-    for (int q = 0; q < NE; ++q) a[q] = R::add(a[q], R::to(e[q]));
+    for (int q = 0; q < NE; ++q) a[q] = R::add(a[q], elem<DT>(&v, q));
   }
   __device__ __forceinline__ void scale(float s) {
 #pragma unroll
@@ -500,6 +512,7 @@ __device__ void bulk_reduce(Ring& rg, const char* const* src, int nsrc, char* co
   const long long seg = (long long)(FC_STAGE / nsrc) & ~15LL;  // bytes per source per piece
   const long long npieces = (nbytes + seg - 1) / seg;
   const unsigned base = rg.seq;
+  char* const d0 = dst[0] + off0;  // the first destination stays in registers
   if (lane == 0) {
     for (long long i = 0; i < npieces && i < FC_NST - 1; ++i) {
       const unsigned q = base + (unsigned)i;
@@ -520,7 +533,7 @@ __device__ void bulk_reduce(Ring& rg, const char* const* src, int nsrc, char* co
     // RU vectors per lane in flight: 4-byte types gain from overlapping
     // independent smem loads (fp32 virtual reduce-scatter 0.92 -> 0.95 of
     // HBM); 2-byte types lose 2-3 % (tools/exp_redu_r02.sh)
-    constexpr int RU = sizeof(typename Red<DT>::E) == 2 ? 1 : FC_RED_U;
+    constexpr int RU = sizeof(typename Red<DT>::E) == 2 ? FC_RED_U2 : FC_RED_U;
     for (int j0 = lane; j0 < nv; j0 += 32 * RU) {
       Acc16<DT> acc[RU];
 #pragma unroll
@@ -539,7 +552,8 @@ __device__ void bulk_reduce(Ring& rg, const char* const* src, int nsrc, char* co
           if (scaled) acc[u].scale(sc);
         }
         const uint4 out = acc[u].pack();
-        for (int d = 0; d < ndst; ++d) reinterpret_cast<uint4*>(dst[d] + off0 + off)[j0 + 32 * u] = out;
+        reinterpret_cast<uint4*>(d0 + off)[j0 + 32 * u] = out;
+        for (int d = 1; d < ndst; ++d) reinterpret_cast<uint4*>(dst[d] + off0 + off)[j0 + 32 * u] = out;
       }
     }
     __syncwarp();
