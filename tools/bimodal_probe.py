@@ -3,7 +3,7 @@ window (N=4, 2 MiB: 10 us usually, 15.7 us in one of three runs) device- or
 host-side?  Times several windows of back-to-back eager calls, and of CUDA
 graph replays of the same calls, reallocating the output between windows.
 
-    torchrun --nproc-per-node 4 tools/bimodal_probe.py [MiB]
+    torchrun --nproc-per-node 4 tools/bimodal_probe.py [MiB] [option=value ...]
 """
 import os
 import sys
@@ -43,6 +43,9 @@ def main():
     rank, n = dist.get_rank(), dist.get_world_size()
     comm = ForestCollComm(nvswitch_doc(n), rank=rank, world_size=n, device=local)
     mib = float(sys.argv[1]) if len(sys.argv) > 1 else 2
+    for o in sys.argv[2:]:  # name=value executor options
+        k, v = o.split("=")
+        comm.set_option(k, int(v))
     S = int(mib * (1 << 20)) // n // 4
     inp = torch.randn(S, device=dev)
     eager, graph, host = [], [], []
