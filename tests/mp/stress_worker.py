@@ -21,12 +21,13 @@ from paper_2402_06787_b200.topology import nvswitch_doc  # noqa: E402
 
 def main():
     iters = int(sys.argv[1]) if len(sys.argv) > 1 else 200
+    seed = int(sys.argv[2]) if len(sys.argv) > 2 else 1234
     local = init()
     dev = torch.device(f"cuda:{local}")
     rank, n = dist.get_rank(), dist.get_world_size()
     comm = ForestCollComm(nvswitch_doc(n), rank=rank, world_size=n, device=local,
                           scratch_bytes=256 << 20, options={"timeout_ms": 20000})
-    rng = random.Random(1234)  # same sequence on every rank
+    rng = random.Random(seed)  # same sequence on every rank
     # a few persistent (registered) output buffers, reused across calls
     pools = {dt: comm.empty(n * (1 << 22), dtype=dt) for dt in (torch.float32, torch.int32)}
     fails = 0
