@@ -1,6 +1,7 @@
 """torchrun worker: randomized soak of back-to-back collectives (mixed
 collective, size, dtype, protocol, buffer reuse) checked against closed
-forms — allgather = concatenation, int32 reductions = exact sums.  Catches
+forms — allgather = concatenation, reductions = exact sums (int32 wrapping;
+bf16 / fp32 on small integers, exact in any order).  Catches
 races in the epoch / entry-barrier / flag protocol that single calls miss."""
 
 import os
@@ -29,7 +30,7 @@ def main():
                           scratch_bytes=256 << 20, options={"timeout_ms": 20000})
     rng = random.Random(seed)  # same sequence on every rank
     # a few persistent (registered) output buffers, reused across calls
-    pools = {dt: comm.empty(n * (1 << 22), dtype=dt) for dt in (torch.float32, torch.int32)}
+    pools = {dt: comm.empty(n * (1 << 22), dtype=dt) for dt in (torch.float32, torch.int32, torch.bfloat16)}
     fails = 0
     for it in range(iters):
         coll = rng.choice(["allgather", "reduce_scatter", "allreduce"])
@@ -44,20 +45,26 @@ def main():
             out = pools[torch.float32][: n * S].view(torch.int32)
             comm.all_gather(out, allin[rank].to(dev))
             ok = torch.equal(out.cpu(), allin.reshape(-1))
-        elif coll == "reduce_scatter":
-            allin = torch.randint(-2**20, 2**20, (n, n * S), generator=g, dtype=torch.int32)
-            out = torch.empty(S, dtype=torch.int32, device=dev)
-            comm.reduce_scatter(out, allin[rank].to(dev))
-            ok = torch.equal(out.cpu(), allin.sum(0, dtype=torch.int64).to(torch.int32)[rank * S:(rank + 1) * S])
         else:
-            allin = torch.randint(-2**20, 2**20, (n, n * S), generator=g, dtype=torch.int32)
-            buf = pools[torch.int32][: n * S]
-            buf.copy_(allin[rank].to(dev))
-            comm.all_reduce(buf)
-            ok = torch.equal(buf.cpu(), allin.sum(0, dtype=torch.int64).to(torch.int32))
+            # int32 wraps exactly; bf16 / fp32 get small integers, so every
+            # partial sum is exact in any order and the result is closed-form
+            dt = rng.choice([torch.int32, torch.bfloat16, torch.float32])
+            lim = 2**20 if dt == torch.int32 else 9
+            allin = torch.randint(-lim, lim, (n, n * S), generator=g, dtype=torch.int32)
+            want = allin.sum(0, dtype=torch.int64).to(dt)
+            src = allin[rank].to(dt).to(dev)
+            if coll == "reduce_scatter":
+                out = torch.empty(S, dtype=dt, device=dev)
+                comm.reduce_scatter(out, src)
+                ok = torch.equal(out.cpu(), want[rank * S:(rank + 1) * S])
+            else:
+                out = pools[dt][: n * S]
+                out.copy_(src)
+                comm.all_reduce(out)
+                ok = torch.equal(out.cpu(), want)
         if not ok:
             fails += 1
-            print(f"rank {rank} iter {it} {coll} S={S} proto={proto} MISMATCH", flush=True)
+            print(f"rank {rank} iter {it} {coll} S={S} proto={proto} {out.dtype} MISMATCH", flush=True)
     # bursts: several collectives queued back to back with no host sync, on two
     # alternating streams, each into its own output, verified only at the end.
     # Exercises launch-to-launch reuse of staging / scratch / flags (LL128
