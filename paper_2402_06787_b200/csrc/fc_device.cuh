@@ -531,8 +531,8 @@ __device__ void bulk_reduce(Ring& rg, const char* const* src, int nsrc, char* co
     const long long off = i * seg;
     const int nv = (int)(((nbytes - off) < seg ? (nbytes - off) : seg) / 16);
     // RU vectors per lane in flight: 4-byte types gain from overlapping
-    // independent smem loads (fp32 virtual reduce-scatter 0.92 -> 0.95 of
-    // HBM); 2-byte types lose 2-3 % (tools/exp_redu_r02.sh)
+    // independent smem loads (fp32 virtual reduce-scatter 0.976 -> 0.991 of
+    // HBM); 2-byte types lose 1 % with two (tools/exp_redu_r02.sh)
     constexpr int RU = sizeof(typename Red<DT>::E) == 2 ? FC_RED_U2 : FC_RED_U;
     for (int j0 = lane; j0 < nv; j0 += 32 * RU) {
       Acc16<DT> acc[RU];
