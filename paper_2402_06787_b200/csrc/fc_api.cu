@@ -536,7 +536,8 @@ int run(fc_comm* c, int coll, const void* const* sends, void* const* recvs, size
     // measured crossover vs the forest's LL128 at N=4: between 16 and 32 MiB
     const long long lim = c->oneshot_ag_max > 0 ? c->oneshot_ag_max : (16LL << 20);
     const long long lines = (S * es + 119) / 120;
-    if (bytes <= lim && (S * es) % 8 == 0 && (long long)N * lines * 128 <= half) {
+    // any shard length: a partial last word travels zero-padded in its line
+    if (bytes <= lim && (long long)N * lines * 128 <= half) {
       if (path_out) return decided(4, 2 * (long long)N * lines * 128);
       return run_oneshot_ag(c, sends, recvs, S * es, half, stream);
     }

@@ -117,4 +117,27 @@ __device__ __forceinline__ void st_u64_any(char* p, unsigned long long v) {
   }
 }
 
+// The first n (< 8) bytes of an 8-byte payload word at the end of a buffer
+// whose length is not a multiple of 8: loaded into the low bytes (the rest
+// zero), stored back byte by byte.
+__device__ __forceinline__ unsigned long long ld_tail(const char* p, long long n) {
+  unsigned long long v = 0;
+  for (long long i = 0; i < n; ++i)
+    v |= (unsigned long long)(unsigned char)__ldcg(reinterpret_cast<const signed char*>(p) + i) << (8 * i);
+  return v;
+}
+__device__ __forceinline__ void st_tail(char* p, unsigned long long v, long long n) {
+  for (long long i = 0; i < n; ++i) p[i] = (char)(v >> (8 * i));
+}
+
+// Word at byte offset pb of an S-byte buffer: whole, tail, or absent (0).
+__device__ __forceinline__ unsigned long long ld_word(const char* base, long long pb, long long S) {
+  if (pb + 8 <= S) return ld_u64_any(base + pb);
+  return pb < S ? ld_tail(base + pb, S - pb) : 0ull;
+}
+__device__ __forceinline__ void st_word(char* base, long long pb, long long S, unsigned long long v) {
+  if (pb + 8 <= S) st_u64_any(base + pb, v);
+  else if (pb < S) st_tail(base + pb, v, S - pb);
+}
+
 }  // namespace

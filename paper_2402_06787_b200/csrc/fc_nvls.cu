@@ -607,17 +607,13 @@ __global__ void __launch_bounds__(FC_NVLS_THREADS) fc_oneshot_ag128_kernel(const
   // 1. own shard: lines to every peer, payload to the own output slot
   for (long long l = gid; l < L; l += ngrp) {
     const long long pb = 120 * l + p_lane;
-    unsigned long long w0 = 0, w1 = flag;
-    if (pb + 8 <= S) {
-      w0 = ld_u64_any(V.send + pb);
-      st_u64_any(own + pb, w0);
-    }
+    // a shard whose length is not a multiple of 8 ends in a partial word
+    // (zero-padded in the line, stored byte by byte)
+    unsigned long long w0 = ld_word(V.send, pb, S), w1 = flag;
+    st_word(own, pb, S, w0);
     if (gl < 7) {
-      w1 = 0;
-      if (pb + 16 <= S) {
-        w1 = ld_u64_any(V.send + pb + 8);
-        st_u64_any(own + pb + 8, w1);
-      }
+      w1 = ld_word(V.send, pb + 8, S);
+      st_word(own, pb + 8, S, w1);
     }
     for (int q = 0; q < P.nranks; ++q)
       if (q != V.rank)
@@ -642,8 +638,8 @@ __global__ void __launch_bounds__(FC_NVLS_THREADS) fc_oneshot_ag128_kernel(const
     if (!valid) continue;
     char* dst = V.out + (long long)q * S;
     const long long pb = 120 * l + p_lane;
-    if (pb + 8 <= S) st_u64_any(dst + pb, a);
-    if (gl < 7 && pb + 16 <= S) st_u64_any(dst + pb + 8, b);
+    st_word(dst, pb, S, a);
+    if (gl < 7) st_word(dst, pb + 8, S, b);
   }
   oneshot_finish(V, P, e);
 }

@@ -168,16 +168,30 @@ def test_real_gpu_defaults_run_virtual(dev):
 # one-hop allgather and one-shot reductions
 # ---------------------------------------------------------------------------
 @pytest.mark.parametrize("base", ["nvs2", "nvs4", "nvs8"])
-@pytest.mark.parametrize("S", [2, 30, 1000, 4096 + 2, 65536, 1 << 20])
+@pytest.mark.parametrize("S", [1, 2, 30, 31, 333, 1000, 4096 + 2, 4097, 65536, 1 << 20])
 @pytest.mark.parametrize("offset", [0, 1])
 def test_onehop_allgather(dev, base, S, offset):
+    """Any shard length goes one hop (odd lengths end in a partial, zero-padded
+    payload word), any buffer offset."""
     comm, s = _comm(f"{base}_allgather")
     ins, outs = _run(comm, "allgather", S, "float32", dev, seed=S + offset, offset=offset)
     info = comm.last_call_info()
     bytes_out = comm.nranks * S * 4
-    if (S * 4) % 8 == 0 and bytes_out <= comm.get_option("oneshot_ag_max"):
+    if bytes_out <= comm.get_option("oneshot_ag_max"):
         assert info["proto"] == "oneshot", info
     _assert_exact(s, "allgather", ins, outs, "float32")
+    comm.close()
+
+
+@pytest.mark.parametrize("base", ["nvs2", "nvs8"])
+@pytest.mark.parametrize("S", [1, 3, 61, 1001])
+def test_onehop_allgather_odd_bf16(dev, base, S):
+    """2-byte elements: shards of 2, 6, 122 and 2002 bytes (partial last words
+    of 2 and 6 bytes), one hop, bit-exact."""
+    comm, s = _comm(f"{base}_allgather")
+    ins, outs = _run(comm, "allgather", S, "bfloat16", dev, seed=7 * S)
+    assert comm.last_call_info()["proto"] == "oneshot"
+    _assert_exact(s, "allgather", ins, outs, "bfloat16")
     comm.close()
 
 
@@ -370,6 +384,7 @@ def test_twohop_reductions(dev, base, dtype, mib, offset):
 
 @pytest.mark.parametrize("coll,S,opts,want", [
     ("allgather", 4096 + 2, {}, "oneshot"),
+    ("allgather", 4096 + 1, {}, "oneshot"),  # partial last payload word
     ("allgather", 3 * 65536, {"oneshot_ag_max": 0}, "ll128"),
     ("allgather", 3 * 65536 + 1, {"proto": 0}, "flags"),
     ("reduce_scatter", 2000, {}, "oneshot"),
