@@ -629,11 +629,9 @@ int run(fc_comm* c, int coll, const void* const* sends, void* const* recvs, size
   int proto = 0;
   long long n = 0, W = 0;
   if (c->proto != 0) {
-    bool aligned = (stride * es) % 8 == 0;  // slice offsets: rank-uniform
-    for (int r = 0; r < N && aligned; ++r) {
-      long long Sr = std::max(0LL, std::min(S, total - (long long)r * stride));
-      for (int m = 0; m <= pl.k && aligned; ++m) aligned = ((Sr * m / pl.k) * es) % 8 == 0;
-    }
+    // any slice length and offset: a slice that is not a multiple of 8 bytes
+    // ends in a partial payload word (run_item_ll)
+    const bool aligned = true;
     const long long unit_lines = (slice_unit + 119) / 120;
     const long long llu = unit_lines * 128;
     const long long rs_need = (long long)pl.max_slot_units * llu + 256LL * pl.max_slots;

@@ -888,10 +888,10 @@ __device__ void run_item_ll(const FcParams& P, int me, FcCtl* ctl, const int* T,
   if (kind == FC_K_AG_ROOT && !P.root_local_done && P.recv[me] + lo != P.send[me] + (lo - base))
     out_local = P.recv[me];
   if (kind == FC_K_RS_ROOT) out_local = P.recv[me] - base;  // out has S elements
-  // payload offsets (pay + 8*q0) are multiples of 8: the base pointers alone
-  // decide whether 8-byte vector accesses apply (warp-uniform)
-  const bool src_al = ((uintptr_t)local_src & 7) == 0;
-  const bool out_al = ((uintptr_t)out_local & 7) == 0;
+  // payload offsets (pay + 8*q0) are lo plus multiples of 8: the base
+  // pointers at lo decide whether 8-byte vector accesses apply (warp-uniform)
+  const bool src_al = ((uintptr_t)(local_src + lo) & 7) == 0;
+  const bool out_al = ((uintptr_t)(out_local + lo) & 7) == 0;
 
   // the line loop, instantiated for 8-byte aligned local buffers (plain
   // vector accesses, all loads of a batch in flight) and for any alignment
@@ -901,6 +901,9 @@ __device__ void run_item_ll(const FcParams& P, int me, FcCtl* ctl, const int* T,
       bool valid[U], v0[U], v1[U];
       long long pay[U];
       unsigned long long w0[U], w1[U];
+      // a slice whose length is not a multiple of 8 ends in a partial word:
+      // n0/n1 its bytes (zero-padded in the line), only the last line has one
+      int n0 = 0, n1 = 0;
   #pragma unroll
       for (int u = 0; u < U; ++u) {
         const long long l = lb + 4 * u + g;
@@ -908,9 +911,14 @@ __device__ void run_item_ll(const FcParams& P, int me, FcCtl* ctl, const int* T,
         pay[u] = lo + (long long)FC_LL_PAY * l;
         v0[u] = valid[u] && pay[u] + 8LL * q0 + 8 <= hi;
         v1[u] = valid[u] && two && pay[u] + 8LL * (q0 + 1) + 8 <= hi;
+        if (valid[u] && !v0[u] && pay[u] + 8LL * q0 < hi) n0 = (int)(hi - pay[u] - 8LL * q0);
+        if (valid[u] && two && !v1[u] && pay[u] + 8LL * (q0 + 1) < hi)
+          n1 = (int)(hi - pay[u] - 8LL * (q0 + 1));
         w0[u] = 0;
         w1[u] = 0;
       }
+      // the line holding the slice's last byte (its partial word, if any)
+      const long long tl = (hi - lo - 1) / FC_LL_PAY;
       if (polls) {
         const char* lp[U];
   #pragma unroll
@@ -926,6 +934,10 @@ __device__ void run_item_ll(const FcParams& P, int me, FcCtl* ctl, const int* T,
           } else {
             if (v0[u]) w0[u] = ld_u64_any(src);
             if (v1[u]) w1[u] = ld_u64_any(src + 8);
+          }
+          if (lb + 4 * u + g == tl) {
+            if (n0) w0[u] = ld_tail(src, n0);
+            if (n1) w1[u] = ld_tail(src + 8, n1);
           }
         }
         if (kind != FC_K_AG_ROOT && n_rs > 0) {
@@ -974,6 +986,10 @@ __device__ void run_item_ll(const FcParams& P, int me, FcCtl* ctl, const int* T,
             if (v0[u]) st_u64_any(o, w0[u]);
             if (v1[u]) st_u64_any(o + 8, w1[u]);
           }
+          if (lb + 4 * u + g == tl) {
+            if (n0) st_tail(o, w0[u], n0);
+            if (n1) st_tail(o + 8, w1[u], n1);
+          }
         }
       }
       // line stores to peers' staging (a per-batch local table measures 13 %
@@ -987,6 +1003,10 @@ __device__ void run_item_ll(const FcParams& P, int me, FcCtl* ctl, const int* T,
           dl[nl++] = slot_ptr(__ldg(T + TW_AG_CHILD + j), P.ll_ag_base, __ldg(T + TW_AG_CSLOT + j),
                               __ldg(T + TW_AG_CPREFIX + j));
       }
+      // one warp-wide store per line: the partial-word loads above diverge,
+      // and a line whose 8 lane stores issued apart could show its flag
+      // before its payload
+      __syncwarp();
       for (int d = 0; d < nl; ++d) {
   #pragma unroll
         for (int u = 0; u < U; ++u)

@@ -604,22 +604,31 @@ __global__ void __launch_bounds__(FC_NVLS_THREADS) fc_oneshot_ag128_kernel(const
   const long long ngrp = (V.nctas * blockDim.x) >> 3;
   const long long p_lane = 16LL * gl;
   char* own = V.out + (long long)V.rank * S;
-  // 1. own shard: lines to every peer, payload to the own output slot
-  for (long long l = gid; l < L; l += ngrp) {
+  // 1. own shard: lines to every peer, payload to the own output slot.  The
+  // loop is warp-uniform (the warp's 4 line groups step together) so every
+  // line leaves as one warp-wide store after __syncwarp.
+  for (long long lw = gid & ~3LL; lw < L; lw += ngrp) {
+    const long long l = lw + (gid & 3);
+    const bool valid = l < L;
     const long long pb = 120 * l + p_lane;
     // a shard whose length is not a multiple of 8 ends in a partial word
     // (zero-padded in the line, stored byte by byte)
-    unsigned long long w0 = ld_word(V.send, pb, S), w1 = flag;
-    st_word(own, pb, S, w0);
-    if (gl < 7) {
-      w1 = ld_word(V.send, pb + 8, S);
-      st_word(own, pb + 8, S, w1);
+    unsigned long long w0 = 0, w1 = flag;
+    if (valid) {
+      w0 = ld_word(V.send, pb, S);
+      st_word(own, pb, S, w0);
+      if (gl < 7) {
+        w1 = ld_word(V.send, pb + 8, S);
+        st_word(own, pb + 8, S, w1);
+      }
     }
-    for (int q = 0; q < P.nranks; ++q)
-      if (q != V.rank)
-        asm volatile("st.volatile.global.v2.u64 [%0], {%1, %2};" ::"l"(P.peer_stage[q] + mine + 128 * l + 16 * gl),
-                     "l"(w0), "l"(w1)
-                     : "memory");
+    __syncwarp();
+    if (valid)
+      for (int q = 0; q < P.nranks; ++q)
+        if (q != V.rank)
+          asm volatile("st.volatile.global.v2.u64 [%0], {%1, %2};" ::"l"(P.peer_stage[q] + mine + 128 * l + 16 * gl),
+                       "l"(w0), "l"(w1)
+                       : "memory");
   }
   // 2. every other root's lines: warp-uniform, 4 lines per warp step
   const unsigned long long t0 = globaltimer();

@@ -387,6 +387,8 @@ def test_twohop_reductions(dev, base, dtype, mib, offset):
     ("allgather", 4096 + 1, {}, "oneshot"),  # partial last payload word
     ("allgather", 3 * 65536, {"oneshot_ag_max": 0}, "ll128"),
     ("allgather", 3 * 65536 + 1, {"proto": 0}, "flags"),
+    ("allgather", 3 * 65536 + 1, {"oneshot_ag_max": 0}, "ll128"),  # partial last words
+    ("reduce_scatter", 98304 + 3, {}, "ll128"),
     ("reduce_scatter", 2000, {}, "oneshot"),
     ("reduce_scatter", 98304, {}, "twohop"),
     ("reduce_scatter", 98304 + 3, {"proto": 0}, "flags"),
@@ -417,5 +419,44 @@ def test_no_writes_outside_the_output(dev, coll, S, opts, want):
     assert comm.last_call_info()["proto"] == want, comm.last_call_info()
     for b in bigs:
         assert torch.all(b[:G] == -12345.0) and torch.all(b[G + out_n:] == -12345.0)
+    _assert_exact(s, coll, ins, outs, "float32")
+    comm.close()
+
+
+# ---------------------------------------------------------------------------
+# LL128 at any length: slices that are not a multiple of 8 bytes (odd counts,
+# k > 1 splits at odd offsets) end in a partial payload word
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("base", ["nvs4", "groups300", "fig3a"])
+@pytest.mark.parametrize("coll", ["allgather", "reduce_scatter", "allreduce"])
+@pytest.mark.parametrize("S", [1, 3, 61, 1001, 65537])
+@pytest.mark.parametrize("dtype", ["float32", "bfloat16"])
+def test_ll128_odd_lengths(dev, base, coll, S, dtype):
+    comm, s = _comm(f"{base}_{coll}", proto=1)
+    ins, outs = _run(comm, coll, S, dtype, dev, seed=S * 3 + len(base))
+    assert comm.last_call_info()["proto"] == "ll128", comm.last_call_info()
+    _assert_exact(s, coll, ins, outs, dtype)
+    comm.close()
+
+
+@pytest.mark.parametrize("coll,op,dtype", [("reduce_scatter", "avg", "bfloat16"),
+                                           ("allreduce", "avg", "float32"),
+                                           ("allreduce", "sum", "int32")])
+@pytest.mark.parametrize("offset", [0, 1])
+def test_ll128_odd_lengths_production_width(dev, coll, op, dtype, offset):
+    """4-warp LL128 workers, unaligned views, AVG and int32 at odd lengths."""
+    comm, s = _comm(f"groups300_{coll}", proto=1, ll_worker_warps=4)
+    ins, outs = _run(comm, coll, 4097, dtype, dev, seed=11 + offset, op=op, offset=offset)
+    assert comm.last_call_info()["proto"] == "ll128"
+    _assert_exact(s, coll, ins, outs, dtype, op=op)
+    comm.close()
+
+
+@pytest.mark.parametrize("coll", ["allgather", "reduce_scatter", "allreduce"])
+def test_odd_lengths_take_ll128_automatically(dev, coll):
+    """An odd count no longer falls through to the chunk-flag protocol."""
+    comm, s = _comm(f"groups300_{coll}")
+    ins, outs = _run(comm, coll, 3 * 65536 + 1, "float32", dev, seed=5)
+    assert comm.last_call_info()["proto"] == "ll128", comm.last_call_info()
     _assert_exact(s, coll, ins, outs, "float32")
     comm.close()
