@@ -38,7 +38,8 @@ def main():
         comm.set_option("proto", proto)
         comm.set_option("chunk_max", rng.choice([16 << 10, 64 << 10, 256 << 10]))
         # up to the copy-engine (N=2, >= 24 MiB output) and two-hop (2-12 MiB) ranges
-        S = rng.choice([1, 17, 256, 4096, 65536 + 8, 1 << 18, 1 << 20, (1 << 21) - 4, 1 << 22])
+        S = rng.choice([1, 17, 256, 4096, 4097, 65536 + 8, 1 << 18, (1 << 18) + 3, 1 << 20, (1 << 21) - 4,
+                        (1 << 21) + 1, 1 << 22])
         g = torch.Generator().manual_seed(it)
         if coll == "allgather":
             allin = torch.randint(-2**31, 2**31 - 1, (n, S), generator=g, dtype=torch.int32)
