@@ -387,7 +387,7 @@ def test_twohop_reductions(dev, base, dtype, mib, offset):
     ("allgather", 4096 + 1, {}, "oneshot"),  # partial last payload word
     ("allgather", 3 * 65536, {"oneshot_ag_max": 0}, "ll128"),
     ("allgather", 3 * 65536 + 1, {"proto": 0}, "flags"),
-    ("allgather", 3 * 65536 + 1, {"oneshot_ag_max": 0}, "ll128"),  # partial last words
+    ("allgather", 3 * 65536 + 1, {"proto": 1}, "ll128"),  # partial last payload words
     ("reduce_scatter", 98304 + 3, {}, "ll128"),
     ("reduce_scatter", 2000, {}, "oneshot"),
     ("reduce_scatter", 98304, {}, "twohop"),
@@ -452,11 +452,14 @@ def test_ll128_odd_lengths_production_width(dev, coll, op, dtype, offset):
     comm.close()
 
 
-@pytest.mark.parametrize("coll", ["allgather", "reduce_scatter", "allreduce"])
-def test_odd_lengths_take_ll128_automatically(dev, coll):
-    """An odd count no longer falls through to the chunk-flag protocol."""
+@pytest.mark.parametrize("coll,want", [("allgather", "flags"), ("reduce_scatter", "ll128"),
+                                       ("allreduce", "ll128")])
+def test_odd_lengths_automatic_protocol(dev, coll, want):
+    """Odd-count reductions take LL128 (they used to fall through to chunk
+    flags); an unaligned allgather above the one-hop range keeps chunk flags,
+    which move it faster than the byte-granular LL128 loops."""
     comm, s = _comm(f"groups300_{coll}")
     ins, outs = _run(comm, coll, 3 * 65536 + 1, "float32", dev, seed=5)
-    assert comm.last_call_info()["proto"] == "ll128", comm.last_call_info()
+    assert comm.last_call_info()["proto"] == want, comm.last_call_info()
     _assert_exact(s, coll, ins, outs, "float32")
     comm.close()

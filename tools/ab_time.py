@@ -2,7 +2,8 @@
 for a list of (collective, MiB, dtype, proto) points.  Uses only the API
 present in every round, so it runs in old checkouts too.
 
-    torchrun --nproc-per-node N tools/ab_time.py ag:64:f32:-1 ar:25:bf16:-1 ...
+    torchrun --nproc-per-node N tools/ab_time.py ag:64:f32:-1 ar:25:bf16:-1 ar:25+1:bf16:-1 ...
+(MiB+k: k extra elements per shard / buffer, for odd counts)
 """
 import os
 import sys
@@ -50,9 +51,10 @@ def main():
                 comm.set_option(k, int(v))
             except Exception:  # noqa: BLE001
                 pass
-        M = int(mib) * MIB
+        mib, _, extra = mib.partition("+")  # "25+1": 25 MiB plus one element (odd counts)
         dt = DT[dt]
         es = torch.tensor([], dtype=dt).element_size()
+        M = int(mib) * MIB + int(extra or 0) * es * (1 if coll == "ar" else n)
         comm.set_option("proto", int(proto))
         if coll == "ag":
             S = M // n // es
