@@ -630,16 +630,16 @@ int run(fc_comm* c, int coll, const void* const* sends, void* const* recvs, size
   long long n = 0, W = 0;
   if (c->proto != 0) {
     // any slice length and offset works: a slice that is not a multiple of 8
-    // bytes ends in a partial payload word (run_item_ll).  Unaligned slices
-    // take the byte-granular copy loops, so automatic selection keeps them for
-    // reductions only, where they beat the chunk flags (N=4: allreduce 25 MiB
-    // + 1 element 317 vs 216 GB/s, reduce-scatter 256 MiB + 1 585 vs 376);
-    // an unaligned allgather above the one-hop range runs faster on chunk
-    // flags (64 MiB + 1: 537 vs 473)
-    bool aligned = (stride * es) % 8 == 0;  // slice offsets: rank-uniform
+    // bytes ends in a partial payload word (run_item_ll), and 4-byte aligned
+    // slices keep batched 4-byte accesses.  Measured at N=4 against the chunk
+    // flags: allreduce bf16 25 MiB + 1 element 317 vs 216 GB/s, reduce-scatter
+    // fp32 256 MiB + 1 738 vs 376, allgather fp32 64 MiB + 1 622 vs 536.
+    // Allgathers whose slices are not even 4-byte aligned (odd 2-byte counts)
+    // would run the byte-granular loops and keep the chunk flags.
+    bool aligned = (stride * es) % 4 == 0;  // slice offsets: rank-uniform
     for (int r = 0; r < N && aligned; ++r) {
       long long Sr = std::max(0LL, std::min(S, total - (long long)r * stride));
-      for (int m = 0; m <= pl.k && aligned; ++m) aligned = ((Sr * m / pl.k) * es) % 8 == 0;
+      for (int m = 0; m <= pl.k && aligned; ++m) aligned = ((Sr * m / pl.k) * es) % 4 == 0;
     }
     aligned = aligned || coll != FC_ALLGATHER || c->proto == 1;
     const long long unit_lines = (slice_unit + 119) / 120;

@@ -888,15 +888,21 @@ __device__ void run_item_ll(const FcParams& P, int me, FcCtl* ctl, const int* T,
   if (kind == FC_K_AG_ROOT && !P.root_local_done && P.recv[me] + lo != P.send[me] + (lo - base))
     out_local = P.recv[me];
   if (kind == FC_K_RS_ROOT) out_local = P.recv[me] - base;  // out has S elements
-  // payload offsets (pay + 8*q0) are lo plus multiples of 8: the base
-  // pointers at lo decide whether 8-byte vector accesses apply (warp-uniform)
-  const bool src_al = ((uintptr_t)(local_src + lo) & 7) == 0;
-  const bool out_al = ((uintptr_t)(out_local + lo) & 7) == 0;
+  // payload offsets (pay + 8*q0) are lo plus multiples of 8: the local
+  // buffers' alignment at lo (8, 4 or any) picks the access width
+  // (warp-uniform)
+  auto acls = [&](const char* b) -> int {
+    if (!b) return 8;
+    const uintptr_t a = (uintptr_t)(b + lo);
+    return (a & 7) == 0 ? 8 : ((a & 3) == 0 ? 4 : 1);
+  };
+  const int align = min(acls(local_src), acls(out_local));
 
-  // the line loop, instantiated for 8-byte aligned local buffers (plain
-  // vector accesses, all loads of a batch in flight) and for any alignment
+  // the line loop, instantiated per alignment class: 8 (one 8-byte access),
+  // 4 (two 4-byte accesses; odd fp32 counts, offset views) -- both without
+  // branches, so all loads of a batch are in flight together -- and any
   auto lines = [&](auto aligned) -> bool {
-    constexpr bool AL = decltype(aligned)::value;
+    constexpr int AL = decltype(aligned)::value;
     for (long long lb = l0 + 4LL * U * wl; lb < l1; lb += 4LL * U * WW) {
       bool valid[U], v0[U], v1[U];
       long long pay[U];
@@ -928,9 +934,13 @@ __device__ void run_item_ll(const FcParams& P, int me, FcCtl* ctl, const int* T,
   #pragma unroll
         for (int u = 0; u < U; ++u) {
           const char* src = local_src + pay[u] + 8 * q0;  // rank-local buffer, any alignment
-          if constexpr (AL) {  // aligned bases: every line's loads in flight together
+          if constexpr (AL == 8) {  // aligned bases: every line's loads in flight together
             if (v0[u]) w0[u] = __ldcg(reinterpret_cast<const unsigned long long*>(src));
             if (v1[u]) w1[u] = __ldcg(reinterpret_cast<const unsigned long long*>(src) + 1);
+          } else if constexpr (AL == 4) {
+            const unsigned* q = reinterpret_cast<const unsigned*>(src);
+            if (v0[u]) w0[u] = (unsigned long long)__ldcg(q) | ((unsigned long long)__ldcg(q + 1) << 32);
+            if (v1[u]) w1[u] = (unsigned long long)__ldcg(q + 2) | ((unsigned long long)__ldcg(q + 3) << 32);
           } else {
             if (v0[u]) w0[u] = ld_u64_any(src);
             if (v1[u]) w1[u] = ld_u64_any(src + 8);
@@ -979,9 +989,19 @@ __device__ void run_item_ll(const FcParams& P, int me, FcCtl* ctl, const int* T,
   #pragma unroll
         for (int u = 0; u < U; ++u) {
           char* o = out_local + pay[u] + 8 * q0;
-          if constexpr (AL) {
+          if constexpr (AL == 8) {
             if (v0[u]) reinterpret_cast<unsigned long long*>(o)[0] = w0[u];
             if (v1[u]) reinterpret_cast<unsigned long long*>(o)[1] = w1[u];
+          } else if constexpr (AL == 4) {
+            unsigned* q = reinterpret_cast<unsigned*>(o);
+            if (v0[u]) {
+              q[0] = (unsigned)w0[u];
+              q[1] = (unsigned)(w0[u] >> 32);
+            }
+            if (v1[u]) {
+              q[2] = (unsigned)w1[u];
+              q[3] = (unsigned)(w1[u] >> 32);
+            }
           } else {
             if (v0[u]) st_u64_any(o, w0[u]);
             if (v1[u]) st_u64_any(o + 8, w1[u]);
@@ -1016,7 +1036,9 @@ __device__ void run_item_ll(const FcParams& P, int me, FcCtl* ctl, const int* T,
     }
     return true;
   };
-  const bool ok = (src_al && out_al) ? lines(std::true_type{}) : lines(std::false_type{});
+  const bool ok = align == 8   ? lines(std::integral_constant<int, 8>{})
+                  : align == 4 ? lines(std::integral_constant<int, 4>{})
+                               : lines(std::integral_constant<int, 1>{});
   if (!ok) return;
   if (P.trace && leader) {  // 128-byte lines of this chunk to every peer destination
     int remote = 0;

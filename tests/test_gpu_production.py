@@ -452,14 +452,17 @@ def test_ll128_odd_lengths_production_width(dev, coll, op, dtype, offset):
     comm.close()
 
 
-@pytest.mark.parametrize("coll,want", [("allgather", "flags"), ("reduce_scatter", "ll128"),
-                                       ("allreduce", "ll128")])
-def test_odd_lengths_automatic_protocol(dev, coll, want):
-    """Odd-count reductions take LL128 (they used to fall through to chunk
-    flags); an unaligned allgather above the one-hop range keeps chunk flags,
-    which move it faster than the byte-granular LL128 loops."""
+@pytest.mark.parametrize("coll,dtype,want", [("allgather", "float32", "ll128"),
+                                             ("allgather", "bfloat16", "flags"),
+                                             ("reduce_scatter", "float32", "ll128"),
+                                             ("reduce_scatter", "bfloat16", "ll128"),
+                                             ("allreduce", "float32", "ll128")])
+def test_odd_lengths_automatic_protocol(dev, coll, dtype, want):
+    """Odd counts take LL128 (they used to fall through to chunk flags),
+    except an allgather whose slices are not even 4-byte aligned (odd 2-byte
+    counts), which the chunk flags move faster than LL128's byte loops."""
     comm, s = _comm(f"groups300_{coll}")
-    ins, outs = _run(comm, coll, 3 * 65536 + 1, "float32", dev, seed=5)
+    ins, outs = _run(comm, coll, 3 * 65536 + 1, dtype, dev, seed=5)
     assert comm.last_call_info()["proto"] == want, comm.last_call_info()
-    _assert_exact(s, coll, ins, outs, "float32")
+    _assert_exact(s, coll, ins, outs, dtype)
     comm.close()

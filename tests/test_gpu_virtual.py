@@ -47,9 +47,9 @@ def _comm(s, proto="auto", **kw):
 
 
 PROTOS = ["auto", "flags"]  # auto: one-hop / one-shot (single-switch forests), else LL128
-# (reductions at any length, odd counts ending in a partial payload word;
-# allgathers with 8-byte aligned slices); the forest LL128 path at production
-# widths is pinned in test_gpu_production.py
+# (odd counts end in a partial payload word; allgathers need 4-byte aligned
+# slices); the forest LL128 path at production widths is pinned in
+# test_gpu_production.py
 
 
 @pytest.mark.parametrize("proto", PROTOS)
